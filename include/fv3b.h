@@ -1,0 +1,92 @@
+/*
+ * fv3b.h — C ABI of the B200 FV3 dycore engine (libfv3b.so).
+ *
+ * This is the boundary below the Python drop-in for the reference engine
+ * slot.  The reference declares, but does not ship, the engine modules
+ * `stencilkit.executor.scheduled` (run_scheduled / benchmark / TimingStats /
+ * BenchmarkResult / timings_to_csv) and `stencilkit.executor.bandwidth`
+ * (measure_bandwidth)  — reference pkg/src/stencilkit/executor/__init__.py:6-13,
+ * contracts SPEC.md:366-427 — and its executing engine is
+ * `run_reference(program, inputs, domain, placement)` (executor/reference.py:307-339).
+ * Each entry point below executes one shipped stencil program (or one fused
+ * group of its stencils) with exactly the semantics of run_reference on that
+ * program; the Python layer (paper_2205_04148_b200.executor) binds them with
+ * ctypes.  A ctypes binding is the reference-side integration: see
+ * INTEGRATION.md.
+ *
+ * Conventions
+ *  - All arithmetic is IEEE fp64, no FMA contraction (built with -fmad=false),
+ *    statement order and association as in the .stn source.
+ *  - Fields are borrowed device pointers in the reference Layout
+ *    (scheduling.py:323-407): I unit-stride, rows padded, strides in
+ *    elements.  `data` is the address of the first allocated element;
+ *    the interior origin is data + sum(halo_lo[a] * stride[a]).
+ *  - Every 3-D field passed to one call must share strides; 2-D fields share
+ *    the J stride.  Output fields must not alias inputs (the reference
+ *    materialises every right-hand side before its store, reference.py:10-12).
+ *  - Status 0 = OK.  Negative = error; fv3b_last_error() has the message.
+ *    No exceptions or aborts cross the ABI; no implicit synchronisation:
+ *    work is enqueued on `stream` (a cudaStream_t, NULL = legacy default).
+ *  - Reentrant; callable from any host thread; one process per GPU.
+ */
+#ifndef FV3B_H
+#define FV3B_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FV3B_ABI_VERSION 1
+
+enum {
+  FV3B_OK = 0,
+  FV3B_EINVAL = -1,   /* bad argument count / null pointer */
+  FV3B_ELAYOUT = -2,  /* stride, halo or alignment mismatch */
+  FV3B_EDOMAIN = -3,  /* domain below the program minimum */
+  FV3B_ELAUNCH = -4,  /* CUDA launch or runtime error */
+};
+
+/* One borrowed field view.  rank = number of declared axes (3 for I,J,K,
+ * 2 for I,J, 1 for K).  Axes are in I, J, K order, I unit-stride. */
+typedef struct {
+  double* data;
+  int64_t stride[3];
+  int32_t shape[3];
+  int32_t halo_lo[3];
+  int32_t rank;
+} fv3b_field;
+
+/* Compute domain and edge ownership (== RankPlacement, ir/graph.py:226-239):
+ * horizontal regions anchored on an edge fire only when it is owned. */
+typedef struct {
+  int32_t ni, nj, nk;
+  uint8_t own_i_start, own_i_end, own_j_start, own_j_end;
+} fv3b_domain;
+
+int fv3b_abi_version(void);
+const char* fv3b_last_error(void);
+
+/* K0  copy.stn — `out = inp` over the interior (PAPER.md:589 copy stencil).
+ *     fields: inp, out.  scalars: none. */
+int fv3b_copy(const fv3b_field* f, int nf, const double* s, int ns,
+              const fv3b_domain* d, void* stream);
+
+/* K1  fv_tp_2d.stn — FV3 fv_tp_2d (x/y PPM fluxes + inner updates) and the
+ *     flux-form update of q.  fields: q, crx, cry, xfx, yfx (3-D),
+ *     area, rarea (2-D), q_out (3-D).  scalars: ppm_p1, ppm_p2. */
+int fv3b_fv_tp_2d(const fv3b_field* f, int nf, const double* s, int ns,
+                  const fv3b_domain* d, void* stream);
+
+/* K7  tracer_2d.stn — nq tracers advected with accumulated Courant numbers
+ *     and mass fluxes, batched in one launch.  fields: cx, cy, xfx, yfx, mfx,
+ *     mfy, dp1 (3-D), area, rarea (2-D), then q_in[0..nq), q_out[0..nq).
+ *     scalars: ppm_p1, ppm_p2. */
+int fv3b_tracer_2d(const fv3b_field* f, int nf, const double* s, int ns,
+                   const fv3b_domain* d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FV3B_H */

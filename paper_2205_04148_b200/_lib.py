@@ -1,0 +1,86 @@
+"""ctypes binding of ``libfv3b.so`` (declared in ``include/fv3b.h``).
+
+There is no CPU fallback: if the library is missing or cannot be loaded the
+import of the engine fails loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_PATH = Path(os.environ.get("FV3B_LIB", Path(__file__).resolve().parent / "libfv3b.so"))
+
+ABI_VERSION = 1
+
+
+class Field(ctypes.Structure):
+    """``fv3b_field``."""
+
+    _fields_ = [
+        ("data", ctypes.c_void_p),
+        ("stride", ctypes.c_int64 * 3),
+        ("shape", ctypes.c_int32 * 3),
+        ("halo_lo", ctypes.c_int32 * 3),
+        ("rank", ctypes.c_int32),
+    ]
+
+
+class Domain(ctypes.Structure):
+    """``fv3b_domain`` (== ``RankPlacement`` + sizes)."""
+
+    _fields_ = [
+        ("ni", ctypes.c_int32),
+        ("nj", ctypes.c_int32),
+        ("nk", ctypes.c_int32),
+        ("own_i_start", ctypes.c_uint8),
+        ("own_i_end", ctypes.c_uint8),
+        ("own_j_start", ctypes.c_uint8),
+        ("own_j_end", ctypes.c_uint8),
+    ]
+
+
+class Fv3bError(RuntimeError):
+    def __init__(self, fn: str, code: int, msg: str):
+        super().__init__(f"{fn} failed with status {code}: {msg}")
+        self.code = code
+
+
+_ENTRY_SIG = [ctypes.POINTER(Field), ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+              ctypes.POINTER(Domain), ctypes.c_void_p]
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(the B200 engine has no CPU fallback)"
+            )
+        h = ctypes.CDLL(str(LIB_PATH))
+        h.fv3b_abi_version.restype = ctypes.c_int
+        h.fv3b_last_error.restype = ctypes.c_char_p
+        if h.fv3b_abi_version() != ABI_VERSION:
+            raise ImportError(f"libfv3b ABI {h.fv3b_abi_version()} != expected {ABI_VERSION}")
+        _lib = h
+    return _lib
+
+
+def entry(name: str):
+    fn = getattr(lib(), name)
+    fn.restype = ctypes.c_int
+    fn.argtypes = _ENTRY_SIG
+    return fn
+
+
+def call(name: str, fields: list[Field], scalars: list[float], domain: Domain, stream: int) -> None:
+    fn = entry(name)
+    farr = (Field * len(fields))(*fields)
+    sarr = (ctypes.c_double * max(1, len(scalars)))(*scalars)
+    rc = fn(farr, len(fields), sarr, len(scalars), ctypes.byref(domain), ctypes.c_void_p(stream))
+    if rc != 0:
+        raise Fv3bError(name, rc, lib().fv3b_last_error().decode())

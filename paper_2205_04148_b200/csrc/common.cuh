@@ -1,0 +1,55 @@
+// Shared helpers for the fv3b kernels: ABI argument checking, error state,
+// device views.  See include/fv3b.h for the ABI contract.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdint.h>
+
+#include "../../include/fv3b.h"
+
+namespace fv3b {
+
+// Sets the thread-local error text and returns `code`.
+int fail(int code, const char* fmt, ...);
+
+// Device-side view of a field: interior-origin pointer + J/K strides
+// (I is unit stride).  For 2-D (I,J) fields sk == 0.
+struct View {
+  double* o;
+  int64_t sj, sk;
+  __device__ __forceinline__ double& operator()(int i, int j, int k) const { return o[i + j * sj + k * sk]; }
+  __device__ __forceinline__ double* ptr(int i, int j, int k) const { return o + i + j * sj + k * sk; }
+};
+
+struct Halo {
+  int ilo, ihi, jlo, jhi, klo, khi;  // allocated halo widths
+};
+
+// Validate one field and produce its view.  `rank` 3 = IJK, 2 = IJ, 1 = K.
+// Checks unit I stride, non-null data and that the allocation covers
+// `need` (lo/hi halo widths per axis) around the domain.
+int view_of(const fv3b_field& f, int rank, const fv3b_domain& d, const Halo& need, const char* name, View* out);
+
+// All 3-D views must share strides (one tile geometry per launch).
+int same_strides(const View* v, int n, const char* what);
+
+int check_launch(const char* what);
+
+inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// Tile-local shared-memory array covering [i0, i1) x [j0, j1) (tile coords).
+struct STile {
+  double* p;
+  int i0, j0, w;
+  __device__ __forceinline__ double& operator()(int i, int j) const { return p[(j - j0) * w + (i - i0)]; }
+};
+
+}  // namespace fv3b
+
+#define FV3B_TRY(expr)        \
+  do {                        \
+    int _rc = (expr);         \
+    if (_rc != FV3B_OK) return _rc; \
+  } while (0)

@@ -1,0 +1,129 @@
+"""Kernel plans: how each shipped program's driver trace maps onto libfv3b
+launches.
+
+A plan is the hand-written counterpart of one ``.stn`` program: it checks
+that the resolved driver trace is the one its fused kernels implement,
+binds the program's fields and scalars to the entry point's fixed argument
+order (``include/fv3b.h``) and enqueues the launches.  Written
+non-temporaries go to separate output buffers (the reference materialises
+each right-hand side before storing it, ``reference.py:10-12``), which the
+caller seeds with the input values so untouched halo cells are returned as
+provided (``reference.py:335-339``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable
+
+import torch
+
+from .. import _lib
+from ..device import Grid
+from ..program import Program
+
+
+@dataclass
+class LaunchCtx:
+    grid: Grid
+    fields: dict[str, torch.Tensor]        # current (input) buffers, by field name
+    outputs: dict[str, torch.Tensor]       # output buffers of written fields
+    placement: tuple
+    stream: int
+    nk: int                                # program vertical domain
+    on_launch: Callable | None = None      # (node, start_event, end_event) timing hook
+    launches: list = field(default_factory=list)
+
+    def f(self, name: str, rank: int | None = None) -> _lib.Field:
+        return self.grid.abi(self.fields[name], rank)
+
+    def o(self, name: str) -> _lib.Field:
+        return self.grid.abi(self.outputs[name])
+
+    def call(self, node: str, entry: str, fields: list, scalars: list[float], nk: int | None = None) -> None:
+        dom = self.grid.domain(self.placement, nk=self.nk if nk is None else nk)
+        if self.on_launch is not None:
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            _lib.call(entry, fields, scalars, dom, self.stream)
+            e.record()
+            self.on_launch(node, s, e)
+        else:
+            _lib.call(entry, fields, scalars, dom, self.stream)
+        self.launches.append(node)
+
+
+class Plan:
+    name: str = ""
+    stencils: tuple[str, ...] = ()   # expected resolved trace (stencil names)
+
+    def written(self, prog: Program) -> list[str]:
+        out = []
+        for s in prog.canon["stencils"]:
+            for b in s["blocks"]:
+                for st in b["statements"]:
+                    t = st["target"]
+                    if not prog.fields[t].temporary and t not in out:
+                        out.append(t)
+        return out
+
+    def check_trace(self, trace) -> None:
+        names = tuple(s for s, _ in trace)
+        if names != self.stencils:
+            raise NotImplementedError(
+                f"{self.name}: the B200 plan implements the trace {self.stencils}, got {names}")
+
+    def run(self, prog: Program, ctx: LaunchCtx) -> None:
+        raise NotImplementedError
+
+
+class CopyPlan(Plan):
+    name = "copy"
+    stencils = ("copy_field",)
+
+    def run(self, prog, ctx):
+        ctx.call("copy_field_0", "fv3b_copy", [ctx.f("inp"), ctx.o("out")], [])
+
+
+class FvTp2dPlan(Plan):
+    name = "fv_tp_2d"
+    stencils = ("fv_tp_2d",)
+
+    def run(self, prog, ctx):
+        (stencil, kw), = prog.trace
+        s = prog.scalars(kw)
+        ctx.call("fv_tp_2d_0", "fv3b_fv_tp_2d",
+                 [ctx.f("q"), ctx.f("crx"), ctx.f("cry"), ctx.f("xfx"), ctx.f("yfx"),
+                  ctx.f("area", 2), ctx.f("rarea", 2), ctx.o("q")],
+                 [s["ppm_p1"], s["ppm_p2"]])
+
+
+class Tracer2dPlan(Plan):
+    name = "tracer_2d"
+
+    def check_trace(self, trace):
+        names = [s for s, _ in trace]
+        nq = len(names) - 1
+        if names != ["tracer_dp"] + [f"tracer_q{n}" for n in range(nq)] or not 1 <= nq <= 16:
+            raise NotImplementedError(f"tracer_2d: unsupported trace {names}")
+
+    def run(self, prog, ctx):
+        trace = prog.trace
+        nq = len(trace) - 1
+        s = prog.scalars(trace[1][1])
+        fields = [ctx.f(n) for n in ("cx", "cy", "xfx", "yfx", "mfx", "mfy", "dp1")]
+        fields += [ctx.f("area", 2), ctx.f("rarea", 2)]
+        fields += [ctx.f(f"q{n}") for n in range(nq)] + [ctx.o(f"q{n}") for n in range(nq)]
+        ctx.call("tracer_2d_0", "fv3b_tracer_2d", fields, [s["ppm_p1"], s["ppm_p2"]])
+
+
+PLANS: dict[str, Plan] = {p.name: p for p in (CopyPlan(), FvTp2dPlan(), Tracer2dPlan())}
+
+
+def plan_for(prog: Program) -> Plan:
+    if prog.name not in PLANS:
+        raise KeyError(f"no B200 plan for program {prog.name!r}")
+    plan = PLANS[prog.name]
+    plan.check_trace(prog.trace)
+    return plan

@@ -1,0 +1,97 @@
+"""GPU parity: the CUDA path through the C-ABI vs the oracle and the
+reference-generated golden fixtures (bitwise: no ``**``/``log``/``exp`` in
+these programs and the library is built with ``-fmad=false``)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from helpers import assert_outputs_equal, golden_cases, load_golden
+from oracle import interp
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def engine():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2205_04148_b200 import executor
+
+    return executor
+
+
+@pytest.mark.parametrize("key,meta", list(golden_cases()))
+def test_cuda_matches_reference_golden(engine, key, meta):
+    inputs, ref_out = load_golden(key)
+    got = engine.run_b200(meta["program"], inputs, meta["domain"], placement=meta["placement"])
+    assert_outputs_equal(got, ref_out)
+
+
+CASES = [
+    ("copy", (48, 48, 16), False, 1),
+    ("copy", (33, 17, 5), True, 2),
+    ("fv_tp_2d", (48, 48, 16), False, 3),
+    ("fv_tp_2d", (37, 21, 4), True, 4),
+    ("fv_tp_2d", (64, 16, 3), False, 5),
+    ("tracer_2d", (48, 48, 6), False, 6),
+    ("tracer_2d", (35, 29, 3), True, 7),
+]
+
+
+@pytest.mark.parametrize("name,domain,tile,seed", CASES)
+def test_cuda_matches_oracle(engine, name, domain, tile, seed):
+    from paper_2205_04148_b200.inputs import synthetic_inputs
+
+    inputs = synthetic_inputs(name, domain, seed)
+    placement = (tile,) * 4
+    got = engine.run_b200(name, inputs, domain, placement=placement)
+    ref = interp.run_program(name, inputs, domain, interp.Placement(*placement))
+    assert_outputs_equal(got, ref)
+
+
+def test_cuda_fv_tp_2d_full_size_c2(engine):
+    """192x192x80 (C2) against the oracle, bitwise."""
+    from paper_2205_04148_b200.inputs import synthetic_inputs
+
+    domain = (192, 192, 80)
+    inputs = synthetic_inputs("fv_tp_2d", domain, 2205)
+    got = engine.run_b200("fv_tp_2d", inputs, domain, placement=(False,) * 4)
+    ref = interp.run_program("fv_tp_2d", inputs, domain, interp.PERIODIC)
+    assert_outputs_equal(got, ref)
+
+
+def test_shape_error_and_unknown_program(engine):
+    from paper_2205_04148_b200.inputs import synthetic_inputs
+
+    inputs = synthetic_inputs("fv_tp_2d", (16, 16, 2), 1)
+    inputs["crx"] = inputs["crx"][:, :-1]
+    with pytest.raises(ValueError, match="has shape"):
+        engine.run_b200("fv_tp_2d", inputs, (16, 16, 2))
+    with pytest.raises(KeyError):
+        engine.run_b200("no_such_program", {}, (16, 16, 2))
+    with pytest.raises(ValueError, match="below the program minimum"):
+        engine.run_b200("fv_tp_2d", {}, (8, 8, 2))
+
+
+def test_timing_api(engine):
+    from paper_2205_04148_b200.inputs import synthetic_inputs
+
+    inputs = synthetic_inputs("fv_tp_2d", (64, 64, 8), 1)
+    res = engine.benchmark("fv_tp_2d", inputs, (64, 64, 8), reps=10)
+    assert res.invocations["fv_tp_2d_0"] == 1
+    st = res.kernels["fv_tp_2d_0"]
+    assert st.reps == 10 and st.min <= st.median
+    csv = engine.timings_to_csv(res)
+    assert csv.startswith("kernel,invocations,median_s,min_s\n")
+    out, stats = engine.run_scheduled("fv_tp_2d", inputs, (64, 64, 8), workers=4)
+    assert "fv_tp_2d_0" in stats
+    with pytest.raises(ValueError):
+        engine.run_scheduled("fv_tp_2d", inputs, (64, 64, 8), workers=0)
+
+
+def test_measure_bandwidth(engine):
+    bw = engine.measure_bandwidth()
+    assert bw > 3.0e12, f"copy-stencil bandwidth {bw / 1e9:.0f} GB/s"
