@@ -86,6 +86,19 @@ int fv3b_fv_tp_2d(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_tracer_2d(const fv3b_field* f, int nf, const double* s, int ns,
                    const fv3b_domain* d, void* stream);
 
+/* K4  riem_solver_c.stn — semi-implicit vertical acoustic solve per column.
+ *     Program domain nk = interface levels (layers + 1).  fields: dm, pt, w
+ *     (layers), gz (interfaces), ws (2-D), pef, gz_out (interfaces; gz_out
+ *     may alias gz).  scalars: ptop, rdgas, grav, gama, p_fac, dt. */
+int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, int ns,
+                       const fv3b_domain* d, void* stream);
+
+/* K5  remap_profile.stn / remap_tracers.stn — PPM edge solve + limited
+ *     sub-grid coefficients.  Program domain nk = interface levels.
+ *     fields: delp, then per tracer: q, a4_2, a4_3, a4_4.  scalars: none. */
+int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns,
+                       const fv3b_domain* d, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,3 +64,74 @@ int check_launch(const char* what) {
 extern "C" int fv3b_abi_version(void) { return FV3B_ABI_VERSION; }
 
 extern "C" const char* fv3b_last_error(void) { return fv3b::g_err.c_str(); }
+
+// ---------------------------------------------------------------------------
+// TMA tensor maps (driver entry point fetched through the runtime, so the
+// library does not link libcuda directly).  Cached by geometry + pointer.
+// ---------------------------------------------------------------------------
+#include <cudaTypedefs.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "tma.cuh"
+
+namespace fv3b {
+
+int tensor_map(const double* base, int64_t pitch, int64_t rows, int64_t levels, int bw, int bh, CUtensorMap* out) {
+  using Key = std::tuple<const void*, int64_t, int64_t, int64_t, int, int>;
+  static std::mutex mu;
+  static std::map<Key, CUtensorMap> cache;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  const Key key{base, pitch, rows, levels, bw, bh};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return FV3B_OK;
+  }
+  if (encode == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr)
+      return fail(FV3B_ELAUNCH, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (((uintptr_t)base) % 16 != 0 || (pitch * 8) % 16 != 0)
+    return fail(FV3B_ELAYOUT, "TMA needs 16-B aligned base and row pitch (pitch=%lld)", (long long)pitch);
+  cuuint64_t dims[3] = {(cuuint64_t)pitch, (cuuint64_t)rows, (cuuint64_t)levels};
+  cuuint64_t strides[2] = {(cuuint64_t)(pitch * 8), (cuuint64_t)(pitch * rows * 8)};
+  cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FV3B_ELAYOUT, "cuTensorMapEncodeTiled failed (%d) box %dx%d", (int)r, bw, bh);
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = *out;
+  return FV3B_OK;
+}
+
+int geo_of(const fv3b_field& f, Geo* g) {
+  if (f.rank == 3) {
+    if (f.stride[0] != 1 || f.stride[2] != f.stride[1] * f.shape[1] || f.stride[1] != f.shape[0])
+      return fail(FV3B_ELAYOUT, "TMA path needs a dense (pitch, rows, levels) field layout");
+    g->pitch = f.stride[1];
+    g->rows = f.shape[1];
+    g->levels = f.shape[2];
+  } else if (f.rank == 2) {
+    if (f.stride[0] != 1 || f.stride[1] != f.shape[0]) return fail(FV3B_ELAYOUT, "TMA path needs dense 2-D fields");
+    g->pitch = f.stride[1];
+    g->rows = f.shape[1];
+    g->levels = 1;
+  } else {
+    return fail(FV3B_ELAYOUT, "TMA path needs 2-D or 3-D fields");
+  }
+  g->i0 = f.halo_lo[0];
+  g->j0 = f.halo_lo[1];
+  return FV3B_OK;
+}
+
+}  // namespace fv3b

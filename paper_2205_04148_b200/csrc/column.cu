@@ -1,0 +1,341 @@
+// K4 riem_solver_c and K5 remap_profile: vertical column solvers
+// (programs/riem_solver_c.stn, remap_profile.stn, remap_tracers.stn;
+// templates.riem_stencils / remap_stencils).
+//
+// One thread owns one column (i, j) and marches in K; consecutive threads
+// own consecutive i, so every level's loads/stores are coalesced 256-B rows
+// of the I-unit-stride Layout.  The DSL expresses each tridiagonal solve as a
+// FORWARD stencil followed by a BACKWARD stencil (validate.py:171-186); the
+// values a backward sweep consumes are staged per column in shared memory
+// (NC columns x (nk+1) levels per array) so nothing round-trips through HBM.
+// Every statement is evaluated with the .stn's operation order, so results
+// are bitwise the interpreter's except where log/exp (CUDA libdevice vs the
+// host libm) differ in the last ulp.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace fv3b {
+
+constexpr int NC = 32;  // columns per CTA (one warp)
+
+// numpy.maximum semantics (NaN-propagating, reference.py:247-257)
+__device__ __forceinline__ double np_max(double a, double b) {
+  if (isnan(a) || isnan(b)) return a + b;
+  return a > b ? a : (b > a ? b : a);
+}
+
+struct RiemArgs {
+  View dm, pt, w, gz, ws, pef, gzo;
+  int ilo, jlo, ni_ext, nj_ext;  // column range [ilo, ilo+ni_ext) x [jlo, jlo+nj_ext)
+  int nk;                        // layers; interfaces 0..nk
+  double dt, ptop, rdgas, grav, gama, p_fac;
+};
+
+// Statement-for-statement restatement of templates.riem_stencils.
+__global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
+  extern __shared__ double sm[];
+  const int nk = a.nk, L = nk + 1;
+  const int c = threadIdx.x;
+  const int i = a.ilo + (blockIdx.x * NC + c) % a.ni_ext;
+  const int cidx = blockIdx.x * NC + c;
+  if (cidx >= a.ni_ext * a.nj_ext) return;
+  const int j = a.jlo + cidx / a.ni_ext;
+  double* S0 = sm + c;               // pp, later pe2
+  double* S1 = sm + L * NC + c;      // gam -> aa -> gw -> pem
+  double* S2 = sm + 2 * L * NC + c;  // pem -> w2
+#define AT(S, k) (S)[(k) * NC]
+  const double dt = a.dt, ptop = a.ptop, rdgas = a.rdgas, grav = a.grav, gama = a.gama;
+  const double* dm = a.dm.ptr(i, j, 0);
+  const double* pt = a.pt.ptr(i, j, 0);
+  const double* w = a.w.ptr(i, j, 0);
+  const double* gz = a.gz.ptr(i, j, 0);
+  const int64_t sk = a.dm.sk;
+
+  // ---- pass A (forward): riem_pem, riem_layer, riem_coef, riem_pp_fwd ----
+  double pem0 = ptop;  // pem(k)
+  AT(S2, 0) = pem0;
+  double pe_prev = 0.0, grat_prev = 0.0, bet_prev = 0.0, pp_prev = 0.0;
+  double dm_k = dm[0];
+  for (int k = 0; k < nk; ++k) {
+    const double pem1 = pem0 + dm_k;  // pem(k+1) = pem + dm
+    AT(S2, k + 1) = pem1;
+    const double gzk = gz[k * sk], gzk1 = gz[(k + 1) * sk];
+    const double pmk = dm_k / log(pem1 / pem0);
+    const double pek = dm_k * rdgas * pt[k * sk] / (gzk - gzk1) - pmk;
+    const double dm_n = (k + 1 < nk) ? dm[(k + 1) * sk] : 0.0;
+    // layer k coefficients (riem_coef)
+    const double grat = (k < nk - 1) ? dm_k / dm_n : 0.0;
+    const double bb = (k < nk - 1) ? 2.0 * (1.0 + grat) : 2.0;
+    // interface k of riem_pp_fwd (uses layer k-1's dd, needing pe(k))
+    if (k == 0) {
+      bet_prev = bb;
+      pp_prev = 0.0;
+      AT(S0, 0) = 0.0;
+    } else {
+      const double dd_prev = (k - 1 < nk - 1) ? 3.0 * (pe_prev + grat_prev * pek) : 3.0 * pe_prev;
+      double ppk;
+      if (k == 1)
+        ppk = dd_prev / bet_prev;
+      else
+        ppk = (dd_prev - pp_prev) / bet_prev;
+      const double gam = grat_prev / bet_prev;
+      bet_prev = bb - gam;
+      pp_prev = ppk;
+      AT(S0, k) = ppk;
+      AT(S1, k) = gam;
+    }
+    pe_prev = pek;
+    grat_prev = grat;
+    pem0 = pem1;
+    dm_k = dm_n;
+  }
+  {  // interface nk: pp = (dd[nk-1] - pp[nk-1]) / bet[nk-1], dd[nk-1] = 3*pe[nk-1]
+    const double dd_prev = (nk - 1 < nk - 1) ? 0.0 : 3.0 * pe_prev;
+    AT(S0, nk) = (nk == 1) ? dd_prev / bet_prev : (dd_prev - pp_prev) / bet_prev;
+  }
+
+  // ---- pass B (backward): riem_pp_bwd, then aa (riem_w_fwd) -------------
+  const double t1g = gama * 2.0 * dt * dt;
+  {
+    double ppn = AT(S0, nk);
+    double dz_n = (gz[nk * sk] - gz[(nk - 1) * sk]) / grav;  // dz(nk-1)
+    AT(S1, nk) = t1g / dz_n * (AT(S2, nk) + ppn);            // aa(nk)
+    for (int k = nk - 1; k >= 1; --k) {
+      const double ppk = AT(S0, k) - AT(S1, k) * ppn;
+      AT(S0, k) = ppk;
+      const double dz_k = (gz[k * sk] - gz[(k - 1) * sk]) / grav;  // dz(k-1)
+      AT(S1, k) = t1g / (dz_k + dz_n) * (AT(S2, k) + ppk);        // aa(k) = t1g/(dz(k-1)+dz(k))*(pem+pp)
+      dz_n = dz_k;
+      ppn = ppk;
+    }
+  }
+
+  // ---- pass C (forward): riem_w_sweep ----------------------------------
+  const double ws = a.ws(i, j, 0);
+  {
+    double bw = 0.0, w2p = 0.0;
+    for (int l = 0; l < nk; ++l) {
+      const double dml = dm[l * sk], wl = w[l * sk];
+      const double aal = AT(S1, l), aan = AT(S1, l + 1);
+      double w2l;
+      if (l == 0) {
+        bw = dml - aan;
+        w2l = (dml * wl + dt * AT(S0, 1)) / bw;
+      } else {
+        const double gw = aal / bw;
+        bw = dml - (aal + aan + aal * gw);
+        if (l < nk - 1)
+          w2l = (dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aal * w2p) / bw;
+        else
+          w2l = (dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aan * ws - aal * w2p) / bw;
+        AT(S1, l) = gw;  // aa(l) no longer needed
+      }
+      AT(S2, l) = w2l;
+      w2p = w2l;
+    }
+  }
+
+  // ---- pass D (backward): riem_w_back ----------------------------------
+  {
+    double w2n = AT(S2, nk - 1);
+    for (int l = nk - 2; l >= 0; --l) {
+      const double w2l = AT(S2, l) - AT(S1, l + 1) * w2n;
+      AT(S2, l) = w2l;
+      w2n = w2l;
+    }
+  }
+
+  // ---- pass E (forward): riem_pe, riem_out (pem recomputed in order) -----
+  {
+    double pe2 = 0.0, pem = ptop;
+    AT(S0, 0) = 0.0;
+    AT(S1, 0) = ptop;
+    a.pef.ptr(i, j, 0)[0] = pe2 + pem;
+    for (int k = 1; k <= nk; ++k) {
+      const double dml = dm[(k - 1) * sk];
+      pe2 = pe2 + dml * (AT(S2, k - 1) - w[(k - 1) * sk]) / dt;
+      pem = pem + dml;
+      AT(S0, k) = pe2;
+      AT(S1, k) = pem;
+      a.pef.ptr(i, j, 0)[k * a.pef.sk] = pe2 + pem;
+    }
+  }
+
+  // ---- pass F (backward): riem_gz ---------------------------------------
+  {
+    double* go = a.gzo.ptr(i, j, 0);
+    const int64_t so = a.gzo.sk;
+    double gzn = gz[nk * sk];
+    go[nk * so] = gzn;
+    for (int l = nk - 1; l >= 0; --l) {
+      const double dml = dm[l * sk];
+      const double pm = dml / log(AT(S1, l + 1) / AT(S1, l));
+      const double g = gzn + dml * rdgas * pt[l * sk] / np_max(a.p_fac * pm, pm + 0.5 * (AT(S0, l) + AT(S0, l + 1)));
+      go[l * so] = g;
+      gzn = g;
+    }
+  }
+#undef AT
+}
+
+// ---------------------------------------------------------------------------
+// remap_profile (templates.remap_stencils): edge values by a tridiagonal
+// solve, then the Colella-Woodward limited PPM coefficients, fused into the
+// backward sweep (layer k needs final edges k and k+1).
+// ---------------------------------------------------------------------------
+struct RemapArgs {
+  View delp;
+  double* q[16];
+  double* a2[16];
+  double* a3[16];
+  double* a4[16];
+  int64_t sj, sk;
+  int nq, ni, nj, nk;  // nk layers (program domain nk+1)
+};
+
+__global__ void __launch_bounds__(NC) remap_kernel(const RemapArgs a) {
+  extern __shared__ double sm[];
+  const int nk = a.nk, L = nk + 1;
+  const int c = threadIdx.x;
+  const int cidx = blockIdx.x * NC + c;
+  if (cidx >= a.ni * a.nj) return;
+  const int i = cidx % a.ni, j = cidx / a.ni;
+  double* G = sm + c;           // gam
+  double* E = sm + L * NC + c;  // qe
+#define AT(S, k) (S)[(k) * NC]
+  const int64_t off = i + (int64_t)j * a.sj, sk = a.sk;
+  const double* dp = a.delp.ptr(i, j, 0);
+  for (int t = 0; t < a.nq; ++t) {
+    const double* q = a.q[t] + off;
+    // forward: remap_edge_fwd
+    double d4p = 0.0;
+    {
+      const double dp0 = dp[0], dp1 = dp[sk];
+      const double grat = dp1 / dp0;
+      const double bet = grat * (grat + 0.5);
+      AT(E, 0) = ((grat + grat) * (grat + 1.0) * q[0] + q[sk]) / bet;
+      AT(G, 0) = (1.0 + grat * (grat + 1.5)) / bet;
+    }
+    double dprev = dp[0], qprev = q[0];
+    for (int k = 1; k < nk; ++k) {
+      const double dk = dp[k * sk], qk = q[k * sk];
+      const double d4 = dprev / dk;
+      const double bet = 2.0 + d4 + d4 - AT(G, k - 1);
+      AT(E, k) = (3.0 * (qprev + d4 * qk) - AT(E, k - 1)) / bet;
+      AT(G, k) = d4 / bet;
+      d4p = d4;
+      dprev = dk;
+      qprev = qk;
+    }
+    {
+      const double abot = 1.0 + d4p * (d4p + 1.5);
+      AT(E, nk) = (2.0 * d4p * (d4p + 1.0) * q[(nk - 1) * sk] + q[(nk - 2) * sk] - abot * AT(E, nk - 1)) /
+                  (d4p * (d4p + 0.5) - abot * AT(G, nk - 1));
+    }
+    // backward: remap_edge_bwd fused with remap_a4 for layer k
+    double* o2 = a.a2[t] + off;
+    double* o3 = a.a3[t] + off;
+    double* o4 = a.a4[t] + off;
+    double qen = AT(E, nk);
+    for (int k = nk - 1; k >= 0; --k) {
+      const double qek = AT(E, k) - AT(G, k) * qen;
+      const double qc = q[k * sk];
+      const double al = qek, ar = qen;
+      const double ext = (ar - qc) * (qc - al);
+      const double da1 = ar - al;
+      const double a6 = 3.0 * (2.0 * qc - (al + ar));
+      const double a6da = a6 * da1;
+      const double da2 = da1 * da1;
+      const double v2 = (ext <= 0.0) ? qc : ((a6da > da2) ? 3.0 * qc - 2.0 * ar : al);
+      const double v3 = (ext <= 0.0) ? qc : ((a6da < -da2) ? 3.0 * qc - 2.0 * al : ar);
+      o2[k * sk] = v2;
+      o3[k * sk] = v3;
+      o4[k * sk] = 3.0 * (2.0 * qc - (v2 + v3));
+      qen = qek;
+    }
+  }
+#undef AT
+}
+
+static int set_smem(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024 &&
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return check_launch("smem attribute");
+  return FV3B_OK;
+}
+
+int launch_riem(const RiemArgs& a, cudaStream_t st) {
+  const size_t bytes = 3 * (size_t)(a.nk + 1) * NC * sizeof(double);
+  FV3B_TRY(set_smem((const void*)riem_kernel, bytes));
+  const int cols = a.ni_ext * a.nj_ext;
+  riem_kernel<<<cdiv(cols, NC), NC, bytes, st>>>(a);
+  return check_launch("riem_solver_c");
+}
+
+}  // namespace fv3b
+
+using namespace fv3b;
+
+// fields: dm, pt, w (layers), gz (interfaces), ws (2-D), pef, gz_out
+// (interfaces; gz_out may alias gz).  scalars: ptop, rdgas, grav, gama,
+// p_fac, dt.  Domain nk = interface levels (program domain, nk_layers + 1).
+extern "C" int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                  void* stream) {
+  if (f == nullptr || d == nullptr || s == nullptr || nf != 7 || ns != 6)
+    return fail(FV3B_EINVAL, "fv3b_riem_solver_c: expects 7 fields, 6 scalars (got %d, %d)", nf, ns);
+  if (d->nk < 4) return fail(FV3B_EDOMAIN, "fv3b_riem_solver_c: program domain nk=%d below minimum 4", d->nk);
+  RiemArgs a;
+  const Halo h0 = {0, 0, 0, 0, 0, 0};
+  FV3B_TRY(view_of(f[0], 3, *d, h0, "dm", &a.dm));
+  FV3B_TRY(view_of(f[1], 3, *d, h0, "pt", &a.pt));
+  FV3B_TRY(view_of(f[2], 3, *d, h0, "w", &a.w));
+  FV3B_TRY(view_of(f[3], 3, *d, h0, "gz", &a.gz));
+  FV3B_TRY(view_of(f[4], 2, *d, h0, "ws", &a.ws));
+  FV3B_TRY(view_of(f[5], 3, *d, h0, "pef", &a.pef));
+  FV3B_TRY(view_of(f[6], 3, *d, h0, "gz_out", &a.gzo));
+  if (a.dm.sk != a.pt.sk || a.dm.sk != a.w.sk || a.dm.sk != a.gz.sk)
+    return fail(FV3B_ELAYOUT, "fv3b_riem_solver_c: input K strides differ");
+  a.ilo = 0;
+  a.jlo = 0;
+  a.ni_ext = d->ni;
+  a.nj_ext = d->nj;
+  a.nk = d->nk - 1;
+  a.ptop = s[0]; a.rdgas = s[1]; a.grav = s[2]; a.gama = s[3]; a.p_fac = s[4]; a.dt = s[5];
+  if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
+  return launch_riem(a, (cudaStream_t)stream);
+}
+
+// fields: delp, then per tracer t: q_t, a2_t, a3_t, a4_t.  Domain nk =
+// interface levels (program domain).  No scalars.
+extern "C" int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                  void* stream) {
+  (void)s;
+  if (f == nullptr || d == nullptr || nf < 5 || (nf - 1) % 4 != 0 || (nf - 1) / 4 > 16 || ns != 0)
+    return fail(FV3B_EINVAL, "fv3b_remap_profile: expects 1 + 4*nq fields (nq <= 16), 0 scalars");
+  if (d->nk < 3) return fail(FV3B_EDOMAIN, "fv3b_remap_profile: program domain nk=%d below minimum 3", d->nk);
+  RemapArgs a;
+  const Halo h0 = {0, 0, 0, 0, 0, 0};
+  FV3B_TRY(view_of(f[0], 3, *d, h0, "delp", &a.delp));
+  a.nq = (nf - 1) / 4;
+  for (int t = 0; t < a.nq; ++t) {
+    View v[4];
+    for (int u = 0; u < 4; ++u) FV3B_TRY(view_of(f[1 + 4 * t + u], 3, *d, h0, "remap field", &v[u]));
+    for (int u = 0; u < 4; ++u)
+      if (v[u].sj != a.delp.sj || v[u].sk != a.delp.sk) return fail(FV3B_ELAYOUT, "fv3b_remap_profile: strides differ");
+    a.q[t] = v[0].o;
+    a.a2[t] = v[1].o;
+    a.a3[t] = v[2].o;
+    a.a4[t] = v[3].o;
+  }
+  a.sj = a.delp.sj;
+  a.sk = a.delp.sk;
+  a.ni = d->ni;
+  a.nj = d->nj;
+  a.nk = d->nk - 1;
+  if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
+  const size_t bytes = 2 * (size_t)(a.nk + 1) * NC * sizeof(double);
+  FV3B_TRY(set_smem((const void*)remap_kernel, bytes));
+  remap_kernel<<<cdiv(a.ni * a.nj, NC), NC, bytes, (cudaStream_t)stream>>>(a);
+  return check_launch("remap_profile");
+}

@@ -1,274 +1,444 @@
 // K1 fv_tp_2d and K7 tracer_2d: FV3 2-D finite-volume transport
 // (programs/fv_tp_2d.stn, programs/tracer_2d.stn; templates.fv_tp_2d).
 //
-// One CTA owns a TI x TJ tile of one level and keeps every intermediate of
-// the .stn statement chain in shared memory:
-//
-//   fy2 = yppm(q, cry)                      faces j in [0, TJ]  , i in [-3, TI+3)
+// Statement chain per level (faces: fx on west faces, fy on south faces):
+//   fy2 = yppm(q, cry)
 //   qi  = (q*area + fy2*yfx - fy2[j+1]*yfx[j+1]) / (area + yfx - yfx[j+1])
-//   fx2 = xppm(q, crx)                      faces i in [0, TI]  , j in [-3, TJ+3)
+//   fx2 = xppm(q, crx)
 //   qj  = (q*area + fx2*xfx - fx2[i+1]*xfx[i+1]) / (area + xfx - xfx[i+1])
 //   fx  = 0.5*(xppm(qi, crx) + fx2) * (xfx | mfx)
 //   fy  = 0.5*(yppm(qj, cry) + fy2) * (yfx | mfy)
-//   q'  = q + (fx - fx[i+1] + fy - fy[j+1]) * rarea                  (fv_tp_2d)
-//   q'  = (q*dp1 + (...)*rarea) / (dp1 + (mfx - mfx[i+1] + mfy - mfy[j+1])*rarea)  (tracer)
+//   q'  = q + (fx - fx[i+1] + fy - fy[j+1]) * rarea                          fv_tp_2d
+//   q'  = (q*dp1 + (...)*rarea) / (dp1 + (mfx-mfx[i+1]+mfy-mfy[j+1])*rarea)   tracer
 //
-// Temporaries are recomputed over the tile halo exactly as the reference
-// computes them over their extension (extents.py:128-164), so every value
-// that reaches an output is produced by the same IEEE operations.  The
-// tracer variant loops over the tracers inside the CTA so the shared
-// Courant numbers and fluxes are read from HBM once per tile.
+// Kernel structure (one CTA = TI x TJ columns x a chunk of levels):
+//  * every level's input tiles (q with a 3-cell halo, Courant numbers and
+//    fluxes on the faces the chain touches) arrive by TMA into a
+//    double-buffered shared-memory stage; the load of level k+1 (or the next
+//    tracer) is issued before level k is computed, so HBM streams while the
+//    FP64 pipes work;
+//  * y-direction passes are column-per-thread, x-direction passes
+//    row-segment-per-thread, each a register sliding window (ppm.cuh);
+//  * temporaries are recomputed over the tile halo exactly where the
+//    reference extends them (extents.py:128-164), so outputs are bitwise the
+//    interpreter's.
+// The tracer variant walks (level, tracer) steps so the shared Courant
+// numbers / fluxes / dp1 are fetched once per level for all tracers.
 #include "common.cuh"
+#include "ppm.cuh"
+#include "tma.cuh"
 
 namespace fv3b {
 
 constexpr int NQMAX = 16;
-
-// PPM face value on the low face of cell `q[0]` along stride `s`
-// (templates.ppm_flux; FV3 xppm/yppm, hord=5 smoothness switch).
-__device__ __forceinline__ double ppm_face(const double* q, int s, double c, double p1, double p2) {
-  const double qm3 = q[-3 * s], qm2 = q[-2 * s], qm1 = q[-s], q0 = q[0], qp1 = q[s], qp2 = q[2 * s];
-  const double al_m = p1 * (qm2 + qm1) + p2 * (qm3 + q0);   // al at cell i-1
-  const double al_0 = p1 * (qm1 + q0) + p2 * (qm2 + qp1);   // al at cell i
-  const double al_p = p1 * (q0 + qp1) + p2 * (qm1 + qp2);   // al at cell i+1
-  const double bl_m = al_m - qm1, br_m = al_0 - qm1, b0_m = bl_m + br_m;
-  const double bl_0 = al_0 - q0, br_0 = al_p - q0, b0_0 = bl_0 + br_0;
-  const bool smooth = (fabs(3.0 * b0_m) < fabs(bl_m - br_m)) || (fabs(3.0 * b0_0) < fabs(bl_0 - br_0));
-  if (c > 0.0) return qm1 + (smooth ? (1.0 - c) * (br_m - c * b0_m) : 0.0);
-  return q0 + (smooth ? (1.0 + c) * (bl_0 + c * b0_0) : 0.0);
-}
+constexpr int SEG = 4;  // cells per sliding-window segment
+constexpr int TP_NT = 352;  // threads per CTA (11 warps): >= phase-A items
 
 struct TpArgs {
-  View crx, cry, xfx, yfx, area, rarea;
-  View mfx, mfy, dp1;  // tracer variant only
-  double* qin[NQMAX];
+  CUtensorMap q[NQMAX];
+  CUtensorMap crx, xfx, cry, yfx, mfx, mfy, dp1, area;
   double* qout[NQMAX];
-  int64_t sj, sk;  // shared 3-D strides
-  int nq, ni, nj, nk;
+  const double* rarea;  // interior origin of rarea (2-D)
+  int64_t sj, sk;       // 3-D strides (elements)
+  int i0, j0;           // allocated column / row of the interior origin
+  int nq, ni, nj, nk, kchunk;
   double p1, p2;
 };
 
-template <int TI, int TJ>
-struct TpSmem {
-  // element counts of each tile array
-  static constexpr int QW = TI + 6, QH = TJ + 6;
-  static constexpr int n_q = QW * QH;
-  static constexpr int n_cx = (TI + 1) * QH;   // crx, xfx, fx2
-  static constexpr int n_cy = QW * (TJ + 1);   // cry, yfx, fy2
-  static constexpr int n_qi = QW * TJ;
-  static constexpr int n_qj = TI * QH;
-  static constexpr int n_fx = (TI + 1) * TJ;
-  static constexpr int n_fy = TI * (TJ + 1);
-  static constexpr int total = n_q + 3 * n_cx + 3 * n_cy + n_qi + n_qj + n_fx + n_fy + n_fx + n_fy + TI * TJ;
-  static constexpr size_t bytes = sizeof(double) * total;
+__host__ __device__ constexpr int align16(int n) { return (n + 15) / 16 * 16; }
+
+template <int TI, int TJ, bool MASS>
+struct TpLayout {
+  // Row widths of tiles read by row-segment threads are = 2 (mod 4) doubles so
+  // the threads of a warp (consecutive rows) hit distinct bank pairs.
+  static constexpr int QW = TI + 10, QH = TJ + 6;  // q, area: i in [-4, TI+6), j in [-3, TJ+3)
+  static constexpr int XW = TI + 2, XH = TJ + 6;   // crx, xfx: i in [0, TI+2), j in [-3, TJ+3)
+  static constexpr int YW = TI + 8, YH = TJ + 1;   // cry, yfx: i in [-4, TI+4), j in [0, TJ+1)
+  static constexpr int JW = TI + 2;                // qj row width
+  static constexpr int n_q = align16(QW * QH);
+  static constexpr int n_x = align16(XW * XH);
+  static constexpr int n_y = align16(YW * YH);
+  static constexpr int n_mx = align16(XW * TJ);    // mfx: i in [0, TI+2), j in [0, TJ)
+  static constexpr int n_my = align16(TI * YH);    // mfy: i in [0, TI), j in [0, TJ+1)
+  static constexpr int n_dp = align16(TI * TJ);    // dp1
+  static constexpr int n_shared = 2 * n_x + 2 * n_y + (MASS ? n_mx + n_my + n_dp : 0);
+  // intermediates
+  static constexpr int n_qi = align16(QW * TJ);    // i in [-4, TI+4), j in [0, TJ)
+  static constexpr int n_qj = align16(JW * QH);    // i in [0, TI), j in [-3, TJ+3)
+  static constexpr int n_fx = align16(XW * TJ);    // faces i in [0, TI+1)
+  static constexpr int n_fy = align16(TI * YH);    // faces j in [0, TJ+1)
+  // offsets (doubles)
+  static constexpr int o_q = 0;                      // 2 q stages
+  static constexpr int o_sh = o_q + 2 * n_q;         // 2 shared stages
+  static constexpr int o_area = o_sh + 2 * n_shared;
+  static constexpr int o_qi = o_area + n_q;
+  static constexpr int o_qj = o_qi + n_qi;
+  static constexpr int o_fx2 = o_qj + n_qj;
+  static constexpr int o_fy2 = o_fx2 + n_fx;
+  static constexpr int o_fx = o_fy2 + n_fy;
+  static constexpr int o_dp2 = o_fx + n_fx;
+  static constexpr int total = o_dp2 + (MASS ? n_dp : 0);
+  static constexpr size_t bytes = total * sizeof(double) + 64;  // + mbarriers
+  static_assert(bytes <= 227 * 1024, "shared memory budget");
+  static_assert(TJ % SEG == 0 && TI % SEG == 0 && QW % 4 == 2 && XW % 4 == 2 && JW % 4 == 2, "tile shape");
+  // TMA transaction bytes
+  static constexpr uint32_t tx_q = QW * QH * 8;
+  static constexpr uint32_t tx_shared = (2 * XW * XH + 2 * YW * YH + (MASS ? XW * TJ + TI * YH + TI * TJ : 0)) * 8;
+  static constexpr uint32_t tx_area = QW * QH * 8;
 };
 
 template <int TI, int TJ, bool MASS>
-__global__ void __launch_bounds__(256) tp_kernel(TpArgs a) {
-  using S = TpSmem<TI, TJ>;
-  extern __shared__ double smem[];
-  const int NT = blockDim.x, tid = threadIdx.x;
-  const int gi0 = blockIdx.x * TI, gj0 = blockIdx.y * TJ, k = blockIdx.z;
-  double* p = smem;
-  const STile sq{p, -3, -3, S::QW};           p += S::n_q;
-  const STile scrx{p, 0, -3, TI + 1};        p += S::n_cx;
-  const STile sxfx{p, 0, -3, TI + 1};        p += S::n_cx;
-  const STile sfx2{p, 0, -3, TI + 1};        p += S::n_cx;
-  const STile scry{p, -3, 0, S::QW};         p += S::n_cy;
-  const STile syfx{p, -3, 0, S::QW};         p += S::n_cy;
-  const STile sfy2{p, -3, 0, S::QW};         p += S::n_cy;
-  const STile sqi{p, -3, 0, S::QW};          p += S::n_qi;
-  const STile sqj{p, 0, -3, TI};             p += S::n_qj;
-  const STile sfx{p, 0, 0, TI + 1};          p += S::n_fx;
-  const STile sfy{p, 0, 0, TI};              p += S::n_fy;
-  const STile swx{p, 0, 0, TI + 1};          p += S::n_fx;   // flux weight xfx | mfx on faces
-  const STile swy{p, 0, 0, TI};              p += S::n_fy;   // flux weight yfx | mfy on faces
-  const STile sdp2{p, 0, 0, TI};
+__global__ void __launch_bounds__(TP_NT, MASS ? 1 : 2) tp_kernel(const __grid_constant__ TpArgs a) {
+  using L = TpLayout<TI, TJ, MASS>;
+  extern __shared__ __align__(128) double smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::total);  // [0],[1] step stages, [2] area
+  const int tid = threadIdx.x;
+  const int gi0 = blockIdx.x * TI, gj0 = blockIdx.y * TJ;
+  const int k0 = blockIdx.z * a.kchunk;
+  const int k1 = min(a.nk, k0 + a.kchunk);
+  const int nsteps = (k1 - k0) * a.nq;
+  const int xq = a.i0 + gi0 - 4, yq = a.j0 + gj0 - 3;  // box origins (allocated coords)
+  const int xx = a.i0 + gi0, yy = a.j0 + gj0;
+  const double p1 = a.p1, p2 = a.p2;
 
-  const int ni = a.ni, nj = a.nj;
-  auto inside = [&](int li, int lj, int hi_lo, int hi_hi, int hj_lo, int hj_hi) {
-    const int gi = gi0 + li, gj = gj0 + lj;
-    return gi >= -hi_lo && gi < ni + hi_hi && gj >= -hj_lo && gj < nj + hj_hi;
+  auto issue = [&](int step) {  // single thread
+    const int k = k0 + step / a.nq, t = step % a.nq;
+    const int b = step & 1;
+    double* sq = smem + L::o_q + b * L::n_q;
+    uint32_t tx = L::tx_q;
+    if (t == 0) tx += L::tx_shared;
+    mbar_expect_tx(&bar[b], tx);
+    tma_load3(sq, &a.q[t], xq, yq, k, &bar[b]);
+    if (t == 0) {
+      double* sh = smem + L::o_sh + ((k - k0) & 1) * L::n_shared;
+      tma_load3(sh, &a.crx, xx, yq, k, &bar[b]);
+      tma_load3(sh + L::n_x, &a.xfx, xx, yq, k, &bar[b]);
+      tma_load3(sh + 2 * L::n_x, &a.cry, xq, yy, k, &bar[b]);
+      tma_load3(sh + 2 * L::n_x + L::n_y, &a.yfx, xq, yy, k, &bar[b]);
+      if (MASS) {
+        double* m = sh + 2 * L::n_x + 2 * L::n_y;
+        tma_load3(m, &a.mfx, xx, yy, k, &bar[b]);
+        tma_load3(m + L::n_mx, &a.mfy, xx, yy, k, &bar[b]);
+        tma_load3(m + L::n_mx + L::n_my, &a.dp1, xx, yy, k, &bar[b]);
+      }
+    }
   };
 
-  // --- shared inputs: Courant numbers and area fluxes ---------------------
-  for (int e = tid; e < S::n_cx; e += NT) {
-    const int li = e % (TI + 1), lj = e / (TI + 1) - 3;
-    const bool ok = inside(li, lj, 0, 1, 3, 3);
-    scrx(li, lj) = ok ? a.crx(gi0 + li, gj0 + lj, k) : 0.0;
-    sxfx(li, lj) = ok ? a.xfx(gi0 + li, gj0 + lj, k) : 0.0;
-  }
-  for (int e = tid; e < S::n_cy; e += NT) {
-    const int li = e % S::QW - 3, lj = e / S::QW;
-    const bool ok = inside(li, lj, 3, 3, 0, 1);
-    scry(li, lj) = ok ? a.cry(gi0 + li, gj0 + lj, k) : 0.0;
-    syfx(li, lj) = ok ? a.yfx(gi0 + li, gj0 + lj, k) : 0.0;
-  }
-  for (int e = tid; e < S::n_fx; e += NT) {
-    const int li = e % (TI + 1), lj = e / (TI + 1);
-    const bool ok = inside(li, lj, 0, 1, 0, 0);
-    swx(li, lj) = ok ? (MASS ? a.mfx(gi0 + li, gj0 + lj, k) : sxfx(li, lj)) : 0.0;
-  }
-  for (int e = tid; e < S::n_fy; e += NT) {
-    const int li = e % TI, lj = e / TI;
-    const bool ok = inside(li, lj, 0, 0, 0, 1);
-    swy(li, lj) = ok ? (MASS ? a.mfy(gi0 + li, gj0 + lj, k) : syfx(li, lj)) : 0.0;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    fence_mbar_init();
   }
   __syncthreads();
-  if (MASS) {
-    // dp2 = dp1 + (mfx - mfx[1,0,0] + mfy - mfy[0,1,0]) * rarea   (tracer_dp)
-    for (int e = tid; e < TI * TJ; e += NT) {
-      const int li = e % TI, lj = e / TI;
-      if (!inside(li, lj, 0, 0, 0, 0)) continue;
-      const int gi = gi0 + li, gj = gj0 + lj;
-      sdp2(li, lj) = a.dp1(gi, gj, k) + (swx(li, lj) - swx(li + 1, lj) + swy(li, lj) - swy(li, lj + 1)) * a.rarea(gi, gj, 0);
-    }
+  if (tid == 0 && nsteps > 0) {
+    mbar_expect_tx(&bar[2], L::tx_area);
+    tma_load3(smem + L::o_area, &a.area, xq, yq, 0, &bar[2]);
+    issue(0);
   }
+  const double* sarea = smem + L::o_area;  // row width QW, origin (-4, -3)
+  double* sqi = smem + L::o_qi;            // QW, origin (-4, 0)
+  double* sqj = smem + L::o_qj;            // JW, origin (0, -3)
+  double* sfx2 = smem + L::o_fx2;          // XW, origin (0, 0)
+  double* sfy2 = smem + L::o_fy2;          // TI, origin (0, 0)
+  double* sfx = smem + L::o_fx;            // XW, origin (0, 0)
+  double* sdp2 = smem + L::o_dp2;          // TI, origin (0, 0)
+  if (nsteps > 0) mbar_wait(&bar[2], 0);
 
-  const double p1 = a.p1, p2 = a.p2;
-  for (int t = 0; t < a.nq; ++t) {
-    const View q{a.qin[t], a.sj, a.sk};
-    const View qo{a.qout[t], a.sj, a.sk};
-    for (int e = tid; e < S::n_q; e += NT) {
-      const int li = e % S::QW - 3, lj = e / S::QW - 3;
-      sq(li, lj) = inside(li, lj, 3, 3, 3, 3) ? q(gi0 + li, gj0 + lj, k) : 0.0;
+  constexpr int NSEG = TI / SEG;
+  static_assert((TI + 6) * (TJ / SEG) + (TJ + 6) * (TI / SEG) <= TP_NT, "one phase-A item per thread");
+  constexpr int NX2 = TJ * NSEG, NY2 = TI * (TJ / SEG);
+  static_assert(NX2 + NY2 <= TP_NT, "one item per thread in phase 2");
+  // Phase-2 y threads own a fixed column segment for the whole CTA: they
+  // keep rarea, and the previous step's fy / q / dp in registers and write
+  // that step's result while the next step's phase 1 runs (2 barriers/level).
+  const bool yth = tid >= NX2 && tid < NX2 + NY2;
+  const int ci2 = yth ? (tid - NX2) % TI : 0;
+  const int jb2 = yth ? ((tid - NX2) / TI) * SEG : 0;
+  const int gi2 = gi0 + ci2;
+  double ra[SEG];
+#pragma unroll
+  for (int u = 0; u < SEG; ++u) {
+    const int gj = gj0 + jb2 + u;
+    ra[u] = (yth && gi2 < a.ni && gj < a.nj) ? a.rarea[gi2 + (int64_t)gj * a.sj] : 0.0;
+  }
+  double fy[SEG + 1], qc[SEG], dpa[SEG], dpb[SEG];
+  int pend_k = -1, pend_t = 0;  // step whose output is pending
+
+  auto write_pending = [&]() {
+    if (!yth || pend_k < 0) return;
+    double* qo = a.qout[pend_t];
+#pragma unroll
+    for (int u = 0; u < SEG; ++u) {
+      const int j = jb2 + u, gj = gj0 + j;
+      if (gi2 < a.ni && gj < a.nj) {
+        const int64_t off = gi2 + (int64_t)gj * a.sj + (int64_t)pend_k * a.sk;
+        const double div = (sfx[j * L::XW + ci2] - sfx[j * L::XW + ci2 + 1] + fy[u] - fy[u + 1]) * ra[u];
+        if (MASS)
+          qo[off] = (qc[u] * dpa[u] + div) / dpb[u];
+        else
+          qo[off] = qc[u] + div;
+      }
+    }
+  };
+
+  for (int step = 0; step < nsteps; ++step) {
+    const int k = k0 + step / a.nq, t = step % a.nq;
+    const int b = step & 1;
+    if (tid == 0 && step + 1 < nsteps) {
+      fence_async_smem();
+      issue(step + 1);
+    }
+    mbar_wait(&bar[b], (step >> 1) & 1);
+    const double* sq = smem + L::o_q + b * L::n_q;                             // QW, origin (-4, -3)
+    const double* sh = smem + L::o_sh + ((k - k0) & 1) * L::n_shared;
+    const double* scrx = sh;                                                   // XW, origin (0, -3)
+    const double* sxfx = sh + L::n_x;                                          // XW, origin (0, -3)
+    const double* scry = sh + 2 * L::n_x;                                      // YW, origin (-4, 0)
+    const double* syfx = sh + 2 * L::n_x + L::n_y;                             // YW, origin (-4, 0)
+    const double* smfx = sh + 2 * L::n_x + 2 * L::n_y;                         // XW, origin (0, 0)
+    const double* smfy = smfx + L::n_mx;                                       // TI, origin (0, 0)
+    const double* sdp1 = smfy + L::n_my;                                       // TI, origin (0, 0)
+    auto Q = [&](int i, int j) { return sq + (j + 3) * L::QW + (i + 4); };
+    auto CX = [&](const double* p, int i, int j) { return p + (j + 3) * L::XW + i; };
+    auto CY = [&](const double* p, int i, int j) { return p + j * L::YW + (i + 4); };
+
+    // ---- phase A: previous step's output; dp2; yppm(q)/xppm(q) ----------
+    write_pending();
+    if (MASS && t == 0) {
+      // dp2 = dp1 + (mfx - mfx[1,0,0] + mfy - mfy[0,1,0]) * rarea      (tracer_dp)
+      for (int e = tid; e < TI * TJ; e += blockDim.x) {
+        const int li = e % TI, lj = e / TI;
+        const double rr = (gi0 + li < a.ni && gj0 + lj < a.nj) ? a.rarea[(gi0 + li) + (int64_t)(gj0 + lj) * a.sj] : 0.0;
+        sdp2[lj * TI + li] = sdp1[lj * TI + li] + (smfx[lj * L::XW + li] - smfx[lj * L::XW + li + 1] +
+                                                   smfy[lj * TI + li] - smfy[(lj + 1) * TI + li]) * rr;
+      }
+    }
+    // Y items: consecutive threads own consecutive columns; X items:
+    // consecutive threads own consecutive rows (bank-conflict-free, see QW).
+    {
+      constexpr int NCY = TI + 6, NSY = TJ / SEG;  // columns i in [-3, TI+3)
+      constexpr int NRX = TJ + 6, NSX = TI / SEG;  // rows j in [-3, TJ+3)
+      constexpr int NY = NCY * NSY, NX = NRX * NSX;
+      for (int item = tid; item < NY + NX; item += blockDim.x) {
+        if (item < NY) {
+          const int ci = item % NCY - 3, jb = (item / NCY) * SEG;
+          double f[SEG + 1];
+          ppm_line<SEG + 1>(Q(ci, jb), L::QW, CY(scry, ci, jb), L::YW, p1, p2, f);
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) {
+            const int j = jb + u;
+            const double ar = sarea[(j + 3) * L::QW + ci + 4];
+            const double y0 = *CY(syfx, ci, j), y1 = *CY(syfx, ci, j + 1);
+            sqi[j * L::QW + ci + 4] = (*Q(ci, j) * ar + f[u] * y0 - f[u + 1] * y1) / (ar + y0 - y1);
+          }
+          if (ci >= 0 && ci < TI) {
+#pragma unroll
+            for (int u = 0; u < SEG; ++u) sfy2[(jb + u) * TI + ci] = f[u];
+            if (jb + SEG == TJ) sfy2[TJ * TI + ci] = f[SEG];
+          }
+        } else {
+          const int it = item - NY;
+          const int rj = it % NRX - 3, ib = (it / NRX) * SEG;
+          double f[SEG + 1];
+          ppm_line<SEG + 1>(Q(ib, rj), 1, CX(scrx, ib, rj), 1, p1, p2, f);
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) {
+            const int i = ib + u;
+            const double ar = sarea[(rj + 3) * L::QW + i + 4];
+            const double x0 = *CX(sxfx, i, rj), x1 = *CX(sxfx, i + 1, rj);
+            sqj[(rj + 3) * L::JW + i] = (*Q(i, rj) * ar + f[u] * x0 - f[u + 1] * x1) / (ar + x0 - x1);
+          }
+          if (rj >= 0 && rj < TJ) {
+#pragma unroll
+            for (int u = 0; u < SEG; ++u) sfx2[rj * L::XW + ib + u] = f[u];
+            if (ib + SEG == TI) sfx2[rj * L::XW + TI] = f[SEG];
+          }
+        }
+      }
     }
     __syncthreads();
-    // fy2 = yppm(q, cry) on faces j in [0, TJ], i in [-3, TI+3)
-    for (int e = tid; e < S::n_cy; e += NT) {
-      const int li = e % S::QW - 3, lj = e / S::QW;
-      sfy2(li, lj) = ppm_face(&sq(li, lj), S::QW, scry(li, lj), p1, p2);
+
+    // ---- phase B: xppm(qi) -> fx (smem) ; yppm(qj) -> fy (registers) -----
+    if (tid < NX2) {
+      const int rj = tid % TJ, ib = (tid / TJ) * SEG;
+      double f[SEG + 1];
+      ppm_line<SEG + 1>(sqi + rj * L::QW + ib + 4, 1, CX(scrx, ib, rj), 1, p1, p2, f);
+      const int nf = (ib + SEG == TI) ? SEG + 1 : SEG;
+#pragma unroll
+      for (int u = 0; u < SEG + 1; ++u) {
+        if (u < nf) {
+          const int i = ib + u;
+          const double w = MASS ? smfx[rj * L::XW + i] : *CX(sxfx, i, rj);
+          sfx[rj * L::XW + i] = 0.5 * (f[u] + sfx2[rj * L::XW + i]) * w;
+        }
+      }
+    } else if (yth) {
+      ppm_line<SEG + 1>(sqj + (jb2 + 3) * L::JW + ci2, L::JW, CY(scry, ci2, jb2), L::YW, p1, p2, fy);
+#pragma unroll
+      for (int u = 0; u < SEG + 1; ++u) {
+        const int j = jb2 + u;
+        const double w = MASS ? smfy[j * TI + ci2] : *CY(syfx, ci2, j);
+        fy[u] = 0.5 * (fy[u] + sfy2[j * TI + ci2]) * w;
+      }
+#pragma unroll
+      for (int u = 0; u < SEG; ++u) {
+        qc[u] = *Q(ci2, jb2 + u);
+        if (MASS) {
+          dpa[u] = sdp1[(jb2 + u) * TI + ci2];
+          dpb[u] = sdp2[(jb2 + u) * TI + ci2];
+        }
+      }
     }
-    // fx2 = xppm(q, crx) on faces i in [0, TI], j in [-3, TJ+3)
-    for (int e = tid; e < S::n_cx; e += NT) {
-      const int li = e % (TI + 1), lj = e / (TI + 1) - 3;
-      sfx2(li, lj) = ppm_face(&sq(li, lj), 1, scrx(li, lj), p1, p2);
-    }
-    __syncthreads();
-    // qi over i in [-3, TI+3), j in [0, TJ); qj over i in [0, TI), j in [-3, TJ+3)
-    for (int e = tid; e < S::n_qi; e += NT) {
-      const int li = e % S::QW - 3, lj = e / S::QW;
-      const double ar = inside(li, lj, 3, 3, 0, 0) ? a.area(gi0 + li, gj0 + lj, 0) : 0.0;
-      sqi(li, lj) = (sq(li, lj) * ar + sfy2(li, lj) * syfx(li, lj) - sfy2(li, lj + 1) * syfx(li, lj + 1)) /
-                    (ar + syfx(li, lj) - syfx(li, lj + 1));
-    }
-    for (int e = tid; e < S::n_qj; e += NT) {
-      const int li = e % TI, lj = e / TI - 3;
-      const double ar = inside(li, lj, 0, 0, 3, 3) ? a.area(gi0 + li, gj0 + lj, 0) : 0.0;
-      sqj(li, lj) = (sq(li, lj) * ar + sfx2(li, lj) * sxfx(li, lj) - sfx2(li + 1, lj) * sxfx(li + 1, lj)) /
-                    (ar + sxfx(li, lj) - sxfx(li + 1, lj));
-    }
-    __syncthreads();
-    // fx = 0.5*(xppm(qi) + fx2) * w ;  fy = 0.5*(yppm(qj) + fy2) * w
-    for (int e = tid; e < S::n_fx; e += NT) {
-      const int li = e % (TI + 1), lj = e / (TI + 1);
-      const double fx1 = ppm_face(&sqi(li, lj), 1, scrx(li, lj), p1, p2);
-      sfx(li, lj) = 0.5 * (fx1 + sfx2(li, lj)) * swx(li, lj);
-    }
-    for (int e = tid; e < S::n_fy; e += NT) {
-      const int li = e % TI, lj = e / TI;
-      const double fy1 = ppm_face(&sqj(li, lj), TI, scry(li, lj), p1, p2);
-      sfy(li, lj) = 0.5 * (fy1 + sfy2(li, lj)) * swy(li, lj);
-    }
-    __syncthreads();
-    for (int e = tid; e < TI * TJ; e += NT) {
-      const int li = e % TI, lj = e / TI;
-      if (!inside(li, lj, 0, 0, 0, 0)) continue;
-      const int gi = gi0 + li, gj = gj0 + lj;
-      const double div = (sfx(li, lj) - sfx(li + 1, lj) + sfy(li, lj) - sfy(li, lj + 1)) * a.rarea(gi, gj, 0);
-      if (MASS)
-        qo(gi, gj, k) = (sq(li, lj) * a.dp1(gi, gj, k) + div) / sdp2(li, lj);
-      else
-        qo(gi, gj, k) = sq(li, lj) + div;
-    }
+    pend_k = k;
+    pend_t = t;
     __syncthreads();
   }
+  write_pending();
 }
 
-template <bool MASS>
-static int launch_tp(const TpArgs& a, cudaStream_t st) {
-  constexpr int TI = 32, TJ = 16;
-  using S = TpSmem<TI, TJ>;
+template <int TI, int TJ, bool MASS>
+static int launch_tp(const TpArgs& a0, cudaStream_t st) {
+  using L = TpLayout<TI, TJ, MASS>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tp_kernel<TI, TJ, MASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+    if (cudaFuncSetAttribute(tp_kernel<TI, TJ, MASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes) !=
+        cudaSuccess)
+      return check_launch("tp smem attribute");
     attr = true;
   }
-  dim3 grid(cdiv(a.ni, TI), cdiv(a.nj, TJ), a.nk);
-  tp_kernel<TI, TJ, MASS><<<grid, 256, S::bytes, st>>>(a);
+  TpArgs a = a0;
+  const int tiles = cdiv(a.ni, TI) * cdiv(a.nj, TJ);
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // ~4 waves of one CTA per SM; at least 2 levels per CTA so the pipeline overlaps
+  const int chunks = std::max(1, std::min(a.nk, ((MASS ? 4 : 8) * sms + tiles - 1) / tiles));
+  a.kchunk = std::max(MASS ? 1 : 2, cdiv(a.nk, chunks));
+  dim3 grid(cdiv(a.ni, TI), cdiv(a.nj, TJ), cdiv(a.nk, a.kchunk));
+  tp_kernel<TI, TJ, MASS><<<grid, TP_NT, L::bytes, st>>>(a);
   return check_launch(MASS ? "tracer_2d" : "fv_tp_2d");
+}
+
+// Build the tensor maps for one call; boxes match TpLayout.
+template <int TI, int TJ, bool MASS>
+static int make_maps(TpArgs& a, const Geo& g, const fv3b_field* f3q, int nq, const fv3b_field& crx,
+                     const fv3b_field& xfx, const fv3b_field& cry, const fv3b_field& yfx, const fv3b_field* mfx,
+                     const fv3b_field* mfy, const fv3b_field* dp1, const fv3b_field& area) {
+  using L = TpLayout<TI, TJ, MASS>;
+  for (int t = 0; t < nq; ++t) FV3B_TRY(tensor_map(f3q[t].data, g.pitch, g.rows, g.levels, L::QW, L::QH, &a.q[t]));
+  FV3B_TRY(tensor_map(crx.data, g.pitch, g.rows, g.levels, L::XW, L::XH, &a.crx));
+  FV3B_TRY(tensor_map(xfx.data, g.pitch, g.rows, g.levels, L::XW, L::XH, &a.xfx));
+  FV3B_TRY(tensor_map(cry.data, g.pitch, g.rows, g.levels, L::YW, L::YH, &a.cry));
+  FV3B_TRY(tensor_map(yfx.data, g.pitch, g.rows, g.levels, L::YW, L::YH, &a.yfx));
+  if (MASS) {
+    FV3B_TRY(tensor_map(mfx->data, g.pitch, g.rows, g.levels, L::XW, TJ, &a.mfx));
+    FV3B_TRY(tensor_map(mfy->data, g.pitch, g.rows, g.levels, TI, L::YH, &a.mfy));
+    FV3B_TRY(tensor_map(dp1->data, g.pitch, g.rows, g.levels, TI, TJ, &a.dp1));
+  }
+  FV3B_TRY(tensor_map(area.data, g.pitch, g.rows, 1, L::QW, L::QH, &a.area));
+  return FV3B_OK;
+}
+
+// Common argument validation: every 3-D field must have the same dense
+// geometry (one TMA box geometry per launch).
+static int same_geo(const fv3b_field* fs, int n, const Geo& g, const char* what) {
+  for (int i = 0; i < n; ++i) {
+    Geo h;
+    FV3B_TRY(geo_of(fs[i], &h));
+    const bool is2d = fs[i].rank == 2;
+    if (h.pitch != g.pitch || h.rows != g.rows || (!is2d && h.levels != g.levels) || h.i0 != g.i0 || h.j0 != g.j0)
+      return fail(FV3B_ELAYOUT, "%s: field %d geometry differs from field 0", what, i);
+  }
+  return FV3B_OK;
 }
 
 }  // namespace fv3b
 
 using namespace fv3b;
 
+static constexpr int TP_TI = 32, TP_TJ = 16;
+
 extern "C" int fv3b_fv_tp_2d(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                              void* stream) {
   if (f == nullptr || d == nullptr || s == nullptr || nf != 8 || ns != 2)
     return fail(FV3B_EINVAL, "fv3b_fv_tp_2d: expects 8 fields, 2 scalars (got %d, %d)", nf, ns);
-  TpArgs a{};
-  View q, qo;
+  View q, crx, cry, xfx, yfx, area, rarea, qo;
   const Halo hq = {3, 3, 3, 3, 0, 0}, hx = {0, 1, 3, 3, 0, 0}, hy = {3, 3, 0, 1, 0, 0}, h0 = {0, 0, 0, 0, 0, 0};
   FV3B_TRY(view_of(f[0], 3, *d, hq, "q", &q));
-  FV3B_TRY(view_of(f[1], 3, *d, hx, "crx", &a.crx));
-  FV3B_TRY(view_of(f[2], 3, *d, hy, "cry", &a.cry));
-  FV3B_TRY(view_of(f[3], 3, *d, hx, "xfx", &a.xfx));
-  FV3B_TRY(view_of(f[4], 3, *d, hy, "yfx", &a.yfx));
-  FV3B_TRY(view_of(f[5], 2, *d, hq, "area", &a.area));
-  FV3B_TRY(view_of(f[6], 2, *d, h0, "rarea", &a.rarea));
+  FV3B_TRY(view_of(f[1], 3, *d, hx, "crx", &crx));
+  FV3B_TRY(view_of(f[2], 3, *d, hy, "cry", &cry));
+  FV3B_TRY(view_of(f[3], 3, *d, hx, "xfx", &xfx));
+  FV3B_TRY(view_of(f[4], 3, *d, hy, "yfx", &yfx));
+  FV3B_TRY(view_of(f[5], 2, *d, hq, "area", &area));
+  FV3B_TRY(view_of(f[6], 2, *d, h0, "rarea", &rarea));
   FV3B_TRY(view_of(f[7], 3, *d, h0, "q_out", &qo));
-  const View v3[6] = {q, a.crx, a.cry, a.xfx, a.yfx, qo};
-  FV3B_TRY(same_strides(v3, 6, "fv3b_fv_tp_2d"));
   if (f[7].data == f[0].data) return fail(FV3B_EINVAL, "fv3b_fv_tp_2d: q_out must not alias q");
-  a.qin[0] = q.o;
+  Geo g;
+  FV3B_TRY(geo_of(f[0], &g));
+  FV3B_TRY(same_geo(f, 8, g, "fv3b_fv_tp_2d"));
+  if (d->ni <= 0 || d->nj <= 0 || d->nk <= 0) return FV3B_OK;
+  TpArgs a;
+  memset(&a, 0, sizeof a);
+  FV3B_TRY((make_maps<TP_TI, TP_TJ, false>(a, g, &f[0], 1, f[1], f[3], f[2], f[4], nullptr, nullptr, nullptr, f[5])));
   a.qout[0] = qo.o;
+  a.rarea = rarea.o;
   a.sj = q.sj;
   a.sk = q.sk;
+  a.i0 = g.i0;
+  a.j0 = g.j0;
   a.nq = 1;
   a.ni = d->ni; a.nj = d->nj; a.nk = d->nk;
   a.p1 = s[0];
   a.p2 = s[1];
-  if (a.ni <= 0 || a.nj <= 0 || a.nk <= 0) return FV3B_OK;
-  return launch_tp<false>(a, (cudaStream_t)stream);
+  return launch_tp<TP_TI, TP_TJ, false>(a, (cudaStream_t)stream);
 }
+
+static constexpr int TR_TI = 32, TR_TJ = 16;
 
 extern "C" int fv3b_tracer_2d(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                               void* stream) {
   if (f == nullptr || d == nullptr || s == nullptr || ns != 2 || nf < 11 || (nf - 9) % 2 != 0 || (nf - 9) / 2 > NQMAX)
     return fail(FV3B_EINVAL, "fv3b_tracer_2d: expects 9 + 2*nq fields (nq <= %d), 2 scalars", NQMAX);
   const int nq = (nf - 9) / 2;
-  TpArgs a{};
+  View v;
   const Halo hq = {3, 3, 3, 3, 0, 0}, hx = {0, 1, 3, 3, 0, 0}, hy = {3, 3, 0, 1, 0, 0}, h0 = {0, 0, 0, 0, 0, 0};
   const Halo hmx = {0, 1, 0, 0, 0, 0}, hmy = {0, 0, 0, 1, 0, 0};
-  FV3B_TRY(view_of(f[0], 3, *d, hx, "cx", &a.crx));
-  FV3B_TRY(view_of(f[1], 3, *d, hy, "cy", &a.cry));
-  FV3B_TRY(view_of(f[2], 3, *d, hx, "xfx", &a.xfx));
-  FV3B_TRY(view_of(f[3], 3, *d, hy, "yfx", &a.yfx));
-  FV3B_TRY(view_of(f[4], 3, *d, hmx, "mfx", &a.mfx));
-  FV3B_TRY(view_of(f[5], 3, *d, hmy, "mfy", &a.mfy));
-  FV3B_TRY(view_of(f[6], 3, *d, h0, "dp1", &a.dp1));
-  FV3B_TRY(view_of(f[7], 2, *d, hq, "area", &a.area));
-  FV3B_TRY(view_of(f[8], 2, *d, h0, "rarea", &a.rarea));
-  View v3[7 + 2 * NQMAX];
-  v3[0] = a.crx; v3[1] = a.cry; v3[2] = a.xfx; v3[3] = a.yfx; v3[4] = a.mfx; v3[5] = a.mfy; v3[6] = a.dp1;
+  FV3B_TRY(view_of(f[0], 3, *d, hx, "cx", &v));
+  FV3B_TRY(view_of(f[1], 3, *d, hy, "cy", &v));
+  FV3B_TRY(view_of(f[2], 3, *d, hx, "xfx", &v));
+  FV3B_TRY(view_of(f[3], 3, *d, hy, "yfx", &v));
+  FV3B_TRY(view_of(f[4], 3, *d, hmx, "mfx", &v));
+  FV3B_TRY(view_of(f[5], 3, *d, hmy, "mfy", &v));
+  FV3B_TRY(view_of(f[6], 3, *d, h0, "dp1", &v));
+  FV3B_TRY(view_of(f[7], 2, *d, hq, "area", &v));
+  View rarea;
+  FV3B_TRY(view_of(f[8], 2, *d, h0, "rarea", &rarea));
+  TpArgs a;
+  memset(&a, 0, sizeof a);
   for (int t = 0; t < nq; ++t) {
-    char nm[32];
-    snprintf(nm, sizeof nm, "q%d", t);
-    FV3B_TRY(view_of(f[9 + t], 3, *d, hq, nm, &v3[7 + t]));
-    snprintf(nm, sizeof nm, "q%d_out", t);
-    FV3B_TRY(view_of(f[9 + nq + t], 3, *d, h0, nm, &v3[7 + nq + t]));
+    View qi, qo;
+    FV3B_TRY(view_of(f[9 + t], 3, *d, hq, "q", &qi));
+    FV3B_TRY(view_of(f[9 + nq + t], 3, *d, h0, "q_out", &qo));
     if (f[9 + t].data == f[9 + nq + t].data) return fail(FV3B_EINVAL, "fv3b_tracer_2d: q%d_out aliases q%d", t, t);
-    a.qin[t] = v3[7 + t].o;
-    a.qout[t] = v3[7 + nq + t].o;
+    a.qout[t] = qo.o;
   }
-  FV3B_TRY(same_strides(v3, 7 + 2 * nq, "fv3b_tracer_2d"));
-  a.sj = a.crx.sj;
-  a.sk = a.crx.sk;
+  Geo g;
+  FV3B_TRY(geo_of(f[0], &g));
+  FV3B_TRY(same_geo(f, nf, g, "fv3b_tracer_2d"));
+  if (d->ni <= 0 || d->nj <= 0 || d->nk <= 0) return FV3B_OK;
+  FV3B_TRY((make_maps<TR_TI, TR_TJ, true>(a, g, &f[9], nq, f[0], f[2], f[1], f[3], &f[4], &f[5], &f[6], f[7])));
+  a.rarea = rarea.o;
+  a.sj = (int64_t)g.pitch;
+  a.sk = (int64_t)g.pitch * g.rows;
+  a.i0 = g.i0;
+  a.j0 = g.j0;
   a.nq = nq;
   a.ni = d->ni; a.nj = d->nj; a.nk = d->nk;
   a.p1 = s[0];
   a.p2 = s[1];
-  if (a.ni <= 0 || a.nj <= 0 || a.nk <= 0) return FV3B_OK;
-  return launch_tp<true>(a, (cudaStream_t)stream);
+  return launch_tp<TR_TI, TR_TJ, true>(a, (cudaStream_t)stream);
 }

@@ -118,7 +118,52 @@ class Tracer2dPlan(Plan):
         ctx.call("tracer_2d_0", "fv3b_tracer_2d", fields, [s["ppm_p1"], s["ppm_p2"]])
 
 
-PLANS: dict[str, Plan] = {p.name: p for p in (CopyPlan(), FvTp2dPlan(), Tracer2dPlan())}
+class RiemSolverCPlan(Plan):
+    name = "riem_solver_c"
+    stencils = ("riem_pem", "riem_layer", "riem_coef", "riem_pp_fwd", "riem_pp_bwd", "riem_w_fwd",
+                "riem_w_sweep", "riem_w_back", "riem_pe", "riem_out", "riem_gz")
+
+    def run(self, prog, ctx):
+        s = prog.scalars(prog.trace[0][1])
+        ctx.call("riem_pem_0", "fv3b_riem_solver_c",
+                 [ctx.f("dm"), ctx.f("pt"), ctx.f("w"), ctx.f("gz"), ctx.f("ws", 2), ctx.o("pef"), ctx.o("gz")],
+                 [s["ptop"], s["rdgas"], s["grav"], s["gama"], s["p_fac"], s["dt"]])
+
+
+class RemapPlan(Plan):
+    """remap_profile (one field) and remap_tracers (q0..q{n-1})."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def _tracers(self, prog) -> list[str]:
+        if self.name == "remap_profile":
+            return [""]
+        n = len(prog.trace) // 3
+        return [str(t) for t in range(n)]
+
+    def check_trace(self, trace):
+        names = [s for s, _ in trace]
+        if self.name == "remap_profile":
+            want = ["remap_edge_fwd", "remap_edge_bwd", "remap_a4"]
+        else:
+            n = len(names) // 3
+            want = [f"{b}_{t}" for t in range(n) for b in ("remap_edge_fwd", "remap_edge_bwd", "remap_a4")]
+        if names != want:
+            raise NotImplementedError(f"{self.name}: unsupported trace {names}")
+
+    def run(self, prog, ctx):
+        fields = [ctx.f("delp")]
+        if self.name == "remap_profile":
+            fields += [ctx.f("q"), ctx.o("a4_2"), ctx.o("a4_3"), ctx.o("a4_4")]
+        else:
+            for t in self._tracers(prog):
+                fields += [ctx.f(f"q{t}"), ctx.o(f"q{t}_a2"), ctx.o(f"q{t}_a3"), ctx.o(f"q{t}_a4")]
+        ctx.call(prog.trace[0][0] + "_0", "fv3b_remap_profile", fields, [])
+
+
+PLANS: dict[str, Plan] = {p.name: p for p in (CopyPlan(), FvTp2dPlan(), Tracer2dPlan(), RiemSolverCPlan(),
+                                              RemapPlan("remap_profile"), RemapPlan("remap_tracers"))}
 
 
 def plan_for(prog: Program) -> Plan:

@@ -81,6 +81,9 @@ def benchmark_uploaded(up: Uploaded, reps: int = 10, warmup: int = 1, flush_l2: 
     for _ in range(reps):
         if flush is not None:
             flush.fill_(0.0)
+        # keep the GPU busy while the host enqueues the timed launches, so the
+        # events bracket device execution only (not Python launch overhead)
+        torch.cuda._sleep(1_000_000)
         col = _Collector()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)

@@ -21,8 +21,15 @@ from .program import as_program
 _RANGES = {
     "crx": (-0.8, 0.8), "cry": (-0.8, 0.8), "cx": (-0.8, 0.8), "cy": (-0.8, 0.8),
     "xfx": (-0.25, 0.25), "yfx": (-0.25, 0.25), "mfx": (-0.25, 0.25), "mfy": (-0.25, 0.25),
-    "area": (0.9, 1.1), "dp1": (5.0, 10.0), "delp": (5.0, 10.0),
+    "area": (0.9, 1.1), "dp1": (5.0, 10.0),
+    # vertical-column state (Pa, K, m/s)
+    "dm": (900.0, 1300.0), "delp": (900.0, 1300.0), "delpc": (900.0, 1300.0),
+    "pt": (270.0, 300.0), "ptc": (270.0, 300.0),
+    "w": (-1.0, 1.0), "wc": (-1.0, 1.0), "ws": (-0.1, 0.1),
 }
+
+PTOP = 300.0
+RDGAS = 287.05
 
 
 def field_range(name: str) -> tuple[float, float]:
@@ -48,4 +55,25 @@ def synthetic_inputs(program, domain, seed: int = 7) -> dict[str, np.ndarray]:
                     continue
         lo, hi = field_range(name)
         out[name] = rng.uniform(lo, hi, shape)
+    for gz in ("gz", "gzc"):
+        if gz in out:
+            dm = next((out[n] for n in ("dm", "delpc", "delp") if n in out), None)
+            pt = next((out[n] for n in ("pt", "ptc") if n in out), None)
+            if dm is not None and pt is not None and dm.shape == out[gz].shape:
+                out[gz] = hydrostatic_gz(dm, pt, rng)
     return out
+
+
+def hydrostatic_gz(dm: np.ndarray, pt: np.ndarray, rng, hs_range=(0.0, 2000.0)) -> np.ndarray:
+    """Interface geopotential (last axis = nk+1 interfaces; the last layer
+    slot of dm/pt is unused) integrated upward from a random surface value,
+    with the log-mean layer pressure, plus 1e-3 relative noise."""
+    n = dm.shape[-1] - 1
+    pem = PTOP + np.concatenate([np.zeros(dm.shape[:-1] + (1,)), np.cumsum(dm[..., :n], axis=-1)], axis=-1)
+    gz = np.empty_like(dm)
+    gz[..., n] = rng.uniform(*hs_range, dm.shape[:-1])
+    for k in range(n - 1, -1, -1):
+        pm = dm[..., k] / np.log(pem[..., k + 1] / pem[..., k])
+        dz = RDGAS * pt[..., k] * dm[..., k] / pm
+        gz[..., k] = gz[..., k + 1] + dz * (1.0 + 1e-3 * rng.uniform(-1.0, 1.0, dz.shape))
+    return gz

@@ -24,7 +24,6 @@ from __future__ import annotations
 
 import hashlib
 import json
-import math
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Any
@@ -291,6 +290,10 @@ def known_programs() -> dict[str, Program]:
     return out
 
 
+def known_programs_names() -> list[str]:
+    return sorted(p.stem for p in PROGRAM_DIR.glob("*.json"))
+
+
 def as_program(program: Any) -> Program:
     """Accept a :class:`Program`, a manifest name, or a reference AST.
 
@@ -320,7 +323,3 @@ def as_program(program: Any) -> Program:
         consts={n: v for n, v in canon["consts"]},
         fp=fp,
     )
-
-
-def finite(x: float) -> bool:
-    return math.isfinite(x)

@@ -203,12 +203,200 @@ def tracer_2d_program(nq: int = NQ) -> str:
     return program_text(COMMON_CONSTS, fields, stencils, driver)
 
 
-def write_all() -> list[Path]:
-    progs = {
+# ---------------------------------------------------------------------------
+# K4: riem_solver_c — semi-implicit vertical acoustic solve (SIM1 type),
+# PAPER.md:595-603.  Program domain nk+1 (interfaces); layer statements use
+# interval(0, -1) (the DSL cannot write level nk of an nk domain,
+# validate.py:266-276).
+# ---------------------------------------------------------------------------
+
+RIEM_CONSTS = [
+    ("ptop", "300.0"),
+    ("rdgas", "287.05"),
+    ("grav", "9.80665"),
+    ("gama", "1.4"),          # 1 / (1 - kappa)
+    ("p_fac", "0.05"),
+]
+
+
+def riem_stencils(dm: str, pt: str, w: str, gz_in: str, ws: str, pef: str, gz_out: str,
+                  dt: str = "dt", sfx: str = "") -> list:
+    """The riem_solver_c stencil sequence (7 stencils; the paper's version
+    is 3 GT4Py stencils / 22 kernels).  ``gz_out`` may equal ``gz_in``;
+    ``sfx`` suffixes temporaries and stencil names."""
+    T = lambda n: f"{n}{sfx}"  # noqa: E731
+    pem, dz, pm, pe, grat, bb, dd = T("pem"), T("dzc"), T("pmc"), T("pec"), T("grat"), T("bbc"), T("ddc")
+    bet, gam, pp, aa, bw, gw, w2, pe2 = T("betp"), T("gamp"), T("ppc"), T("aac"), T("betw"), T("gamw"), T("w2c"), T("pe2c")
+    t1g = f"gama * 2.0 * {dt} * {dt}"
+    st = [
+        (T("riem_pem"), [], [
+            ("FORWARD", "0, 1", [f"{pem} = ptop"]),
+            ("FORWARD", "1, None", [f"{pem} = {pem}[0, 0, -1] + {dm}[0, 0, -1]"]),
+        ]),
+        (T("riem_layer"), [], [
+            ("PARALLEL", "0, -1", [
+                f"{dz} = ({gz_in}[0, 0, 1] - {gz_in}) / grav",
+                f"{pm} = {dm} / log({pem}[0, 0, 1] / {pem})",
+                f"{pe} = {dm} * rdgas * {pt} / ({gz_in} - {gz_in}[0, 0, 1]) - {pm}",
+            ]),
+        ]),
+        (T("riem_coef"), [], [
+            ("PARALLEL", "0, -2", [
+                f"{grat} = {dm} / {dm}[0, 0, 1]",
+                f"{bb} = 2.0 * (1.0 + {grat})",
+                f"{dd} = 3.0 * ({pe} + {grat} * {pe}[0, 0, 1])",
+            ]),
+            ("PARALLEL", "-2, -1", [
+                f"{bb} = 2.0",
+                f"{dd} = 3.0 * {pe}",
+            ]),
+        ]),
+        (T("riem_pp_fwd"), [], [
+            ("FORWARD", "0, 1", [f"{bet} = {bb}", f"{pp} = 0.0"]),
+            ("FORWARD", "1, 2", [
+                f"{pp} = {dd}[0, 0, -1] / {bet}[0, 0, -1]",
+                f"{gam} = {grat}[0, 0, -1] / {bet}[0, 0, -1]",
+                f"{bet} = {bb} - {gam}",
+            ]),
+            ("FORWARD", "2, -1", [
+                f"{pp} = ({dd}[0, 0, -1] - {pp}[0, 0, -1]) / {bet}[0, 0, -1]",
+                f"{gam} = {grat}[0, 0, -1] / {bet}[0, 0, -1]",
+                f"{bet} = {bb} - {gam}",
+            ]),
+            ("FORWARD", "-1, None", [f"{pp} = ({dd}[0, 0, -1] - {pp}[0, 0, -1]) / {bet}[0, 0, -1]"]),
+        ]),
+        (T("riem_pp_bwd"), [], [
+            ("BACKWARD", "1, -1", [f"{pp} = {pp} - {gam} * {pp}[0, 0, 1]"]),
+        ]),
+        (T("riem_w_fwd"), [], [
+            ("PARALLEL", "1, -1", [f"{aa} = {t1g} / ({dz}[0, 0, -1] + {dz}) * ({pem} + {pp})"]),
+            ("PARALLEL", "-1, None", [f"{aa} = {t1g} / {dz}[0, 0, -1] * ({pem} + {pp})"]),
+        ]),
+        (T("riem_w_sweep"), [], [
+            ("FORWARD", "0, 1", [
+                f"{bw} = {dm} - {aa}[0, 0, 1]",
+                f"{w2} = ({dm} * {w} + {dt} * {pp}[0, 0, 1]) / {bw}",
+            ]),
+            ("FORWARD", "1, -2", [
+                f"{gw} = {aa} / {bw}[0, 0, -1]",
+                f"{bw} = {dm} - ({aa} + {aa}[0, 0, 1] + {aa} * {gw})",
+                f"{w2} = ({dm} * {w} + {dt} * ({pp}[0, 0, 1] - {pp}) - {aa} * {w2}[0, 0, -1]) / {bw}",
+            ]),
+            ("FORWARD", "-2, -1", [
+                f"{gw} = {aa} / {bw}[0, 0, -1]",
+                f"{bw} = {dm} - ({aa} + {aa}[0, 0, 1] + {aa} * {gw})",
+                f"{w2} = ({dm} * {w} + {dt} * ({pp}[0, 0, 1] - {pp}) - {aa}[0, 0, 1] * {ws} - {aa} * {w2}[0, 0, -1]) / {bw}",
+            ]),
+        ]),
+        (T("riem_w_back"), [], [
+            ("BACKWARD", "0, -2", [f"{w2} = {w2} - {gw}[0, 0, 1] * {w2}[0, 0, 1]"]),
+        ]),
+        (T("riem_pe"), [], [
+            ("FORWARD", "0, 1", [f"{pe2} = 0.0"]),
+            ("FORWARD", "1, None", [f"{pe2} = {pe2}[0, 0, -1] + {dm}[0, 0, -1] * ({w2}[0, 0, -1] - {w}[0, 0, -1]) / {dt}"]),
+        ]),
+        (T("riem_out"), [], [
+            ("PARALLEL", "...", [f"{pef} = {pe2} + {pem}"]),
+        ]),
+    ]
+    gz_lines = []
+    if gz_out != gz_in:
+        gz_lines.append(("BACKWARD", "-1, None", [f"{gz_out} = {gz_in}"]))
+    gz_lines.append(("BACKWARD", "0, -1", [
+        f"{gz_out} = {gz_out}[0, 0, 1] + {dm} * rdgas * {pt} / max(p_fac * {pm}, {pm} + 0.5 * ({pe2} + {pe2}[0, 0, 1]))",
+    ]))
+    st.append((T("riem_gz"), [], gz_lines))
+    return st
+
+
+def riem_solver_c_program() -> str:
+    fields = [("dm", IJK, False), ("pt", IJK, False), ("w", IJK, False), ("gz", IJK, False),
+              ("ws", IJ, False), ("pef", IJK, False)]
+    stencils = riem_stencils("dm", "pt", "w", "gz", "ws", "pef", "gz")
+    return program_text(RIEM_CONSTS + [("dt", "18.75")], fields, stencils, [f"{s[0]}()" for s in stencils])
+
+
+# ---------------------------------------------------------------------------
+# K5: remap_profile — PPM sub-grid profile for vertical remapping
+# (cs_profile-type edge solve + Colella-Woodward monotonicity), PAPER.md:87-89.
+# Program domain nk+1: edge values live on interfaces.
+# ---------------------------------------------------------------------------
+
+
+def remap_stencils(q: str, delp: str, a2: str, a3: str, a4: str, sfx: str = "") -> list:
+    T = lambda n: f"{n}{sfx}"  # noqa: E731
+    grat, bet, gam, qe, d4, abot = T("grat_r"), T("bet_r"), T("gam_r"), T("qe_r"), T("d4_r"), T("abot_r")
+    al, ar, ext, da1, a6, a6da, da2 = T("al_r"), T("ar_r"), T("ext_r"), T("da1_r"), T("a6_r"), T("a6da_r"), T("da2_r")
+    return [
+        (T("remap_edge_fwd"), [], [
+            ("FORWARD", "0, 1", [
+                f"{grat} = {delp}[0, 0, 1] / {delp}",
+                f"{bet} = {grat} * ({grat} + 0.5)",
+                f"{qe} = (({grat} + {grat}) * ({grat} + 1.0) * {q} + {q}[0, 0, 1]) / {bet}",
+                f"{gam} = (1.0 + {grat} * ({grat} + 1.5)) / {bet}",
+            ]),
+            ("FORWARD", "1, -1", [
+                f"{d4} = {delp}[0, 0, -1] / {delp}",
+                f"{bet} = 2.0 + {d4} + {d4} - {gam}[0, 0, -1]",
+                f"{qe} = (3.0 * ({q}[0, 0, -1] + {d4} * {q}) - {qe}[0, 0, -1]) / {bet}",
+                f"{gam} = {d4} / {bet}",
+            ]),
+            ("FORWARD", "-1, None", [
+                f"{abot} = 1.0 + {d4}[0, 0, -1] * ({d4}[0, 0, -1] + 1.5)",
+                f"{qe} = (2.0 * {d4}[0, 0, -1] * ({d4}[0, 0, -1] + 1.0) * {q}[0, 0, -1] + {q}[0, 0, -2] - {abot} * {qe}[0, 0, -1]) / "
+                f"({d4}[0, 0, -1] * ({d4}[0, 0, -1] + 0.5) - {abot} * {gam}[0, 0, -1])",
+            ]),
+        ]),
+        (T("remap_edge_bwd"), [], [
+            ("BACKWARD", "0, -1", [f"{qe} = {qe} - {gam} * {qe}[0, 0, 1]"]),
+        ]),
+        (T("remap_a4"), [], [
+            ("PARALLEL", "0, -1", [
+                f"{al} = {qe}",
+                f"{ar} = {qe}[0, 0, 1]",
+                f"{ext} = ({ar} - {q}) * ({q} - {al})",
+                f"{da1} = {ar} - {al}",
+                f"{a6} = 3.0 * (2.0 * {q} - ({al} + {ar}))",
+                f"{a6da} = {a6} * {da1}",
+                f"{da2} = {da1} * {da1}",
+                f"{a2} = select({ext} <= 0.0, {q}, select({a6da} > {da2}, 3.0 * {q} - 2.0 * {ar}, {al}))",
+                f"{a3} = select({ext} <= 0.0, {q}, select({a6da} < -{da2}, 3.0 * {q} - 2.0 * {al}, {ar}))",
+                f"{a4} = 3.0 * (2.0 * {q} - ({a2} + {a3}))",
+            ]),
+        ]),
+    ]
+
+
+def remap_profile_program() -> str:
+    fields = [("q", IJK, False), ("delp", IJK, False), ("a4_2", IJK, False), ("a4_3", IJK, False),
+              ("a4_4", IJK, False)]
+    st = remap_stencils("q", "delp", "a4_2", "a4_3", "a4_4")
+    return program_text([], fields, st, [f"{s[0]}()" for s in st])
+
+
+def remap_tracers_program(nq: int = NQ) -> str:
+    fields = [("delp", IJK, False)]
+    st = []
+    for n in range(nq):
+        fields += [(f"q{n}", IJK, False), (f"q{n}_a2", IJK, False), (f"q{n}_a3", IJK, False), (f"q{n}_a4", IJK, False)]
+        st += remap_stencils(f"q{n}", "delp", f"q{n}_a2", f"q{n}_a3", f"q{n}_a4", sfx=f"_{n}")
+    return program_text([], fields, st, [f"{s[0]}()" for s in st])
+
+
+def programs() -> dict:
+    """name -> .stn text of every shipped program."""
+    return {
         "copy": copy_program(),
         "fv_tp_2d": fv_tp_2d_program(),
         "tracer_2d": tracer_2d_program(),
+        "riem_solver_c": riem_solver_c_program(),
+        "remap_profile": remap_profile_program(),
+        "remap_tracers": remap_tracers_program(),
     }
+
+
+def write_all() -> list[Path]:
+    progs = programs()
     paths = []
     for name, text in progs.items():
         p = HERE / f"{name}.stn"

@@ -34,6 +34,9 @@ CASES = [
     ("fv_tp_2d", "periodic", (16, 14, 3), (False, False, False, False), 7),
     ("fv_tp_2d", "tile", (17, 15, 2), (True, True, True, True), 11),
     ("tracer_2d", "periodic", (14, 16, 2), (False, False, False, False), 7),
+    ("riem_solver_c", "column", (5, 4, 17), (True, True, True, True), 7),
+    ("remap_profile", "column", (5, 4, 17), (True, True, True, True), 7),
+    ("remap_tracers", "column", (3, 2, 9), (True, True, True, True), 7),
 ]
 
 

@@ -23,11 +23,18 @@ def engine():
     return executor
 
 
+# Programs whose .stn uses log/exp (oracle extension): CUDA libdevice and the
+# host libm may differ in the last ulp there, so they are held to the
+# per-stencil tolerance of the north star (max relative error <= 1e-12,
+# denominator max(|ref|, 1e-300)); every other program must be bitwise.
+RTOL = {"riem_solver_c": 1e-12}
+
+
 @pytest.mark.parametrize("key,meta", list(golden_cases()))
 def test_cuda_matches_reference_golden(engine, key, meta):
     inputs, ref_out = load_golden(key)
     got = engine.run_b200(meta["program"], inputs, meta["domain"], placement=meta["placement"])
-    assert_outputs_equal(got, ref_out)
+    assert_outputs_equal(got, ref_out, rtol=RTOL.get(meta["program"], 0.0))
 
 
 CASES = [
@@ -38,6 +45,10 @@ CASES = [
     ("fv_tp_2d", (64, 16, 3), False, 5),
     ("tracer_2d", (48, 48, 6), False, 6),
     ("tracer_2d", (35, 29, 3), True, 7),
+    ("riem_solver_c", (48, 48, 17), False, 8),
+    ("riem_solver_c", (33, 7, 81), True, 9),
+    ("remap_profile", (48, 48, 17), False, 10),
+    ("remap_tracers", (20, 12, 81), False, 11),
 ]
 
 
@@ -49,7 +60,19 @@ def test_cuda_matches_oracle(engine, name, domain, tile, seed):
     placement = (tile,) * 4
     got = engine.run_b200(name, inputs, domain, placement=placement)
     ref = interp.run_program(name, inputs, domain, interp.Placement(*placement))
-    assert_outputs_equal(got, ref)
+    assert_outputs_equal(got, ref, rtol=RTOL.get(name, 0.0))
+
+
+@pytest.mark.parametrize("name", ["riem_solver_c", "remap_profile"])
+def test_cuda_column_full_size_c2(engine, name):
+    """192x192 columns x 80 layers (program domain nk = 81) vs the oracle."""
+    from paper_2205_04148_b200.inputs import synthetic_inputs
+
+    domain = (192, 192, 81)
+    inputs = synthetic_inputs(name, domain, 2205)
+    got = engine.run_b200(name, inputs, domain)
+    ref = interp.run_program(name, inputs, domain)
+    assert_outputs_equal(got, ref, rtol=RTOL.get(name, 0.0))
 
 
 def test_cuda_fv_tp_2d_full_size_c2(engine):

@@ -56,14 +56,17 @@ needs_ref = pytest.mark.skipif(not _ref.available(), reason="reference package n
 
 
 @needs_ref
-@pytest.mark.parametrize("name", ["copy", "fv_tp_2d", "tracer_2d"])
+@pytest.mark.parametrize("name", ["copy", "fv_tp_2d", "tracer_2d", "riem_solver_c", "remap_profile"])
 def test_oracle_matches_live_reference(name):
     from paper_2205_04148_b200.inputs import synthetic_inputs
     from paper_2205_04148_b200.program import PROGRAM_DIR
 
     ref = _ref.load()
     prog = ref.parse_program((PROGRAM_DIR / f"{name}.stn").read_text())
-    for domain, placement, seed in [((15, 17, 3), (False,) * 4, 1), ((16, 16, 2), (True,) * 4, 2)]:
+    cases = [((15, 17, 3), (False,) * 4, 1), ((16, 16, 2), (True,) * 4, 2)]
+    if name.startswith(("riem", "remap")):
+        cases = [((4, 3, 12), (True,) * 4, 1), ((3, 3, 30), (False,) * 4, 2)]
+    for domain, placement, seed in cases:
         inputs = synthetic_inputs(name, domain, seed)
         a = ref.run_reference(prog, inputs, domain, placement=ref.RankPlacement(*placement))
         b = interp.run_program(name, inputs, domain, interp.Placement(*placement))

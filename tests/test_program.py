@@ -31,16 +31,15 @@ def test_stn_regenerates_identically():
     """The committed .stn files are exactly what the templates emit."""
     from paper_2205_04148_b200.programs import templates
 
-    for name, fn in [("copy", templates.copy_program), ("fv_tp_2d", templates.fv_tp_2d_program),
-                     ("tracer_2d", templates.tracer_2d_program)]:
+    for name, text_now in templates.programs().items():
         text = (P.PROGRAM_DIR / f"{name}.stn").read_text()
-        assert text.split("\n", 1)[1] == fn()
+        assert text.split("\n", 1)[1] == text_now, name
 
 
 @needs_ref
 def test_reference_ast_dispatches_by_fingerprint():
     ref = _ref.load()
-    for name in ("copy", "fv_tp_2d", "tracer_2d"):
+    for name in P.known_programs_names():
         prog = ref.parse_program((P.PROGRAM_DIR / f"{name}.stn").read_text())
         got = P.as_program(prog)
         assert got.name == name
