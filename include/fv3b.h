@@ -99,6 +99,40 @@ int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns,
                        const fv3b_domain* d, void* stream);
 
+/* K2  c_sw.stn — C-grid half step.  fields: u, v, delp, pt, w (3-D); dx, dy,
+ *     dxc, dyc, rdxc, rdyc, rarea, rarea_c, fc (2-D); uc, vc, delpc, ptc, wc
+ *     (3-D outputs).  scalars: dt2. */
+int fv3b_c_sw(const fv3b_field* f, int nf, const double* s, int ns,
+              const fv3b_domain* d, void* stream);
+
+/* K2+K4  c_grid.stn — c_sw + riem_solver_c + p_grad_c fused (program domain
+ *     nk = layers + 1).  fields: u, v, delp, pt, w, gz (3-D); the 9 c_sw
+ *     metrics, ws (2-D); uc, vc (3-D outputs); scratch delpcc, ptcc, wcc, pkc,
+ *     gzc (3-D, >= 1-cell halo).  scalars: dt2, ptop, rdgas, grav, gama,
+ *     p_fac. */
+int fv3b_c_grid(const fv3b_field* f, int nf, const double* s, int ns,
+                const fv3b_domain* d, void* stream);
+
+/* K3  d_sw.stn — D-grid Lagrangian step (two fused kernels).  fields: u, v,
+ *     w, delp, pt, uc, vc, cx, cy, xfa, yfa, mfx, mfy (3-D); dx, dy, dxc, dyc,
+ *     rdx, rdy, rdxa, rdya, area, rarea, rarea_c, f0 (2-D); u, v, w, delp, pt,
+ *     cx, cy, xfa, yfa, mfx, mfy outputs (3-D; accumulators may alias).
+ *     scalars: ppm_p1, ppm_p2, dt, dddmp, d2_bg, da_min, damp_w. */
+int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns,
+              const fv3b_domain* d, void* stream);
+
+/* nh_d.stn — D-grid vertical solve (riem_solver3 role), program domain
+ *     nk = layers + 1.  fields: delp, pt, w, gz (3-D), ws (2-D), pef,
+ *     gz_out, w_out (3-D).  scalars: ptop, rdgas, grav, gama, p_fac, dt. */
+int fv3b_nh_d(const fv3b_field* f, int nf, const double* s, int ns,
+              const fv3b_domain* d, void* stream);
+
+/* p_grad_d.stn — D-grid pressure-gradient force (nh_p_grad role), program
+ *     domain nk = layers + 1.  fields: u, v, pef, gz (3-D), rdx, rdy (2-D),
+ *     u_out, v_out (3-D).  scalars: dt. */
+int fv3b_p_grad_d(const fv3b_field* f, int nf, const double* s, int ns,
+                  const fv3b_domain* d, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

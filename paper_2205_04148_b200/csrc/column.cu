@@ -13,7 +13,7 @@
 // host libm) differ in the last ulp.
 #include <math.h>
 
-#include "common.cuh"
+#include "column.cuh"
 
 namespace fv3b {
 
@@ -25,12 +25,6 @@ __device__ __forceinline__ double np_max(double a, double b) {
   return a > b ? a : (b > a ? b : a);
 }
 
-struct RiemArgs {
-  View dm, pt, w, gz, ws, pef, gzo;
-  int ilo, jlo, ni_ext, nj_ext;  // column range [ilo, ilo+ni_ext) x [jlo, jlo+nj_ext)
-  int nk;                        // layers; interfaces 0..nk
-  double dt, ptop, rdgas, grav, gama, p_fac;
-};
 
 // Statement-for-statement restatement of templates.riem_stencils.
 __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
@@ -139,9 +133,12 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
   // ---- pass D (backward): riem_w_back ----------------------------------
   {
     double w2n = AT(S2, nk - 1);
+    double* wo = a.has_wout ? a.wout.ptr(i, j, 0) : nullptr;
+    if (wo) wo[(nk - 1) * a.wout.sk] = w2n;
     for (int l = nk - 2; l >= 0; --l) {
       const double w2l = AT(S2, l) - AT(S1, l + 1) * w2n;
       AT(S2, l) = w2l;
+      if (wo) wo[l * a.wout.sk] = w2l;
       w2n = w2l;
     }
   }
@@ -296,6 +293,7 @@ extern "C" int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, 
   FV3B_TRY(view_of(f[6], 3, *d, h0, "gz_out", &a.gzo));
   if (a.dm.sk != a.pt.sk || a.dm.sk != a.w.sk || a.dm.sk != a.gz.sk)
     return fail(FV3B_ELAYOUT, "fv3b_riem_solver_c: input K strides differ");
+  a.has_wout = false;
   a.ilo = 0;
   a.jlo = 0;
   a.ni_ext = d->ni;

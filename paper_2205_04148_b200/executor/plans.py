@@ -33,6 +33,14 @@ class LaunchCtx:
     nk: int                                # program vertical domain
     on_launch: Callable | None = None      # (node, start_event, end_event) timing hook
     launches: list = field(default_factory=list)
+    workspace: dict = field(default_factory=dict)  # device scratch for fused temporaries
+
+    def scratch(self, name: str) -> _lib.Field:
+        """3-D device buffer for a temporary that crosses kernels of one
+        fused plan (allocated once per state, reused across calls)."""
+        if name not in self.workspace:
+            self.workspace[name] = self.grid.new3(device=self.fields[next(iter(self.fields))].device)
+        return self.grid.abi(self.workspace[name])
 
     def f(self, name: str, rank: int | None = None) -> _lib.Field:
         return self.grid.abi(self.fields[name], rank)
@@ -162,8 +170,75 @@ class RemapPlan(Plan):
         ctx.call(prog.trace[0][0] + "_0", "fv3b_remap_profile", fields, [])
 
 
+C_METRICS = ("dx", "dy", "dxc", "dyc", "rdxc", "rdyc", "rarea", "rarea_c", "fc")
+D_METRICS = ("dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxa", "rdya", "area", "rarea", "rarea_c", "f0")
+D_STATE = ("u", "v", "w", "delp", "pt", "uc", "vc", "cx", "cy", "xfa", "yfa", "mfx", "mfy")
+D_OUT = ("u", "v", "w", "delp", "pt", "cx", "cy", "xfa", "yfa", "mfx", "mfy")
+
+
+class CswPlan(Plan):
+    name = "c_sw"
+    stencils = ("c_sw_winds", "c_sw_transport", "c_sw_ke_vort", "c_sw_update")
+
+    def run(self, prog, ctx):
+        s = prog.scalars(prog.trace[0][1])
+        fields = [ctx.f(n) for n in ("u", "v", "delp", "pt", "w")] + [ctx.f(m, 2) for m in C_METRICS]
+        fields += [ctx.o(n) for n in ("uc", "vc", "delpc", "ptc", "wc")]
+        ctx.call("c_sw_winds_0", "fv3b_c_sw", fields, [s["dt2"]])
+
+
+class CGridPlan(Plan):
+    name = "c_grid"
+    stencils = ("c_sw_winds", "c_sw_transport", "c_sw_ke_vort", "c_sw_update") + tuple(
+        f"{n}_c" for n in RiemSolverCPlan.stencils) + ("p_grad_c",)
+
+    def run(self, prog, ctx):
+        s = prog.scalars(prog.trace[0][1])
+        fields = [ctx.f(n) for n in ("u", "v", "delp", "pt", "w", "gz")] + [ctx.f(m, 2) for m in C_METRICS]
+        fields += [ctx.f("ws", 2), ctx.o("uc"), ctx.o("vc")]
+        fields += [ctx.scratch(n) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc")]
+        ctx.call("c_sw_winds_0", "fv3b_c_grid", fields,
+                 [s["dt2"], s["ptop"], s["rdgas"], s["grav"], s["gama"], s["p_fac"]])
+
+
+class DswPlan(Plan):
+    name = "d_sw"
+    stencils = ("d_sw_courant", "d_sw_mass", "d_sw_heat", "d_sw_vert", "d_sw_ke", "d_sw_vort", "d_sw_damp",
+                "d_sw_update")
+
+    def run(self, prog, ctx):
+        s = prog.scalars(prog.trace[0][1])
+        fields = [ctx.f(n) for n in D_STATE] + [ctx.f(m, 2) for m in D_METRICS] + [ctx.o(n) for n in D_OUT]
+        ctx.call("d_sw_courant_0", "fv3b_d_sw", fields,
+                 [s["ppm_p1"], s["ppm_p2"], s["dt"], s["dddmp"], s["d2_bg"], s["da_min"], s["damp_w"]])
+
+
+class NhDPlan(Plan):
+    name = "nh_d"
+    stencils = tuple(f"{n}_d" for n in RiemSolverCPlan.stencils) + ("nh_d_w",)
+
+    def run(self, prog, ctx):
+        s = prog.scalars(prog.trace[0][1])
+        fields = [ctx.f(n) for n in ("delp", "pt", "w", "gz")] + [ctx.f("ws", 2)]
+        fields += [ctx.o("pef"), ctx.o("gz"), ctx.o("w")]
+        ctx.call("riem_pem_d_0", "fv3b_nh_d", fields,
+                 [s["ptop"], s["rdgas"], s["grav"], s["gama"], s["p_fac"], s["dt"]])
+
+
+class PGradDPlan(Plan):
+    name = "p_grad_d"
+    stencils = ("p_grad_d_corners", "p_grad_d")
+
+    def run(self, prog, ctx):
+        s = prog.scalars(prog.trace[0][1])
+        fields = [ctx.f(n) for n in ("u", "v", "pef", "gz")] + [ctx.f("rdx", 2), ctx.f("rdy", 2)]
+        fields += [ctx.o("u"), ctx.o("v")]
+        ctx.call("p_grad_d_corners_0", "fv3b_p_grad_d", fields, [s["dt"]])
+
+
 PLANS: dict[str, Plan] = {p.name: p for p in (CopyPlan(), FvTp2dPlan(), Tracer2dPlan(), RiemSolverCPlan(),
-                                              RemapPlan("remap_profile"), RemapPlan("remap_tracers"))}
+                                              RemapPlan("remap_profile"), RemapPlan("remap_tracers"), CswPlan(),
+                                              CGridPlan(), DswPlan(), NhDPlan(), PGradDPlan())}
 
 
 def plan_for(prog: Program) -> Plan:

@@ -49,11 +49,15 @@ class Uploaded:
     fields: dict[str, torch.Tensor]
     outputs: dict[str, torch.Tensor]
     placement: tuple
+    workspace: dict = None
 
     def ctx(self, stream: int | None = None, on_launch=None) -> LaunchCtx:
         if stream is None:
             stream = torch.cuda.current_stream().cuda_stream
-        return LaunchCtx(self.grid, self.fields, self.outputs, self.placement, stream, self.domain[2], on_launch)
+        if self.workspace is None:
+            self.workspace = {}
+        return LaunchCtx(self.grid, self.fields, self.outputs, self.placement, stream, self.domain[2], on_launch,
+                         workspace=self.workspace)
 
     def download(self) -> dict[str, np.ndarray]:
         out = {}

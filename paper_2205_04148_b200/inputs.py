@@ -28,17 +28,33 @@ _RANGES = {
     "w": (-1.0, 1.0), "wc": (-1.0, 1.0), "ws": (-0.1, 0.1),
 }
 
+# Programs on a physical grid (they declare metric terms): ~10 km cells,
+# f-plane Coriolis, winds of tens of m/s.
+_PHYSICAL = {
+    "u": (-15.0, 15.0), "v": (-15.0, 15.0), "uc": (-15.0, 15.0), "vc": (-15.0, 15.0),
+    "dx": (9.5e3, 1.05e4), "dy": (9.5e3, 1.05e4), "dxc": (9.5e3, 1.05e4), "dyc": (9.5e3, 1.05e4),
+    "rdxa": (0.95e-4, 1.05e-4), "rdya": (0.95e-4, 1.05e-4),
+    "rdx": (0.95e-4, 1.05e-4), "rdy": (0.95e-4, 1.05e-4), "rdxc": (0.95e-4, 1.05e-4), "rdyc": (0.95e-4, 1.05e-4),
+    "area": (0.9e8, 1.1e8), "rarea": (0.9e-8, 1.1e-8), "rarea_c": (0.9e-8, 1.1e-8),
+    "fc": (0.9e-4, 1.1e-4), "f0": (0.9e-4, 1.1e-4),
+    "cx": (-1.0, 1.0), "cy": (-1.0, 1.0), "xfa": (-1.0, 1.0), "yfa": (-1.0, 1.0),
+    "mfx": (-1.0, 1.0), "mfy": (-1.0, 1.0),
+}
+
 PTOP = 300.0
 RDGAS = 287.05
 
 
-def field_range(name: str) -> tuple[float, float]:
+def field_range(name: str, physical: bool = False) -> tuple[float, float]:
+    if physical and name in _PHYSICAL:
+        return _PHYSICAL[name]
     return _RANGES.get(name, (0.1, 10.0))
 
 
 def synthetic_inputs(program, domain, seed: int = 7) -> dict[str, np.ndarray]:
     prog = as_program(program)
     rng = np.random.default_rng(seed)
+    physical = any(m in prog.fields for m in ("dx", "dy", "rdx", "rdy"))
     out = {}
     for name, info in prog.fields.items():
         if info.temporary:
@@ -53,8 +69,14 @@ def synthetic_inputs(program, domain, seed: int = 7) -> dict[str, np.ndarray]:
                 if all(s.stop <= m for s, m in zip(sl, out[name[1:]].shape)):
                     out[name] = 1.0 / out[name[1:]][sl]
                     continue
-        lo, hi = field_range(name)
+        lo, hi = field_range(name, physical)
         out[name] = rng.uniform(lo, hi, shape)
+    if "pef" in out and "gz" in out and not any(n in out for n in ("dm", "delp", "delpc")):
+        # interface pressure and geopotential of a random hydrostatic column
+        dm = rng.uniform(900.0, 1300.0, out["pef"].shape)
+        pt = rng.uniform(270.0, 300.0, out["pef"].shape)
+        out["pef"] = PTOP + np.concatenate([np.zeros(dm.shape[:-1] + (1,)), np.cumsum(dm[..., :-1], axis=-1)], axis=-1)
+        out["gz"] = hydrostatic_gz(dm, pt, rng)
     for gz in ("gz", "gzc"):
         if gz in out:
             dm = next((out[n] for n in ("dm", "delpc", "delp") if n in out), None)

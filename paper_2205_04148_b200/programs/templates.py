@@ -383,6 +383,195 @@ def remap_tracers_program(nq: int = NQ) -> str:
     return program_text([], fields, st, [f"{s[0]}()" for s in st])
 
 
+# ---------------------------------------------------------------------------
+# K2: c_sw — C-grid half step (d2a2c winds, transportdelp, C-grid KE and
+# vorticity, uc/vc update).  Orthogonal-metric form; the
+# four tile-corner circulation fixes are regions that fire only on owned
+# tile corners (cubed sphere).  ``layer`` is the interval of layer
+# statements: "..." in an nk domain, "0, -1" in the nk+1 fused C-grid program.
+# ---------------------------------------------------------------------------
+
+C_METRICS = ["dx", "dy", "dxc", "dyc", "rdxc", "rdyc", "rarea", "rarea_c", "fc"]
+
+
+def c_sw_stencils(layer: str, out_delpc: str, out_ptc: str, out_wc: str, uc: str, vc: str) -> list:
+    return [
+        ("c_sw_winds", [], [("PARALLEL", layer, [
+            f"ua = {A2} * (u[0, -1, 0] + u[0, 2, 0]) + {A1} * (u + u[0, 1, 0])",
+            f"va = {A2} * (v[-1, 0, 0] + v[2, 0, 0]) + {A1} * (v + v[1, 0, 0])",
+            f"uct = {A2} * (ua[-2, 0, 0] + ua[1, 0, 0]) + {A1} * (ua[-1, 0, 0] + ua)",
+            f"vct = {A2} * (va[0, -2, 0] + va[0, 1, 0]) + {A1} * (va[0, -1, 0] + va)",
+        ])]),
+        ("c_sw_transport", [], [("PARALLEL", layer, [
+            "utc = dt2 * uct * dy",
+            "vtc = dt2 * vct * dx",
+            "fxc = utc * select(utc > 0.0, delp[-1, 0, 0], delp)",
+            "fyc = vtc * select(vtc > 0.0, delp[0, -1, 0], delp)",
+            "fxp = fxc * select(utc > 0.0, pt[-1, 0, 0], pt)",
+            "fyp = fyc * select(vtc > 0.0, pt[0, -1, 0], pt)",
+            "fxw = fxc * select(utc > 0.0, w[-1, 0, 0], w)",
+            "fyw = fyc * select(vtc > 0.0, w[0, -1, 0], w)",
+            f"{out_delpc} = delp + (fxc - fxc[1, 0, 0] + fyc - fyc[0, 1, 0]) * rarea",
+            f"{out_ptc} = (pt * delp + (fxp - fxp[1, 0, 0] + fyp - fyp[0, 1, 0]) * rarea) / {out_delpc}",
+            f"{out_wc} = (w * delp + (fxw - fxw[1, 0, 0] + fyw - fyw[0, 1, 0]) * rarea) / {out_delpc}",
+        ])]),
+        ("c_sw_ke_vort", [], [("PARALLEL", layer, [
+            "keu = select(ua > 0.0, uct, uct[1, 0, 0])",
+            "kev = select(va > 0.0, vct, vct[0, 1, 0])",
+            "kec = 0.5 * dt2 * (ua * keu + va * kev)",
+            "vortc = fc + rarea_c * (uct[0, -1, 0] * dxc[0, -1] - uct * dxc + vct * dyc - vct[-1, 0, 0] * dyc[-1, 0])",
+            *_region("i_start, j_start", ["vortc = fc + rarea_c * (vct * dyc - uct * dxc - vct[-1, 0, 0] * dyc[-1, 0])"]),
+            *_region("i_end, j_start", ["vortc = fc + rarea_c * (uct[0, -1, 0] * dxc[0, -1] - uct * dxc - vct[-1, 0, 0] * dyc[-1, 0])"]),
+            *_region("i_end, j_end", ["vortc = fc + rarea_c * (uct[0, -1, 0] * dxc[0, -1] + vct * dyc - vct[-1, 0, 0] * dyc[-1, 0])"]),
+            *_region("i_start, j_end", ["vortc = fc + rarea_c * (uct[0, -1, 0] * dxc[0, -1] - uct * dxc + vct * dyc)"]),
+        ])]),
+        ("c_sw_update", [], [("PARALLEL", layer, [
+            "fy1c = dt2 * v",
+            f"{uc} = uct + fy1c * select(fy1c > 0.0, vortc, vortc[0, 1, 0]) + rdxc * (kec[-1, 0, 0] - kec)",
+            "fx1c = dt2 * u",
+            f"{vc} = vct - fx1c * select(fx1c > 0.0, vortc, vortc[1, 0, 0]) + rdyc * (kec[0, -1, 0] - kec)",
+        ])]),
+    ]
+
+
+def c_sw_program() -> str:
+    fields = [(n, IJK, False) for n in ("u", "v", "delp", "pt", "w", "uc", "vc", "delpc", "ptc", "wc")]
+    fields += [(m, IJ, False) for m in C_METRICS]
+    st = c_sw_stencils("...", "delpc", "ptc", "wc", "uc", "vc")
+    return program_text([("dt2", "18.75")], fields, st, [f"{x[0]}()" for x in st])
+
+
+def c_grid_program() -> str:
+    """c_sw + riem_solver_c + p_grad_c fused in one nk+1 program, so the
+    C-grid thickness/temperature/w and the solver's pressure/geopotential
+    are temporaries (extended one cell where p_grad_c needs them) and no
+    halo exchange is needed between them (FV3 computes them on the
+    extended domain for the same reason)."""
+    fields = [(n, IJK, False) for n in ("u", "v", "delp", "pt", "w", "gz", "uc", "vc")]
+    fields += [(m, IJ, False) for m in C_METRICS] + [("ws", IJ, False)]
+    st = c_sw_stencils("0, -1", "delpcc", "ptcc", "wcc", "uc", "vc")
+    st += riem_stencils("delpcc", "ptcc", "wcc", "gz", "ws", "pkc", "gzc", dt="dt2", sfx="_c")
+    st.append(("p_grad_c", [], [("PARALLEL", "0, -1", [
+        "wkc = pkc[0, 0, 1] - pkc",
+        "uc = uc + dt2 * rdxc / (wkc[-1, 0, 0] + wkc) * ((gzc[-1, 0, 1] - gzc) * (pkc[0, 0, 1] - pkc[-1, 0, 0]) + "
+        "(gzc[-1, 0, 0] - gzc[0, 0, 1]) * (pkc[-1, 0, 1] - pkc))",
+        "vc = vc + dt2 * rdyc / (wkc[0, -1, 0] + wkc) * ((gzc[0, -1, 1] - gzc) * (pkc[0, 0, 1] - pkc[0, -1, 0]) + "
+        "(gzc[0, -1, 0] - gzc[0, 0, 1]) * (pkc[0, -1, 1] - pkc))",
+    ])]))
+    return program_text(RIEM_CONSTS + [("dt2", "18.75")], fields, st, [f"{x[0]}()" for x in st])
+
+
+# ---------------------------------------------------------------------------
+# K3: d_sw — D-grid Lagrangian step: Courant numbers from the C-grid winds,
+# fv_tp_2d of delp (mass fluxes) / pt / w (mass weighted), vorticity and
+# kinetic energy, vorticity transport, Smagorinsky-scaled divergence
+# damping (the paper's Smagorinsky listing with sqrt instead of **,
+# PAPER.md:532-537), u/v update, and the tracer-flux accumulators.
+# ---------------------------------------------------------------------------
+
+D_METRICS = ["dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxa", "rdya", "area", "rarea", "rarea_c", "f0"]
+D_CONSTS = [("dt", "37.5"), ("dddmp", "0.2"), ("d2_bg", "0.0"), ("da_min", "1.0"), ("damp_w", "0.02")]
+
+
+def d_sw_stencils() -> list:
+    courant = [
+        "xfx = dt * uc * dy",
+        "crx = select(uc > 0.0, dt * uc * rdxa[-1, 0], dt * uc * rdxa)",
+        "yfx = dt * vc * dx",
+        "cry = select(vc > 0.0, dt * vc * rdya[0, -1], dt * vc * rdya)",
+    ]
+    mass = fv_tp_2d("delp", "crx", "cry", "xfx", "yfx", "fxm", "fym", "d")
+    mass += ["delpn = delp + (fxm - fxm[1, 0, 0] + fym - fym[0, 1, 0]) * rarea"]
+    heat = fv_tp_2d("pt", "crx", "cry", "xfx", "yfx", "gxp", "gyp", "p", mfx="fxm", mfy="fym")
+    vert = fv_tp_2d("w", "crx", "cry", "xfx", "yfx", "hxw", "hyw", "w", mfx="fxm", mfy="fym")
+    ke = [
+        "ub = 0.5 * dt * (uc[0, -1, 0] + uc)",
+        "cub = select(ub > 0.0, ub * rdx[-1, 0], ub * rdx)",
+        *ppm_flux("x", "u", "cub", "uu", "ku"),
+        "vb = 0.5 * dt * (vc[-1, 0, 0] + vc)",
+        "cvb = select(vb > 0.0, vb * rdy[0, -1], vb * rdy)",
+        *ppm_flux("y", "v", "cvb", "vv", "kv"),
+        "ked = 0.5 * (ub * uu + vb * vv)",
+    ]
+    vort = ["wk = f0 + rarea * (u * dx - u[0, 1, 0] * dx[0, 1] + v[1, 0, 0] * dy[1, 0] - v * dy)"]
+    vort += fv_tp_2d("wk", "crx", "cry", "xfx", "yfx", "fxv", "fyv", "v")
+    damp = [
+        "divg = rarea_c * (u * dyc - u[-1, 0, 0] * dyc[-1, 0] + v * dxc - v[0, -1, 0] * dxc[0, -1])",
+        "tens = rarea_c * (u * dyc - u[-1, 0, 0] * dyc[-1, 0] - v * dxc + v[0, -1, 0] * dxc[0, -1])",
+        "smag = dt * sqrt(divg * divg + tens * tens)",
+        "dmp = da_min * max(d2_bg, min(0.2, dddmp * smag))",
+        "ddv = dmp * divg",
+    ]
+    update = [
+        "cx = cx + crx",
+        "cy = cy + cry",
+        "xfa = xfa + xfx",
+        "yfa = yfa + yfx",
+        "mfx = mfx + fxm",
+        "mfy = mfy + fym",
+        "pt = (pt * delp + (gxp - gxp[1, 0, 0] + gyp - gyp[0, 1, 0]) * rarea) / delpn",
+        "w = (w * delp + (hxw - hxw[1, 0, 0] + hyw - hyw[0, 1, 0]) * rarea) / delpn + "
+        "damp_w * (w[-1, 0, 0] + w[1, 0, 0] + w[0, -1, 0] + w[0, 1, 0] - 4.0 * w)",
+        "delp = delpn",
+        "u = (u * dx + ked - ked[1, 0, 0] + fyv) * rdx + (ddv[1, 0, 0] - ddv) * rdx",
+        "v = (v * dy + ked - ked[0, 1, 0] - fxv) * rdy + (ddv[0, 1, 0] - ddv) * rdy",
+    ]
+    return [
+        ("d_sw_courant", [], [("PARALLEL", "...", courant)]),
+        ("d_sw_mass", [], [("PARALLEL", "...", mass)]),
+        ("d_sw_heat", [], [("PARALLEL", "...", heat)]),
+        ("d_sw_vert", [], [("PARALLEL", "...", vert)]),
+        ("d_sw_ke", [], [("PARALLEL", "...", ke)]),
+        ("d_sw_vort", [], [("PARALLEL", "...", vort)]),
+        ("d_sw_damp", [], [("PARALLEL", "...", damp)]),
+        ("d_sw_update", [], [("PARALLEL", "...", update)]),
+    ]
+
+
+D_STATE = ["u", "v", "w", "delp", "pt", "uc", "vc", "cx", "cy", "xfa", "yfa", "mfx", "mfy"]
+
+
+def d_sw_program() -> str:
+    fields = [(n, IJK, False) for n in D_STATE] + [(m, IJ, False) for m in D_METRICS]
+    st = d_sw_stencils()
+    return program_text(COMMON_CONSTS + D_CONSTS, fields, st, [f"{x[0]}()" for x in st])
+
+
+# ---------------------------------------------------------------------------
+# D-grid nonhydrostatic update (FV3 riem_solver3 + nh_p_grad): the column
+# solve updates w, gz and the interface pressure; after a halo exchange of
+# pef/gz the pressure-gradient force is applied to the D-grid winds with
+# corner-averaged pressure and geopotential.  Both run in nk+1 domains.
+# ---------------------------------------------------------------------------
+
+
+def nh_d_program() -> str:
+    fields = [("delp", IJK, False), ("pt", IJK, False), ("w", IJK, False), ("gz", IJK, False),
+              ("ws", IJ, False), ("pef", IJK, False)]
+    st = riem_stencils("delp", "pt", "w", "gz", "ws", "pef", "gz", dt="dt", sfx="_d")
+    st.append(("nh_d_w", [], [("PARALLEL", "0, -1", ["w = w2c_d"])]))
+    return program_text(RIEM_CONSTS + [("dt", "37.5")], fields, st, [f"{x[0]}()" for x in st])
+
+
+def p_grad_d_program() -> str:
+    fields = [("u", IJK, False), ("v", IJK, False), ("pef", IJK, False), ("gz", IJK, False),
+              ("rdx", IJ, False), ("rdy", IJ, False)]
+    body = [
+        "pkd = 0.25 * (pef + pef[-1, 0, 0] + pef[0, -1, 0] + pef[-1, -1, 0])",
+        "gzd = 0.25 * (gz + gz[-1, 0, 0] + gz[0, -1, 0] + gz[-1, -1, 0])",
+    ]
+    layer = [
+        "wkd = pkd[0, 0, 1] - pkd",
+        "u = u + dt * rdx / (wkd + wkd[1, 0, 0]) * ((gzd[0, 0, 1] - gzd[1, 0, 0]) * (pkd[1, 0, 1] - pkd) + "
+        "(gzd - gzd[1, 0, 1]) * (pkd[0, 0, 1] - pkd[1, 0, 0]))",
+        "v = v + dt * rdy / (wkd + wkd[0, 1, 0]) * ((gzd[0, 0, 1] - gzd[0, 1, 0]) * (pkd[0, 1, 1] - pkd) + "
+        "(gzd - gzd[0, 1, 1]) * (pkd[0, 0, 1] - pkd[0, 1, 0]))",
+    ]
+    st = [("p_grad_d_corners", [], [("PARALLEL", "...", body)]),
+          ("p_grad_d", [], [("PARALLEL", "0, -1", layer)])]
+    return program_text([("dt", "37.5")], fields, st, [f"{x[0]}()" for x in st])
+
+
 def programs() -> dict:
     """name -> .stn text of every shipped program."""
     return {
@@ -392,6 +581,11 @@ def programs() -> dict:
         "riem_solver_c": riem_solver_c_program(),
         "remap_profile": remap_profile_program(),
         "remap_tracers": remap_tracers_program(),
+        "c_sw": c_sw_program(),
+        "c_grid": c_grid_program(),
+        "d_sw": d_sw_program(),
+        "nh_d": nh_d_program(),
+        "p_grad_d": p_grad_d_program(),
     }
 
 

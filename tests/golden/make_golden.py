@@ -37,6 +37,12 @@ CASES = [
     ("riem_solver_c", "column", (5, 4, 17), (True, True, True, True), 7),
     ("remap_profile", "column", (5, 4, 17), (True, True, True, True), 7),
     ("remap_tracers", "column", (3, 2, 9), (True, True, True, True), 7),
+    ("c_sw", "periodic", (14, 13, 2), (False, False, False, False), 7),
+    ("c_sw", "tile", (13, 14, 2), (True, True, True, True), 8),
+    ("c_grid", "tile", (13, 12, 5), (True, True, True, True), 7),
+    ("d_sw", "periodic", (17, 16, 2), (False, False, False, False), 7),
+    ("nh_d", "column", (5, 4, 17), (True, True, True, True), 7),
+    ("p_grad_d", "periodic", (7, 6, 5), (False, False, False, False), 7),
 ]
 
 

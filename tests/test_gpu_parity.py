@@ -27,7 +27,7 @@ def engine():
 # host libm may differ in the last ulp there, so they are held to the
 # per-stencil tolerance of the north star (max relative error <= 1e-12,
 # denominator max(|ref|, 1e-300)); every other program must be bitwise.
-RTOL = {"riem_solver_c": 1e-12}
+RTOL = {"riem_solver_c": 1e-12, "c_grid": 1e-12, "nh_d": 1e-12}
 
 
 @pytest.mark.parametrize("key,meta", list(golden_cases()))
@@ -49,6 +49,15 @@ CASES = [
     ("riem_solver_c", (33, 7, 81), True, 9),
     ("remap_profile", (48, 48, 17), False, 10),
     ("remap_tracers", (20, 12, 81), False, 11),
+    ("c_sw", (48, 48, 16), False, 12),
+    ("c_sw", (37, 21, 3), True, 13),
+    ("c_grid", (48, 48, 17), False, 14),
+    ("c_grid", (33, 19, 9), True, 15),
+    ("d_sw", (48, 48, 8), False, 16),
+    ("d_sw", (37, 21, 3), True, 17),
+    ("nh_d", (48, 48, 17), False, 18),
+    ("p_grad_d", (48, 48, 17), False, 19),
+    ("p_grad_d", (37, 21, 5), True, 20),
 ]
 
 

@@ -56,7 +56,8 @@ needs_ref = pytest.mark.skipif(not _ref.available(), reason="reference package n
 
 
 @needs_ref
-@pytest.mark.parametrize("name", ["copy", "fv_tp_2d", "tracer_2d", "riem_solver_c", "remap_profile"])
+@pytest.mark.parametrize("name", ["copy", "fv_tp_2d", "tracer_2d", "riem_solver_c", "remap_profile", "c_sw",
+                                  "c_grid", "d_sw", "nh_d", "p_grad_d"])
 def test_oracle_matches_live_reference(name):
     from paper_2205_04148_b200.inputs import synthetic_inputs
     from paper_2205_04148_b200.program import PROGRAM_DIR
@@ -64,8 +65,10 @@ def test_oracle_matches_live_reference(name):
     ref = _ref.load()
     prog = ref.parse_program((PROGRAM_DIR / f"{name}.stn").read_text())
     cases = [((15, 17, 3), (False,) * 4, 1), ((16, 16, 2), (True,) * 4, 2)]
-    if name.startswith(("riem", "remap")):
+    if name.startswith(("riem", "remap", "nh_d")):
         cases = [((4, 3, 12), (True,) * 4, 1), ((3, 3, 30), (False,) * 4, 2)]
+    elif name in ("c_grid", "d_sw"):
+        cases = [((17, 16, 5), (False,) * 4, 1), ((16, 17, 4), (True,) * 4, 2)]
     for domain, placement, seed in cases:
         inputs = synthetic_inputs(name, domain, seed)
         a = ref.run_reference(prog, inputs, domain, placement=ref.RankPlacement(*placement))
