@@ -9,11 +9,12 @@
 // values a backward sweep consumes are staged per column in shared memory
 // (NC columns x (nk+1) levels per array) so nothing round-trips through HBM.
 // Every statement is evaluated with the .stn's operation order, so results
-// are bitwise the interpreter's except where log/exp (CUDA libdevice vs the
-// host libm) differ in the last ulp.
+// are bitwise the interpreter's (log is the deterministic det_log of the
+// oracle extension, detmath.cuh).
 #include <math.h>
 
 #include "column.cuh"
+#include "detmath.cuh"
 
 namespace fv3b {
 
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
     const double pem1 = pem0 + dm_k;  // pem(k+1) = pem + dm
     AT(S2, k + 1) = pem1;
     const double gzk = gz[k * sk], gzk1 = gz[(k + 1) * sk];
-    const double pmk = dm_k / log(pem1 / pem0);
+    const double pmk = dm_k / det_log(pem1 / pem0);
     const double pek = dm_k * rdgas * pt[k * sk] / (gzk - gzk1) - pmk;
     const double dm_n = (k + 1 < nk) ? dm[(k + 1) * sk] : 0.0;
     // layer k coefficients (riem_coef)
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
     go[nk * so] = gzn;
     for (int l = nk - 1; l >= 0; --l) {
       const double dml = dm[l * sk];
-      const double pm = dml / log(AT(S1, l + 1) / AT(S1, l));
+      const double pm = dml / det_log(AT(S1, l + 1) / AT(S1, l));
       const double g = gzn + dml * rdgas * pt[l * sk] / np_max(a.p_fac * pm, pm + 0.5 * (AT(S0, l) + AT(S0, l + 1)));
       go[l * so] = g;
       gzn = g;

@@ -10,7 +10,8 @@ One documented oracle extension is installed: ``log`` and ``exp`` builtins
 ``sqrt abs min max select``, ``frontend/ast.py:28``).  The parser shares the
 ``BUILTINS`` dict (``parser.py:31,261``) and ``_eval`` recurses through its
 module-global name (``reference.py:202-258``), so wrapping the global is
-enough.  Evaluation is ``numpy.log`` / ``numpy.exp`` elementwise.
+enough.  ``log`` is the deterministic fdlibm-algorithm ``oracle.detmath.det_log``
+(so host and device agree bitwise); ``exp`` is ``numpy.exp``.
 
 The reference is located through ``$STENCILKIT_REF`` (default
 ``/root/reference/pkg/src``).  It is never present on the GPU host; callers
@@ -42,6 +43,8 @@ def load():
         raise ImportError(f"reference package not found under {REF}")
     import numpy as np
 
+    from oracle.detmath import det_log
+
     if str(REF) not in sys.path:
         sys.path.insert(0, str(REF))
     import stencilkit  # noqa: F401
@@ -65,8 +68,10 @@ def load():
         def _eval_ext(expr, ctx, ranges, k, scalars, record):
             if isinstance(expr, sk_ast.Call) and expr.func in ("log", "exp"):
                 arg = _eval_ext(expr.args[0], ctx, ranges, k, scalars, record)
+                if expr.func == "log":
+                    return det_log(arg)
                 with np.errstate(all="ignore"):
-                    return np.log(arg) if expr.func == "log" else np.exp(arg)
+                    return np.exp(arg)
             return base_eval(expr, ctx, ranges, k, scalars, record)
 
         sk_ref._eval = _eval_ext

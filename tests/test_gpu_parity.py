@@ -23,11 +23,12 @@ def engine():
     return executor
 
 
-# Programs whose .stn uses log/exp (oracle extension): CUDA libdevice and the
-# host libm may differ in the last ulp there, so they are held to the
-# per-stencil tolerance of the north star (max relative error <= 1e-12,
-# denominator max(|ref|, 1e-300)); every other program must be bitwise.
-RTOL = {"riem_solver_c": 1e-12, "c_grid": 1e-12, "nh_d": 1e-12}
+# Every program is held to bitwise equality: no ``**`` in the .stn sources,
+# -fmad=false, and the ``log`` extension is the deterministic fdlibm
+# algorithm on both sides (oracle/detmath.py, csrc/detmath.cuh).  A program
+# that used libm transcendentals would be listed here with the north star's
+# per-stencil tolerance (max relative error <= 1e-12).
+RTOL: dict[str, float] = {}
 
 
 @pytest.mark.parametrize("key,meta", list(golden_cases()))
