@@ -133,6 +133,20 @@ int fv3b_nh_d(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_p_grad_d(const fv3b_field* f, int nf, const double* s, int ns,
                   const fv3b_domain* d, void* stream);
 
+/* K6  halo_update, on-device parts.
+ *   fv3b_halo_periodic  fill the I/J halos of up to 32 fields of a doubly
+ *                       periodic single-rank domain.  scalars: [halo width].
+ *   fv3b_halo_pack / fv3b_halo_unpack  copy an edge strip (all levels) of up
+ *                       to 32 fields to / from one contiguous buffer for the
+ *                       NCCL neighbour exchange.  scalars: [i0, j0, w, h,
+ *                       buffer address as the bits of a double]. */
+int fv3b_halo_periodic(const fv3b_field* f, int nf, const double* s, int ns,
+                       const fv3b_domain* d, void* stream);
+int fv3b_halo_pack(const fv3b_field* f, int nf, const double* s, int ns,
+                   const fv3b_domain* d, void* stream);
+int fv3b_halo_unpack(const fv3b_field* f, int nf, const double* s, int ns,
+                     const fv3b_domain* d, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

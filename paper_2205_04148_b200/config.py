@@ -1,0 +1,57 @@
+"""Frozen run configuration shared by the CPU oracle step and the B200 step
+("Freeze n_split, k_split, nq and dt in one run-config").
+
+One dycore timestep (k_split = 1):
+
+    for it in range(n_split):                         acoustic substeps
+        halo_update(u, v, w, delp, pt, gz)
+        c_grid    (c_sw + riem_solver_c + p_grad_c)   -> uc, vc
+        halo_update(uc, vc)
+        d_sw                                          -> u, v, w, delp, pt, cx, cy, xfa, yfa, mfx, mfy
+        nh_d      (riem_solver3 role)                 -> w, gz, pef
+        halo_update(pef, gz)
+        p_grad_d                                      -> u, v
+    halo_update(q*, cx, cy, xfa, yfa, mfx, mfy)
+    tracer_2d (nq tracers)                            -> q*
+    remap_tracers (remap_profile of every tracer)     -> q*_a2, q*_a3, q*_a4
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    ni: int = 192
+    nj: int = 192
+    nk: int = 80
+    n_split: int = 6
+    nq: int = 8
+    dt_atmos: float = 90.0
+    halo: int = 4
+    seed: int = 2205
+    # physical constants of the programs (templates.RIEM_CONSTS / D_CONSTS)
+    consts: dict = field(default_factory=lambda: {
+        "ptop": 300.0, "rdgas": 287.05, "grav": 9.80665, "gama": 1.4, "p_fac": 0.05,
+        "dddmp": 0.2, "d2_bg": 0.0, "da_min": 1.0e8, "damp_w": 0.02,
+        "ppm_p1": 7.0 / 12.0, "ppm_p2": -1.0 / 12.0,
+    })
+
+    @property
+    def dt_acoustic(self) -> float:
+        return self.dt_atmos / self.n_split
+
+    @property
+    def cells(self) -> int:
+        return self.ni * self.nj * self.nk
+
+    def tracer_names(self) -> list[str]:
+        return [f"q{n}" for n in range(self.nq)]
+
+
+# Prognostic / diagnostic state fields.  3-D fields have nk+1 levels
+# (interface-capable); 2-D fields are metrics and the surface w.
+STATE_3D = ["u", "v", "w", "delp", "pt", "gz", "pef", "uc", "vc", "cx", "cy", "xfa", "yfa", "mfx", "mfy", "dp1"]
+METRICS_2D = ["dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxc", "rdyc", "rdxa", "rdya", "area", "rarea", "rarea_c",
+              "f0", "fc", "ws"]

@@ -1,0 +1,148 @@
+// K6 halo_update, on-device parts.
+//
+//  * fv3b_halo_periodic: fills the I/J halo of every field of a doubly
+//    periodic single-rank domain in one launch (corners included);
+//  * fv3b_halo_pack / fv3b_halo_unpack: copy the edge strips of a batch of
+//    fields to / from one contiguous message buffer for the neighbour
+//    exchange of a decomposed domain (NCCL P2P moves the buffers).  A strip
+//    is a rectangle [i0, i0+w) x [j0, j0+h) x all levels of every field;
+//    buffer layout is field-major, then level, row, column.
+#include "common.cuh"
+
+namespace fv3b {
+
+constexpr int HALO_MAXF = 32;
+
+struct HaloArgs {
+  double* o[HALO_MAXF];  // interior origins
+  int64_t sj, sk;
+  int levels[HALO_MAXF];  // levels to process per field (1 for 2-D)
+  int nf, ni, nj, h;
+};
+
+// One thread per halo cell of a level: (i, j) enumerates the ring
+// [-h, n+h)^2 minus the interior; source = periodic wrap.
+__global__ void halo_periodic_kernel(const HaloArgs a) {
+  const int W = a.ni + 2 * a.h, H = a.nj + 2 * a.h;
+  const int f = blockIdx.z, k = blockIdx.y;
+  if (k >= a.levels[f]) return;
+  double* o = a.o[f] + (int64_t)k * a.sk;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < W * H; e += gridDim.x * blockDim.x) {
+    const int i = e % W - a.h, j = e / W - a.h;
+    if (i >= 0 && i < a.ni && j >= 0 && j < a.nj) continue;
+    const int si = (i + a.ni) % a.ni, sj = (j + a.nj) % a.nj;
+    o[i + (int64_t)j * a.sj] = o[si + (int64_t)sj * a.sj];
+  }
+}
+
+struct StripArgs {
+  double* o[HALO_MAXF];
+  int64_t sj, sk;
+  int levels[HALO_MAXF];
+  int64_t off[HALO_MAXF];  // element offset of each field's strip in the buffer
+  double* buf;
+  int nf, i0, j0, w, h;
+  bool unpack;
+};
+
+__global__ void strip_kernel(const StripArgs a) {
+  const int f = blockIdx.z, k = blockIdx.y;
+  if (k >= a.levels[f]) return;
+  const int n = a.w * a.h;
+  double* o = a.o[f] + (int64_t)k * a.sk;
+  double* b = a.buf + a.off[f] + (int64_t)k * n;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int i = a.i0 + e % a.w, j = a.j0 + e / a.w;
+    double* p = o + i + (int64_t)j * a.sj;
+    if (a.unpack)
+      *p = b[e];
+    else
+      b[e] = *p;
+  }
+}
+
+static int collect(const fv3b_field* f, int nf, const fv3b_domain* d, int h, double** o, int* levels, int64_t* sj,
+                   int64_t* sk) {
+  if (nf < 1 || nf > HALO_MAXF) return fail(FV3B_EINVAL, "halo: 1..%d fields per call (got %d)", HALO_MAXF, nf);
+  *sj = 0;
+  *sk = 0;
+  for (int t = 0; t < nf; ++t) {
+    View v;
+    const Halo hh = {h, h, h, h, 0, 0};
+    fv3b_domain dd = *d;
+    dd.nk = 0;
+    FV3B_TRY(view_of(f[t], f[t].rank, dd, hh, "halo field", &v));
+    if (f[t].rank == 3) {
+      if (*sk == 0) *sk = v.sk;
+      if (v.sk != *sk) return fail(FV3B_ELAYOUT, "halo: 3-D fields must share strides");
+    }
+    if (*sj == 0) *sj = v.sj;
+    if (v.sj != *sj) return fail(FV3B_ELAYOUT, "halo: fields must share the J stride");
+    o[t] = v.o;
+    levels[t] = f[t].rank == 3 ? f[t].shape[2] : 1;
+  }
+  return FV3B_OK;
+}
+
+}  // namespace fv3b
+
+using namespace fv3b;
+
+// fields: any mix of 3-D / 2-D fields (<= 32) of one geometry.  scalars:
+// [halo width].  Fills all allocated levels.
+extern "C" int fv3b_halo_periodic(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                  void* stream) {
+  if (f == nullptr || d == nullptr || s == nullptr || ns != 1) return fail(FV3B_EINVAL, "fv3b_halo_periodic: 1 scalar");
+  HaloArgs a;
+  a.h = (int)s[0];
+  if (a.h < 0 || a.h > d->ni || a.h > d->nj) return fail(FV3B_EINVAL, "fv3b_halo_periodic: bad halo width %d", a.h);
+  FV3B_TRY(collect(f, nf, d, a.h, a.o, a.levels, &a.sj, &a.sk));
+  a.nf = nf;
+  a.ni = d->ni;
+  a.nj = d->nj;
+  int maxl = 1;
+  for (int t = 0; t < nf; ++t) maxl = a.levels[t] > maxl ? a.levels[t] : maxl;
+  const int ring = (d->ni + 2 * a.h) * (d->nj + 2 * a.h);
+  dim3 grid(cdiv(ring, 256) < 8 ? cdiv(ring, 256) : 8, maxl, nf);
+  halo_periodic_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch("fv3b_halo_periodic");
+}
+
+static int strip_call(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d, void* stream,
+                      bool unpack) {
+  // scalars: i0, j0, w, h (strip rectangle, interior-relative), buffer
+  // pointer passed as the bit pattern of s[4] (uint64 in a double slot).
+  if (f == nullptr || d == nullptr || s == nullptr || ns != 5) return fail(FV3B_EINVAL, "halo strip: 5 scalars");
+  StripArgs a;
+  a.i0 = (int)s[0];
+  a.j0 = (int)s[1];
+  a.w = (int)s[2];
+  a.h = (int)s[3];
+  uint64_t bits;
+  memcpy(&bits, &s[4], sizeof bits);
+  a.buf = reinterpret_cast<double*>(bits);
+  if (a.buf == nullptr || a.w <= 0 || a.h <= 0) return fail(FV3B_EINVAL, "halo strip: empty strip or null buffer");
+  FV3B_TRY(collect(f, nf, d, 0, a.o, a.levels, &a.sj, &a.sk));
+  a.nf = nf;
+  a.unpack = unpack;
+  int64_t off = 0;
+  int maxl = 1;
+  for (int t = 0; t < nf; ++t) {
+    a.off[t] = off;
+    off += (int64_t)a.levels[t] * a.w * a.h;
+    maxl = a.levels[t] > maxl ? a.levels[t] : maxl;
+  }
+  dim3 grid(cdiv(a.w * a.h, 256) < 16 ? cdiv(a.w * a.h, 256) : 16, maxl, nf);
+  strip_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch(unpack ? "fv3b_halo_unpack" : "fv3b_halo_pack");
+}
+
+extern "C" int fv3b_halo_pack(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                              void* stream) {
+  return strip_call(f, nf, s, ns, d, stream, false);
+}
+
+extern "C" int fv3b_halo_unpack(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                void* stream) {
+  return strip_call(f, nf, s, ns, d, stream, true);
+}

@@ -1,0 +1,204 @@
+"""The B200 dycore timestep: device-resident state, the shipped programs'
+hand-written kernels in the step order of ``config.py``, halo updates on
+device, and CUDA-graph replay of whole timesteps.
+
+State lives in the uniform device Layout (``device.Grid``): every 3-D field
+has ``nk + 1`` levels and a 4-cell I/J halo, so layer programs (domain nk)
+and interface programs (domain nk + 1) address the same buffers.  Fields a
+kernel reads at horizontal offsets and rewrites (u, v, w, delp, pt, tracers)
+are ping-ponged between two buffers; pointwise accumulators and in-place
+column outputs are updated in place.
+
+The CPU counterpart is ``oracle/dycore.py`` (tests only); the two agree
+bitwise (tests/test_gpu_dycore.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import METRICS_2D, STATE_3D, RunConfig
+from .device import Grid
+
+C_METRICS = ("dx", "dy", "dxc", "dyc", "rdxc", "rdyc", "rarea", "rarea_c", "fc")
+D_METRICS = ("dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxa", "rdya", "area", "rarea", "rarea_c", "f0")
+PINGPONG = ("u", "v", "w", "delp", "pt")
+ACCUM = ("cx", "cy", "xfa", "yfa", "mfx", "mfy")
+
+
+class PeriodicHalo:
+    """Single-rank doubly periodic halo update (one launch per group)."""
+
+    def __init__(self, dycore: "Dycore"):
+        self.d = dycore
+
+    def update(self, names: list[str]) -> None:
+        d = self.d
+        for i in range(0, len(names), 32):
+            fields = [d.f(n) for n in names[i : i + 32]]
+            d.launch("halo", "fv3b_halo_periodic", fields, [float(d.cfg.halo)], d.dom_layers)
+
+
+class Dycore:
+    def __init__(self, cfg: RunConfig, state: dict[str, np.ndarray] | None = None, device: str = "cuda",
+                 placement=(False, False, False, False), halo=None):
+        self.cfg = cfg
+        self.device = device
+        self.grid = Grid(cfg.ni, cfg.nj, cfg.nk, halo=cfg.halo)
+        self.placement = placement
+        self.dom_layers = self.grid.domain(placement, nk=cfg.nk)
+        self.dom_ifaces = self.grid.domain(placement, nk=cfg.nk + 1)
+        g = self.grid
+        names3 = STATE_3D + cfg.tracer_names() + [f"q{t}_{a}" for t in range(cfg.nq) for a in ("a2", "a3", "a4")]
+        self.cur: dict[str, torch.Tensor] = {n: g.new3(device) for n in names3}
+        self.cur.update({n: g.new2(device) for n in METRICS_2D})
+        self.alt: dict[str, torch.Tensor] = {n: g.new3(device) for n in list(PINGPONG) + cfg.tracer_names()}
+        self.scratch = {n: g.new3(device) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc")}
+        self.halo = halo or PeriodicHalo(self)
+        self.stream = None
+        self.launches = 0
+        self.timer = None
+        self._graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self._parity = 0
+        if state is not None:
+            self.load(state)
+
+    # -- state transfer (reference array convention, uniform halo) ----------
+
+    def load(self, state: dict[str, np.ndarray]) -> None:
+        h = self.cfg.halo
+        for n, t in self.cur.items():
+            if n in state:
+                a = state[n]
+                self.grid.put(t, a, ("I", "J", "K")[: a.ndim], (h, h, 0)[: a.ndim])
+
+    def download(self, names=None) -> dict[str, np.ndarray]:
+        h = self.cfg.halo
+        out = {}
+        for n in names or self.cur:
+            t = self.cur[n]
+            dims = ("I", "J", "K") if t.dim() == 3 else ("I", "J")
+            shape = (self.cfg.ni + 2 * h, self.cfg.nj + 2 * h, self.cfg.nk + 1)[: t.dim()]
+            out[n] = self.grid.get(t, dims, (h, h, 0)[: t.dim()], shape)
+        return out
+
+    # -- launch helpers -----------------------------------------------------
+
+    def f(self, name: str) -> _lib.Field:
+        return self.grid.abi(self.cur[name])
+
+    def a(self, name: str) -> _lib.Field:
+        return self.grid.abi(self.alt[name])
+
+    def s(self, name: str) -> _lib.Field:
+        return self.grid.abi(self.scratch[name])
+
+    def swap(self, *names: str) -> None:
+        for n in names:
+            self.cur[n], self.alt[n] = self.alt[n], self.cur[n]
+
+    def launch(self, node: str, entry: str, fields, scalars, dom) -> None:
+        stream = torch.cuda.current_stream().cuda_stream
+        if self.timer is not None:
+            self.timer.start(node)
+        _lib.call(entry, fields, scalars, dom, stream)
+        if self.timer is not None:
+            self.timer.stop(node)
+        self.launches += 1
+
+    # -- the programs of one timestep ----------------------------------------
+
+    def c_grid(self) -> None:
+        c, dt = self.cfg.consts, self.cfg.dt_acoustic
+        fields = [self.f(n) for n in ("u", "v", "delp", "pt", "w", "gz")] + [self.f(m) for m in C_METRICS]
+        fields += [self.f("ws"), self.f("uc"), self.f("vc")] + [self.s(n) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc")]
+        self.launch("c_grid", "fv3b_c_grid", fields,
+                    [0.5 * dt, c["ptop"], c["rdgas"], c["grav"], c["gama"], c["p_fac"]], self.dom_ifaces)
+
+    def d_sw(self) -> None:
+        c, dt = self.cfg.consts, self.cfg.dt_acoustic
+        fields = [self.f(n) for n in PINGPONG + ("uc", "vc") + ACCUM] + [self.f(m) for m in D_METRICS]
+        fields += [self.a(n) for n in PINGPONG] + [self.f(n) for n in ACCUM]
+        self.launch("d_sw", "fv3b_d_sw", fields,
+                    [c["ppm_p1"], c["ppm_p2"], dt, c["dddmp"], c["d2_bg"], c["da_min"], c["damp_w"]], self.dom_layers)
+        self.swap(*PINGPONG)
+
+    def nh_d(self) -> None:
+        c, dt = self.cfg.consts, self.cfg.dt_acoustic
+        fields = [self.f(n) for n in ("delp", "pt", "w", "gz", "ws")] + [self.f("pef"), self.f("gz"), self.a("w")]
+        self.launch("nh_d", "fv3b_nh_d", fields, [c["ptop"], c["rdgas"], c["grav"], c["gama"], c["p_fac"], dt],
+                    self.dom_ifaces)
+        self.swap("w")
+
+    def p_grad_d(self) -> None:
+        fields = [self.f(n) for n in ("u", "v", "pef", "gz", "rdx", "rdy")] + [self.a("u"), self.a("v")]
+        self.launch("p_grad_d", "fv3b_p_grad_d", fields, [self.cfg.dt_acoustic], self.dom_ifaces)
+        self.swap("u", "v")
+
+    def tracer_2d(self) -> None:
+        c = self.cfg.consts
+        qs = self.cfg.tracer_names()
+        fields = [self.f(n) for n in ("cx", "cy", "xfa", "yfa", "mfx", "mfy", "dp1", "area", "rarea")]
+        fields += [self.f(q) for q in qs] + [self.a(q) for q in qs]
+        self.launch("tracer_2d", "fv3b_tracer_2d", fields, [c["ppm_p1"], c["ppm_p2"]], self.dom_layers)
+        self.swap(*qs)
+
+    def remap(self) -> None:
+        fields = [self.f("delp")]
+        for q in self.cfg.tracer_names():
+            fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4")]
+        self.launch("remap_tracers", "fv3b_remap_profile", fields, [], self.dom_ifaces)
+
+    def step(self) -> None:
+        """Enqueue one full timestep on the current stream."""
+        cfg = self.cfg
+        for n in ACCUM:
+            self.cur[n].zero_()
+        self.cur["dp1"].copy_(self.cur["delp"])
+        for _ in range(cfg.n_split):
+            self.halo.update(["u", "v", "w", "delp", "pt", "gz"])
+            self.c_grid()
+            self.halo.update(["uc", "vc"])
+            self.d_sw()
+            self.nh_d()
+            self.halo.update(["pef", "gz"])
+            self.p_grad_d()
+        self.halo.update(cfg.tracer_names() + list(ACCUM))
+        self.tracer_2d()
+        self.remap()
+        self._parity ^= 1  # the tracers swap buffers once per step
+
+    # -- CUDA graphs ---------------------------------------------------------
+
+    def capture(self) -> None:
+        """Capture one timestep per buffer parity (the tracers alternate
+        buffers each step; every other ping-pong field swaps an even number of
+        times).  Capture executes nothing, so the state is unchanged; the
+        two captures leave the buffer bookkeeping where it started."""
+        torch.cuda.synchronize()
+        start = self._parity
+        for _ in range(2):
+            parity = self._parity
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.step()
+            self._graphs[parity] = g
+        assert self._parity == start
+        torch.cuda.synchronize()
+
+    def replay(self) -> None:
+        """Run one captured timestep on the current stream."""
+        self._graphs[self._parity].replay()
+        self._parity ^= 1
+        self.swap(*self.cfg.tracer_names())
+
+
+# libfv3b kernels launched per entry point (fused entries launch several)
+KERNELS = {"fv3b_c_grid": 3, "fv3b_d_sw": 2}
+
+
+def kernels_per_step(cfg: RunConfig) -> int:
+    per_sub = 3 + KERNELS["fv3b_c_grid"] + KERNELS["fv3b_d_sw"] + 1 + 1
+    return cfg.n_split * per_sub + 1 + 1 + 1

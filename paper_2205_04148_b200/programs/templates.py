@@ -313,7 +313,7 @@ def riem_solver_c_program() -> str:
     fields = [("dm", IJK, False), ("pt", IJK, False), ("w", IJK, False), ("gz", IJK, False),
               ("ws", IJ, False), ("pef", IJK, False)]
     stencils = riem_stencils("dm", "pt", "w", "gz", "ws", "pef", "gz")
-    return program_text(RIEM_CONSTS + [("dt", "18.75")], fields, stencils, [f"{s[0]}()" for s in stencils])
+    return program_text(RIEM_CONSTS + [("dt", "7.5")], fields, stencils, [f"{s[0]}()" for s in stencils])
 
 
 # ---------------------------------------------------------------------------
@@ -438,7 +438,7 @@ def c_sw_program() -> str:
     fields = [(n, IJK, False) for n in ("u", "v", "delp", "pt", "w", "uc", "vc", "delpc", "ptc", "wc")]
     fields += [(m, IJ, False) for m in C_METRICS]
     st = c_sw_stencils("...", "delpc", "ptc", "wc", "uc", "vc")
-    return program_text([("dt2", "18.75")], fields, st, [f"{x[0]}()" for x in st])
+    return program_text([("dt2", "7.5")], fields, st, [f"{x[0]}()" for x in st])
 
 
 def c_grid_program() -> str:
@@ -458,7 +458,7 @@ def c_grid_program() -> str:
         "vc = vc + dt2 * rdyc / (wkc[0, -1, 0] + wkc) * ((gzc[0, -1, 1] - gzc) * (pkc[0, 0, 1] - pkc[0, -1, 0]) + "
         "(gzc[0, -1, 0] - gzc[0, 0, 1]) * (pkc[0, -1, 1] - pkc))",
     ])]))
-    return program_text(RIEM_CONSTS + [("dt2", "18.75")], fields, st, [f"{x[0]}()" for x in st])
+    return program_text(RIEM_CONSTS + [("dt2", "7.5")], fields, st, [f"{x[0]}()" for x in st])
 
 
 # ---------------------------------------------------------------------------
@@ -470,7 +470,7 @@ def c_grid_program() -> str:
 # ---------------------------------------------------------------------------
 
 D_METRICS = ["dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxa", "rdya", "area", "rarea", "rarea_c", "f0"]
-D_CONSTS = [("dt", "37.5"), ("dddmp", "0.2"), ("d2_bg", "0.0"), ("da_min", "1.0"), ("damp_w", "0.02")]
+D_CONSTS = [("dt", "15.0"), ("dddmp", "0.2"), ("d2_bg", "0.0"), ("da_min", "1.0e8"), ("damp_w", "0.02")]
 
 
 def d_sw_stencils() -> list:
@@ -550,7 +550,7 @@ def nh_d_program() -> str:
               ("ws", IJ, False), ("pef", IJK, False)]
     st = riem_stencils("delp", "pt", "w", "gz", "ws", "pef", "gz", dt="dt", sfx="_d")
     st.append(("nh_d_w", [], [("PARALLEL", "0, -1", ["w = w2c_d"])]))
-    return program_text(RIEM_CONSTS + [("dt", "37.5")], fields, st, [f"{x[0]}()" for x in st])
+    return program_text(RIEM_CONSTS + [("dt", "15.0")], fields, st, [f"{x[0]}()" for x in st])
 
 
 def p_grad_d_program() -> str:
@@ -569,7 +569,7 @@ def p_grad_d_program() -> str:
     ]
     st = [("p_grad_d_corners", [], [("PARALLEL", "...", body)]),
           ("p_grad_d", [], [("PARALLEL", "0, -1", layer)])]
-    return program_text([("dt", "37.5")], fields, st, [f"{x[0]}()" for x in st])
+    return program_text([("dt", "15.0")], fields, st, [f"{x[0]}()" for x in st])
 
 
 def programs() -> dict:
