@@ -1,0 +1,386 @@
+"""bench.py — FV3 dycore timestep throughput on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): one full fp64 dycore timestep of
+a doubly periodic 192x192x80 domain per GPU — n_split = 6 acoustic substeps
+(c_grid = c_sw + riem_solver_c + p_grad_c, d_sw, nh_d, p_grad_d with their
+halo updates), then tracer_2d (nq = 8) and remap_tracers.  The state
+(~1.3 GB) exceeds the 126 MB L2, so no flush is needed between steps.
+
+* ``value``  — grid cells per second over the whole job (N x cells / step
+  time), device-resident state, CUDA-graph replay, CUDA events on the
+  launching stream, max over ranks.
+* ``e2e``    — the same metric through the public API with host buffers:
+  each step copies the prognostic state (u, v, w, delp, pt, gz, q0..q7)
+  from pinned host memory, runs the step and copies it back.
+* ``roofline`` — the dominant program launch (by device time) against the
+  measured HBM copy bandwidth: algorithmic (first-touch compulsory) bytes per
+  launch / its mean CUDA-event duration.
+* ``cpu_baseline`` — the oracle restatement of the reference CPU path
+  (``oracle/``, pinned bitwise against ``run_reference``) on the host cores.
+
+N > 1: one process per GPU (torchrun), weak scaling: every rank owns a
+192x192x80 block of a px x py doubly periodic domain (1x2, 2x2, 2x4) and
+exchanges halos with its neighbours over NCCL.
+
+``--impl reference`` times the reference CPU path (the oracle port; the
+reference is Python and is not shipped to the GPU box) on all host cores on
+rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "dycore step grid-cells/s (fp64 FV3 timestep, 192x192x80 per GPU)"
+UNIT = "cells/s"
+
+
+# ---------------------------------------------------------------------------
+# CPU path: the oracle restatement of run_reference on host cores
+# ---------------------------------------------------------------------------
+
+def _cpu_tile(args):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    ni, nj, nk, steps = args
+    sys.path.insert(0, str(ROOT))
+    from oracle.dycore import OracleDycore
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.state import initial_state
+
+    cfg = RunConfig(ni=ni, nj=nj, nk=nk)
+    d = OracleDycore(cfg, initial_state(cfg))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        d.step()
+    return time.perf_counter() - t0
+
+
+def cpu_tiles(cores: int, ni=192, nj=192, min_tile=32):
+    """Split the domain into at most ``cores`` tiles of >= min_tile cells."""
+    best = (1, 1)
+    for px in range(1, ni // min_tile + 1):
+        for py in range(1, nj // min_tile + 1):
+            if px * py <= cores and ni % px == 0 and nj % py == 0 and px * py > best[0] * best[1]:
+                best = (px, py)
+    return best
+
+
+def cpu_run(steps: int, nk=80, tile=None, cores=None):
+    """Run ``steps`` oracle timesteps on P processes, one doubly periodic tile
+    each; returns (cells/s, cores, sample)."""
+    import multiprocessing as mp
+
+    cores = cores or os.cpu_count() or 1
+    px, py = cpu_tiles(cores)
+    ti, tj = tile or (192 // px, 192 // py)
+    nproc = px * py
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(nproc) as pool:
+        times = pool.map(_cpu_tile, [(ti, tj, nk, steps)] * nproc)
+    wall = time.perf_counter() - t0
+    # cells/s over the compute itself (the slowest process; pool start-up excluded)
+    t = max(times)
+    cells = nproc * ti * tj * nk * steps
+    sample = (f"{steps} full timestep(s) (n_split=6, nq=8) of {nproc} independent doubly periodic "
+              f"{ti}x{tj}x{nk} tiles, one per process ({nproc * ti}x{tj}x{nk} cells total; tile-local "
+              f"periodic halos, no inter-process exchange); slowest process {t:.1f} s, wall {wall:.1f} s")
+    return cells / t, nproc, sample
+
+
+def run_reference_arm(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    K, W = args.steps, args.warmup
+    # bounded: each step is one full C2 timestep decomposed over the host cores
+    # (tiles >= 32x32); per-step CPU time ~ (192*192*80 / cores) / 25e3 s
+    rates = []
+    for i in range(W + K):
+        v, cores, sample = cpu_run(1)
+        if i >= W:
+            rates.append(v)
+    v = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": 192 * 192 * 80 / v * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 doubly periodic 192x192x80 fp64 dycore timestep (n_split=6, nq=8)",
+                   "ni": 192, "nj": 192, "nk": 80, "decomposition": "CPU: tiles over host processes"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            out, _ = self.p.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            c = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(c[0]))
+                mx = max(mx, float(c[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, c[3:]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+class LaunchTimer:
+    """CUDA events around every libfv3b launch, on the launching stream."""
+
+    def __init__(self):
+        import torch
+
+        self.torch = torch
+        self.ev = []
+
+    def start(self, node):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.ev.append([node, e, None])
+
+    def stop(self, node):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.ev[-1][2] = e
+
+    def per_node(self):
+        out = {}
+        for n, a, b in self.ev:
+            out.setdefault(n, []).append(a.elapsed_time(b) * 1e-3)
+        return out
+
+
+def grid_for(world: int) -> tuple[int, int]:
+    return {1: (1, 1), 2: (1, 2), 4: (2, 2), 6: (2, 3), 8: (2, 4)}.get(world, (1, world))
+
+
+def run_ours(args, rank: int, world: int, local: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_04148_b200 import _lib
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.dycore import Dycore, kernels_per_step
+    from paper_2205_04148_b200.state import initial_state
+    from paper_2205_04148_b200.traffic import compulsory_bytes
+
+    torch.cuda.set_device(local)
+    _lib.lib()  # no CPU fallback: fail loudly if the library is missing
+    cfg = RunConfig(ni=args.ni, nj=args.ni, nk=args.nk)
+    px, py = grid_for(world)
+    halo = None
+    if world > 1:
+        from paper_2205_04148_b200.parallel import DecomposedHalo
+
+        halo_cls = DecomposedHalo
+    state = initial_state(cfg)
+    d = Dycore(cfg, state)
+    if world > 1:
+        d.halo = halo_cls(d, px, py, rank)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (eager, then capture and replay)
+    d.step()
+    d.capture()
+    for _ in range(max(args.warmup, 3)):
+        d.replay()
+    barrier()
+
+    stream = torch.cuda.current_stream()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            d.replay()
+        t1.record(stream)
+        barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    clocks = clk.summary()
+
+    # end to end: pinned host state in, step, host state out
+    h_in = d.host_buffers()
+    h_out = d.host_buffers()
+    for n, t in h_in.items():
+        t.copy_(torch.from_numpy(state[n]))
+    d.load_host(h_in)
+    d.replay()
+    d.store_host(h_out)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        d.load_host(h_in)
+        d.replay()
+        d.store_host(h_out)
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    io_bytes = sum(t.numel() * t.element_size() for t in h_in.values())
+    assert all(bool(torch.isfinite(t).all()) for t in h_out.values()), "non-finite state after the e2e steps"
+
+    # per-launch device times: the same K steps eagerly with events around
+    # every libfv3b launch on the launching stream
+    d.timer = LaunchTimer()
+    d.launches = 0
+    barrier()
+    for _ in range(args.steps):
+        d.step()
+    barrier()
+    eager_launches = d.launches
+    per_node = d.timer.per_node()
+    d.timer = None
+
+    def reduce_max(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = reduce_max(ms)
+    e2e_ms = reduce_max(e2e_ms)
+    if rank != 0:
+        return
+
+    cells = cfg.cells * world
+    value = cells / (ms * 1e-3)
+    node_total = {n: sum(v) for n, v in per_node.items()}
+    top = max(node_total, key=node_total.get)
+    nk_prog = {"c_grid": cfg.nk + 1, "nh_d": cfg.nk + 1, "p_grad_d": cfg.nk + 1, "remap_tracers": cfg.nk + 1}
+    prog = {"halo": None}.get(top, top)
+    algo = compulsory_bytes(prog, (cfg.ni, cfg.nj, nk_prog.get(top, cfg.nk)))
+    mean_launch = statistics.mean(per_node[top])
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = algo / mean_launch / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(top)
+    step_bytes = 0
+    for n, v in per_node.items():
+        if n != "halo":
+            step_bytes += compulsory_bytes(n, (cfg.ni, cfg.nj, nk_prog.get(n, cfg.nk))) * len(v) / args.steps
+
+    cpu = None
+    if not args.no_cpu:
+        v, cores, sample = cpu_run(1)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded analytic state, state.py)",
+        "config": {"workload": "C2 doubly periodic 192x192x80 fp64 dycore timestep (n_split=6, nq=8)",
+                   "ni": cfg.ni, "nj": cfg.nj, "nk": cfg.nk, "n_split": cfg.n_split, "nq": cfg.nq,
+                   "decomposition": f"{px}x{py}", "l2": "state 1.3 GB/GPU > 126 MB L2 (no flush)",
+                   "timing": "CUDA-graph replay of whole timesteps, CUDA events, max over ranks"},
+        "e2e": {"value": cells / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes},
+        "gpu_launches": kernels_per_step(cfg) * args.steps,
+        "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "algo_bytes_per_launch": algo,
+                     "mean_launch_s": mean_launch, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)",
+                     "step_algo_bytes": step_bytes, "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak},
+        "kernels_ms_per_step": {n: round(v * 1e3 / args.steps, 4) for n, v in
+                                sorted(node_total.items(), key=lambda x: -x[1])},
+        "eager_launches_per_step": eager_launches / args.steps,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--ni", type=int, default=192)
+    ap.add_argument("--nk", type=int, default=80)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        run_ours(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -84,6 +84,47 @@ class Dycore:
             out[n] = self.grid.get(t, dims, (h, h, 0)[: t.dim()], shape)
         return out
 
+    # -- host I/O through pinned buffers (the end-to-end path) ---------------
+
+    def prognostic(self) -> list[str]:
+        """Fields a timestep evolves (the state a host caller owns)."""
+        return ["u", "v", "w", "delp", "pt", "gz"] + self.cfg.tracer_names()
+
+    def host_buffers(self, names=None) -> dict[str, torch.Tensor]:
+        """Pinned host tensors in the reference array convention (I, J, K,
+        halo-inclusive, C order) for ``names`` (default: the prognostic
+        state)."""
+        h, c = self.cfg.halo, self.cfg
+        shape = (c.ni + 2 * h, c.nj + 2 * h, c.nk + 1)
+        return {n: torch.empty(shape, dtype=torch.float64).pin_memory() for n in (names or self.prognostic())}
+
+    def _staging(self) -> torch.Tensor:
+        if getattr(self, "_stage", None) is None:
+            h, c = self.cfg.halo, self.cfg
+            self._stage = torch.empty((c.ni + 2 * h, c.nj + 2 * h, c.nk + 1), dtype=torch.float64,
+                                      device=self.device)
+        return self._stage
+
+    def _window(self, t: torch.Tensor) -> torch.Tensor:
+        g = self.grid
+        a = g.i0 - self.cfg.halo
+        return t[:, :, a : a + self.cfg.ni + 2 * self.cfg.halo].permute(2, 1, 0)
+
+    def load_host(self, host: dict[str, torch.Tensor]) -> None:
+        """Enqueue host -> device copies (pinned, async) of ``host`` fields
+        into the current state, then the layout transpose on the device."""
+        st = self._staging()
+        for n, src in host.items():
+            st.copy_(src, non_blocking=True)
+            self._window(self.cur[n]).copy_(st)
+
+    def store_host(self, host: dict[str, torch.Tensor]) -> None:
+        """Enqueue device -> host copies of the current state into ``host``."""
+        st = self._staging()
+        for n, dst in host.items():
+            st.copy_(self._window(self.cur[n]))
+            dst.copy_(st, non_blocking=True)
+
     # -- launch helpers -----------------------------------------------------
 
     def f(self, name: str) -> _lib.Field:
