@@ -27,6 +27,40 @@ __device__ __forceinline__ double np_max(double a, double b) {
 }
 
 
+// Software-pipelined level streaming for the column sweeps: step s = 0..n-1
+// of a pass loads its per-level global operands U steps ahead into a
+// register double buffer, so the loop-carried recurrence never waits on
+// HBM/L2 latency (the reference interpreter's level loop, reference.py:293,
+// becomes a register pipeline).  load(s) -> T must be side-effect free;
+// use(s, T) runs strictly in step order.
+template <int U, class T, class LoadF, class UseF>
+__device__ __forceinline__ void pipelined(int n, LoadF load, UseF use) {
+  T a[U], b[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (u < n) a[u] = load(u);
+  for (int s0 = 0; s0 < n; s0 += 2 * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (s0 + U + u < n) b[u] = load(s0 + U + u);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (s0 + u < n) use(s0 + u, a[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (s0 + 2 * U + u < n) a[u] = load(s0 + 2 * U + u);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (s0 + U + u < n) use(s0 + U + u, b[u]);
+  }
+}
+
+struct D1 { double x; };
+struct D2 { double x, y; };
+struct D3 { double x, y, z; };
+
+constexpr int PF = 8;  // prefetch distance (levels)
+
 // Statement-for-statement restatement of templates.riem_stencils.
 __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
   extern __shared__ double sm[];
@@ -41,52 +75,54 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
   double* S2 = sm + 2 * L * NC + c;  // pem -> w2
 #define AT(S, k) (S)[(k) * NC]
   const double dt = a.dt, ptop = a.ptop, rdgas = a.rdgas, grav = a.grav, gama = a.gama;
-  const double* dm = a.dm.ptr(i, j, 0);
-  const double* pt = a.pt.ptr(i, j, 0);
-  const double* w = a.w.ptr(i, j, 0);
-  const double* gz = a.gz.ptr(i, j, 0);
+  const double* __restrict__ dm = a.dm.ptr(i, j, 0);
+  const double* __restrict__ pt = a.pt.ptr(i, j, 0);
+  const double* __restrict__ w = a.w.ptr(i, j, 0);
+  const double* gz = a.gz.ptr(i, j, 0);  // may alias gzo (read before pass F writes)
   const int64_t sk = a.dm.sk;
 
   // ---- pass A (forward): riem_pem, riem_layer, riem_coef, riem_pp_fwd ----
-  double pem0 = ptop;  // pem(k)
-  AT(S2, 0) = pem0;
-  double pe_prev = 0.0, grat_prev = 0.0, bet_prev = 0.0, pp_prev = 0.0;
-  double dm_k = dm[0];
-  for (int k = 0; k < nk; ++k) {
-    const double pem1 = pem0 + dm_k;  // pem(k+1) = pem + dm
-    AT(S2, k + 1) = pem1;
-    const double gzk = gz[k * sk], gzk1 = gz[(k + 1) * sk];
-    const double pmk = dm_k / det_log(pem1 / pem0);
-    const double pek = dm_k * rdgas * pt[k * sk] / (gzk - gzk1) - pmk;
-    const double dm_n = (k + 1 < nk) ? dm[(k + 1) * sk] : 0.0;
-    // layer k coefficients (riem_coef)
-    const double grat = (k < nk - 1) ? dm_k / dm_n : 0.0;
-    const double bb = (k < nk - 1) ? 2.0 * (1.0 + grat) : 2.0;
-    // interface k of riem_pp_fwd (uses layer k-1's dd, needing pe(k))
-    if (k == 0) {
-      bet_prev = bb;
-      pp_prev = 0.0;
-      AT(S0, 0) = 0.0;
-    } else {
-      const double dd_prev = (k - 1 < nk - 1) ? 3.0 * (pe_prev + grat_prev * pek) : 3.0 * pe_prev;
-      double ppk;
-      if (k == 1)
-        ppk = dd_prev / bet_prev;
-      else
-        ppk = (dd_prev - pp_prev) / bet_prev;
-      const double gam = grat_prev / bet_prev;
-      bet_prev = bb - gam;
-      pp_prev = ppk;
-      AT(S0, k) = ppk;
-      AT(S1, k) = gam;
-    }
-    pe_prev = pek;
-    grat_prev = grat;
-    pem0 = pem1;
-    dm_k = dm_n;
-  }
-  {  // interface nk: pp = (dd[nk-1] - pp[nk-1]) / bet[nk-1], dd[nk-1] = 3*pe[nk-1]
-    const double dd_prev = (nk - 1 < nk - 1) ? 0.0 : 3.0 * pe_prev;
+  {
+    double pem0 = ptop;  // pem(k)
+    AT(S2, 0) = pem0;
+    double pe_prev = 0.0, grat_prev = 0.0, bet_prev = 0.0, pp_prev = 0.0;
+    double dm_k = __ldg(dm), gzk = gz[0];
+    pipelined<PF, D3>(
+        nk,
+        [&](int k) {  // dm(k+1), gz(k+1), pt(k)
+          return D3{(k + 1 < nk) ? __ldg(dm + (k + 1) * sk) : 0.0, gz[(k + 1) * sk], __ldg(pt + k * sk)};
+        },
+        [&](int k, const D3& v) {
+          const double dm_n = v.x, gzk1 = v.y;
+          const double pem1 = pem0 + dm_k;  // pem(k+1) = pem + dm
+          AT(S2, k + 1) = pem1;
+          const double pmk = dm_k / det_log(pem1 / pem0);
+          const double pek = dm_k * rdgas * v.z / (gzk - gzk1) - pmk;
+          // layer k coefficients (riem_coef)
+          const double grat = (k < nk - 1) ? dm_k / dm_n : 0.0;
+          const double bb = (k < nk - 1) ? 2.0 * (1.0 + grat) : 2.0;
+          // interface k of riem_pp_fwd (uses layer k-1's dd, needing pe(k))
+          if (k == 0) {
+            bet_prev = bb;
+            pp_prev = 0.0;
+            AT(S0, 0) = 0.0;
+          } else {
+            const double dd_prev = (k - 1 < nk - 1) ? 3.0 * (pe_prev + grat_prev * pek) : 3.0 * pe_prev;
+            const double ppk = (k == 1) ? dd_prev / bet_prev : (dd_prev - pp_prev) / bet_prev;
+            const double gam = grat_prev / bet_prev;
+            bet_prev = bb - gam;
+            pp_prev = ppk;
+            AT(S0, k) = ppk;
+            AT(S1, k) = gam;
+          }
+          pe_prev = pek;
+          grat_prev = grat;
+          pem0 = pem1;
+          dm_k = dm_n;
+          gzk = gzk1;
+        });
+    // interface nk: pp = (dd[nk-1] - pp[nk-1]) / bet[nk-1], dd[nk-1] = 3*pe[nk-1]
+    const double dd_prev = 3.0 * pe_prev;
     AT(S0, nk) = (nk == 1) ? dd_prev / bet_prev : (dd_prev - pp_prev) / bet_prev;
   }
 
@@ -94,52 +130,60 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
   const double t1g = gama * 2.0 * dt * dt;
   {
     double ppn = AT(S0, nk);
-    double dz_n = (gz[nk * sk] - gz[(nk - 1) * sk]) / grav;  // dz(nk-1)
-    AT(S1, nk) = t1g / dz_n * (AT(S2, nk) + ppn);            // aa(nk)
-    for (int k = nk - 1; k >= 1; --k) {
-      const double ppk = AT(S0, k) - AT(S1, k) * ppn;
-      AT(S0, k) = ppk;
-      const double dz_k = (gz[k * sk] - gz[(k - 1) * sk]) / grav;  // dz(k-1)
-      AT(S1, k) = t1g / (dz_k + dz_n) * (AT(S2, k) + ppk);        // aa(k) = t1g/(dz(k-1)+dz(k))*(pem+pp)
-      dz_n = dz_k;
-      ppn = ppk;
-    }
+    double gzn = gz[(nk - 1) * sk];
+    double dz_n = (gz[nk * sk] - gzn) / grav;          // dz(nk-1)
+    AT(S1, nk) = t1g / dz_n * (AT(S2, nk) + ppn);       // aa(nk)
+    pipelined<PF, D1>(
+        nk - 1, [&](int s) { return D1{gz[(nk - 2 - s) * sk]}; },  // k = nk-1-s: gz(k-1)
+        [&](int s, const D1& v) {
+          const int k = nk - 1 - s;
+          const double ppk = AT(S0, k) - AT(S1, k) * ppn;
+          AT(S0, k) = ppk;
+          const double dz_k = (gzn - v.x) / grav;                    // dz(k-1)
+          AT(S1, k) = t1g / (dz_k + dz_n) * (AT(S2, k) + ppk);      // aa(k) = t1g/(dz(k-1)+dz(k))*(pem+pp)
+          dz_n = dz_k;
+          ppn = ppk;
+          gzn = v.x;
+        });
   }
 
   // ---- pass C (forward): riem_w_sweep ----------------------------------
   const double ws = a.ws(i, j, 0);
   {
     double bw = 0.0, w2p = 0.0;
-    for (int l = 0; l < nk; ++l) {
-      const double dml = dm[l * sk], wl = w[l * sk];
-      const double aal = AT(S1, l), aan = AT(S1, l + 1);
-      double w2l;
-      if (l == 0) {
-        bw = dml - aan;
-        w2l = (dml * wl + dt * AT(S0, 1)) / bw;
-      } else {
-        const double gw = aal / bw;
-        bw = dml - (aal + aan + aal * gw);
-        if (l < nk - 1)
-          w2l = (dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aal * w2p) / bw;
-        else
-          w2l = (dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aan * ws - aal * w2p) / bw;
-        AT(S1, l) = gw;  // aa(l) no longer needed
-      }
-      AT(S2, l) = w2l;
-      w2p = w2l;
-    }
+    pipelined<PF, D2>(
+        nk, [&](int l) { return D2{__ldg(dm + l * sk), __ldg(w + l * sk)}; },
+        [&](int l, const D2& v) {
+          const double dml = v.x, wl = v.y;
+          const double aal = AT(S1, l), aan = AT(S1, l + 1);
+          double w2l;
+          if (l == 0) {
+            bw = dml - aan;
+            w2l = (dml * wl + dt * AT(S0, 1)) / bw;
+          } else {
+            const double gw = aal / bw;
+            bw = dml - (aal + aan + aal * gw);
+            if (l < nk - 1)
+              w2l = (dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aal * w2p) / bw;
+            else
+              w2l = (dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aan * ws - aal * w2p) / bw;
+            AT(S1, l) = gw;  // aa(l) no longer needed
+          }
+          AT(S2, l) = w2l;
+          w2p = w2l;
+        });
   }
 
   // ---- pass D (backward): riem_w_back ----------------------------------
   {
     double w2n = AT(S2, nk - 1);
     double* wo = a.has_wout ? a.wout.ptr(i, j, 0) : nullptr;
-    if (wo) wo[(nk - 1) * a.wout.sk] = w2n;
+    const int64_t so = a.wout.sk;
+    if (wo) wo[(nk - 1) * so] = w2n;
     for (int l = nk - 2; l >= 0; --l) {
       const double w2l = AT(S2, l) - AT(S1, l + 1) * w2n;
       AT(S2, l) = w2l;
-      if (wo) wo[l * a.wout.sk] = w2l;
+      if (wo) wo[l * so] = w2l;
       w2n = w2l;
     }
   }
@@ -147,17 +191,21 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
   // ---- pass E (forward): riem_pe, riem_out (pem recomputed in order) -----
   {
     double pe2 = 0.0, pem = ptop;
+    double* pf = a.pef.ptr(i, j, 0);
+    const int64_t so = a.pef.sk;
     AT(S0, 0) = 0.0;
     AT(S1, 0) = ptop;
-    a.pef.ptr(i, j, 0)[0] = pe2 + pem;
-    for (int k = 1; k <= nk; ++k) {
-      const double dml = dm[(k - 1) * sk];
-      pe2 = pe2 + dml * (AT(S2, k - 1) - w[(k - 1) * sk]) / dt;
-      pem = pem + dml;
-      AT(S0, k) = pe2;
-      AT(S1, k) = pem;
-      a.pef.ptr(i, j, 0)[k * a.pef.sk] = pe2 + pem;
-    }
+    pf[0] = pe2 + pem;
+    pipelined<PF, D2>(
+        nk, [&](int s) { return D2{__ldg(dm + s * sk), __ldg(w + s * sk)}; },  // k = s+1: layer k-1
+        [&](int s, const D2& v) {
+          const int k = s + 1;
+          pe2 = pe2 + v.x * (AT(S2, k - 1) - v.y) / dt;
+          pem = pem + v.x;
+          AT(S0, k) = pe2;
+          AT(S1, k) = pem;
+          pf[k * so] = pe2 + pem;
+        });
   }
 
   // ---- pass F (backward): riem_gz ---------------------------------------
@@ -166,13 +214,16 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
     const int64_t so = a.gzo.sk;
     double gzn = gz[nk * sk];
     go[nk * so] = gzn;
-    for (int l = nk - 1; l >= 0; --l) {
-      const double dml = dm[l * sk];
-      const double pm = dml / det_log(AT(S1, l + 1) / AT(S1, l));
-      const double g = gzn + dml * rdgas * pt[l * sk] / np_max(a.p_fac * pm, pm + 0.5 * (AT(S0, l) + AT(S0, l + 1)));
-      go[l * so] = g;
-      gzn = g;
-    }
+    pipelined<PF, D2>(
+        nk, [&](int s) { return D2{__ldg(dm + (nk - 1 - s) * sk), __ldg(pt + (nk - 1 - s) * sk)}; },
+        [&](int s, const D2& v) {
+          const int l = nk - 1 - s;
+          const double dml = v.x;
+          const double pm = dml / det_log(AT(S1, l + 1) / AT(S1, l));
+          const double g = gzn + dml * rdgas * v.y / np_max(a.p_fac * pm, pm + 0.5 * (AT(S0, l) + AT(S0, l + 1)));
+          go[l * so] = g;
+          gzn = g;
+        });
   }
 #undef AT
 }
@@ -199,36 +250,51 @@ __global__ void __launch_bounds__(NC) remap_kernel(const RemapArgs a) {
   const int cidx = blockIdx.x * NC + c;
   if (cidx >= a.ni * a.nj) return;
   const int i = cidx % a.ni, j = cidx / a.ni;
-  double* G = sm + c;           // gam
+  double* G = sm + c;           // gam (depends on delp only: shared by all tracers)
   double* E = sm + L * NC + c;  // qe
 #define AT(S, k) (S)[(k) * NC]
   const int64_t off = i + (int64_t)j * a.sj, sk = a.sk;
-  const double* dp = a.delp.ptr(i, j, 0);
+  const double* __restrict__ dp = a.delp.ptr(i, j, 0);
+  // gam of remap_edge_fwd, once per column
+  const double dp0 = __ldg(dp), dp1 = __ldg(dp + sk);
+  const double grat0 = dp1 / dp0;
+  const double bet0 = grat0 * (grat0 + 0.5);
+  AT(G, 0) = (1.0 + grat0 * (grat0 + 1.5)) / bet0;
+  double d4last = 0.0;
+  {
+    double dprev = dp0, gprev = AT(G, 0);
+    pipelined<PF, D1>(
+        nk - 1, [&](int s) { return D1{__ldg(dp + (s + 1) * sk)}; },
+        [&](int s, const D1& v) {
+          const double d4 = dprev / v.x;
+          const double bet = 2.0 + d4 + d4 - gprev;
+          gprev = d4 / bet;
+          AT(G, s + 1) = gprev;
+          dprev = v.x;
+          d4last = d4;
+        });
+  }
   for (int t = 0; t < a.nq; ++t) {
-    const double* q = a.q[t] + off;
-    // forward: remap_edge_fwd
-    double d4p = 0.0;
+    const double* __restrict__ q = a.q[t] + off;
+    // forward: remap_edge_fwd (qe)
+    const double q0 = __ldg(q), q1 = __ldg(q + sk);
+    AT(E, 0) = ((grat0 + grat0) * (grat0 + 1.0) * q0 + q1) / bet0;
     {
-      const double dp0 = dp[0], dp1 = dp[sk];
-      const double grat = dp1 / dp0;
-      const double bet = grat * (grat + 0.5);
-      AT(E, 0) = ((grat + grat) * (grat + 1.0) * q[0] + q[sk]) / bet;
-      AT(G, 0) = (1.0 + grat * (grat + 1.5)) / bet;
-    }
-    double dprev = dp[0], qprev = q[0];
-    for (int k = 1; k < nk; ++k) {
-      const double dk = dp[k * sk], qk = q[k * sk];
-      const double d4 = dprev / dk;
-      const double bet = 2.0 + d4 + d4 - AT(G, k - 1);
-      AT(E, k) = (3.0 * (qprev + d4 * qk) - AT(E, k - 1)) / bet;
-      AT(G, k) = d4 / bet;
-      d4p = d4;
-      dprev = dk;
-      qprev = qk;
-    }
-    {
+      double dprev = dp0, qprev = q0, eprev = AT(E, 0);
+      pipelined<PF, D2>(
+          nk - 1, [&](int s) { return D2{__ldg(dp + (s + 1) * sk), __ldg(q + (s + 1) * sk)}; },
+          [&](int s, const D2& v) {
+            const int k = s + 1;
+            const double d4 = dprev / v.x;
+            const double bet = 2.0 + d4 + d4 - AT(G, k - 1);
+            eprev = (3.0 * (qprev + d4 * v.y) - eprev) / bet;
+            AT(E, k) = eprev;
+            dprev = v.x;
+            qprev = v.y;
+          });
+      const double d4p = d4last;
       const double abot = 1.0 + d4p * (d4p + 1.5);
-      AT(E, nk) = (2.0 * d4p * (d4p + 1.0) * q[(nk - 1) * sk] + q[(nk - 2) * sk] - abot * AT(E, nk - 1)) /
+      AT(E, nk) = (2.0 * d4p * (d4p + 1.0) * qprev + __ldg(q + (nk - 2) * sk) - abot * eprev) /
                   (d4p * (d4p + 0.5) - abot * AT(G, nk - 1));
     }
     // backward: remap_edge_bwd fused with remap_a4 for layer k
@@ -236,29 +302,35 @@ __global__ void __launch_bounds__(NC) remap_kernel(const RemapArgs a) {
     double* o3 = a.a3[t] + off;
     double* o4 = a.a4[t] + off;
     double qen = AT(E, nk);
-    for (int k = nk - 1; k >= 0; --k) {
-      const double qek = AT(E, k) - AT(G, k) * qen;
-      const double qc = q[k * sk];
-      const double al = qek, ar = qen;
-      const double ext = (ar - qc) * (qc - al);
-      const double da1 = ar - al;
-      const double a6 = 3.0 * (2.0 * qc - (al + ar));
-      const double a6da = a6 * da1;
-      const double da2 = da1 * da1;
-      const double v2 = (ext <= 0.0) ? qc : ((a6da > da2) ? 3.0 * qc - 2.0 * ar : al);
-      const double v3 = (ext <= 0.0) ? qc : ((a6da < -da2) ? 3.0 * qc - 2.0 * al : ar);
-      o2[k * sk] = v2;
-      o3[k * sk] = v3;
-      o4[k * sk] = 3.0 * (2.0 * qc - (v2 + v3));
-      qen = qek;
-    }
+    pipelined<PF, D1>(
+        nk, [&](int s) { return D1{__ldg(q + (nk - 1 - s) * sk)}; },
+        [&](int s, const D1& v) {
+          const int k = nk - 1 - s;
+          const double qek = AT(E, k) - AT(G, k) * qen;
+          const double qc = v.x;
+          const double al = qek, ar = qen;
+          const double ext = (ar - qc) * (qc - al);
+          const double da1 = ar - al;
+          const double a6 = 3.0 * (2.0 * qc - (al + ar));
+          const double a6da = a6 * da1;
+          const double da2 = da1 * da1;
+          const double v2 = (ext <= 0.0) ? qc : ((a6da > da2) ? 3.0 * qc - 2.0 * ar : al);
+          const double v3 = (ext <= 0.0) ? qc : ((a6da < -da2) ? 3.0 * qc - 2.0 * al : ar);
+          o2[k * sk] = v2;
+          o3[k * sk] = v3;
+          o4[k * sk] = 3.0 * (2.0 * qc - (v2 + v3));
+          qen = qek;
+        });
   }
 #undef AT
 }
 
 static int set_smem(const void* fn, size_t bytes) {
-  if (bytes > 48 * 1024 &&
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+  // shared memory bounds how many column recurrences are in flight per SM:
+  // take the whole 228 KB carve-out
+  if ((bytes > 48 * 1024 &&
+       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) ||
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
     return check_launch("smem attribute");
   return FV3B_OK;
 }
