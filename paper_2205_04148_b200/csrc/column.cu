@@ -7,7 +7,7 @@
 // of the I-unit-stride Layout.  The DSL expresses each tridiagonal solve as a
 // FORWARD stencil followed by a BACKWARD stencil (validate.py:171-186); the
 // values a backward sweep consumes are staged per column in shared memory
-// (NC columns x (nk+1) levels per array) so nothing round-trips through HBM.
+// (up to 32 columns x (nk+1) levels per array) so nothing round-trips through HBM.
 // Every statement is evaluated with the .stn's operation order, so results
 // are bitwise the interpreter's (log is the deterministic det_log of the
 // oracle extension, detmath.cuh).
@@ -15,10 +15,11 @@
 
 #include "column.cuh"
 #include "detmath.cuh"
+#include "fastdiv.cuh"
 
 namespace fv3b {
 
-constexpr int NC = 32;  // columns per CTA (one warp)
+constexpr int NC_MAX = 32;  // columns per CTA (at most one warp; see cols_per_cta)
 
 // numpy.maximum semantics (NaN-propagating, reference.py:247-257)
 __device__ __forceinline__ double np_max(double a, double b) {
@@ -35,44 +36,46 @@ __device__ __forceinline__ double np_max(double a, double b) {
 // use(s, T) runs strictly in step order.
 template <int U, class T, class LoadF, class UseF>
 __device__ __forceinline__ void pipelined(int n, LoadF load, UseF use) {
-  T a[U], b[U];
+  // ring of U register slots; step s uses the value loaded U steps earlier.
+  // Loads are clamped to the last step (always a valid level) so the main
+  // loop carries no guards and the compiler can interleave the independent
+  // work (logs, divisions) of U consecutive levels around the recurrence.
+  // The body is instantiated U + 1 times only: the kernels are large and a
+  // few warps per SM cannot hide instruction-cache misses.
+  T a[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u)
-    if (u < n) a[u] = load(u);
-  for (int s0 = 0; s0 < n; s0 += 2 * U) {
+  for (int u = 0; u < U; ++u) a[u] = load(min(u, n - 1));
+  int s0 = 0;
+  for (; s0 + U <= n; s0 += U) {
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (s0 + U + u < n) b[u] = load(s0 + U + u);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (s0 + u < n) use(s0 + u, a[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (s0 + 2 * U + u < n) a[u] = load(s0 + 2 * U + u);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (s0 + U + u < n) use(s0 + U + u, b[u]);
+    for (int u = 0; u < U; ++u) {
+      const T v = a[u];
+      a[u] = load(min(s0 + U + u, n - 1));
+      use(s0 + u, v);
+    }
   }
+#pragma unroll 1
+  for (int s = s0; s < n; ++s) use(s, load(s));
 }
 
 struct D1 { double x; };
 struct D2 { double x, y; };
 struct D3 { double x, y, z; };
 
-constexpr int PF = 8;  // prefetch distance (levels)
+constexpr int PF = 4;  // prefetch distance (levels)
 
-// Statement-for-statement restatement of templates.riem_stencils.
-__global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
-  extern __shared__ double sm[];
+// Statement-for-statement restatement of templates.riem_stencils for one
+// column.  FAST: branch-free divisions/logs (fastdiv.cuh), returns false if
+// any of them left nvcc's fast-path range, in which case the caller
+// re-evaluates the column with EXACT.  In FAST mode the gz output is staged
+// in S2 and only written by the caller (gz may alias gz_out).
+template <bool FAST>
+__device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int c, int NC, double* sm) {
+  ColArith<FAST> ar;
   const int nk = a.nk, L = nk + 1;
-  const int c = threadIdx.x;
-  const int i = a.ilo + (blockIdx.x * NC + c) % a.ni_ext;
-  const int cidx = blockIdx.x * NC + c;
-  if (cidx >= a.ni_ext * a.nj_ext) return;
-  const int j = a.jlo + cidx / a.ni_ext;
   double* S0 = sm + c;               // pp, later pe2
   double* S1 = sm + L * NC + c;      // gam -> aa -> gw -> pem
-  double* S2 = sm + 2 * L * NC + c;  // pem -> w2
+  double* S2 = sm + 2 * L * NC + c;  // pem -> w2 -> (FAST) gz
 #define AT(S, k) (S)[(k) * NC]
   const double dt = a.dt, ptop = a.ptop, rdgas = a.rdgas, grav = a.grav, gama = a.gama;
   const double* __restrict__ dm = a.dm.ptr(i, j, 0);
@@ -96,10 +99,10 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
           const double dm_n = v.x, gzk1 = v.y;
           const double pem1 = pem0 + dm_k;  // pem(k+1) = pem + dm
           AT(S2, k + 1) = pem1;
-          const double pmk = dm_k / det_log(pem1 / pem0);
-          const double pek = dm_k * rdgas * v.z / (gzk - gzk1) - pmk;
+          const double pmk = ar.div(dm_k, ar.log(ar.div(pem1, pem0)));
+          const double pek = ar.div(dm_k * rdgas * v.z, gzk - gzk1) - pmk;
           // layer k coefficients (riem_coef)
-          const double grat = (k < nk - 1) ? dm_k / dm_n : 0.0;
+          const double grat = (k < nk - 1) ? ar.div(dm_k, dm_n) : 0.0;
           const double bb = (k < nk - 1) ? 2.0 * (1.0 + grat) : 2.0;
           // interface k of riem_pp_fwd (uses layer k-1's dd, needing pe(k))
           if (k == 0) {
@@ -108,8 +111,8 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
             AT(S0, 0) = 0.0;
           } else {
             const double dd_prev = (k - 1 < nk - 1) ? 3.0 * (pe_prev + grat_prev * pek) : 3.0 * pe_prev;
-            const double ppk = (k == 1) ? dd_prev / bet_prev : (dd_prev - pp_prev) / bet_prev;
-            const double gam = grat_prev / bet_prev;
+            const double ppk = ar.div((k == 1) ? dd_prev : dd_prev - pp_prev, bet_prev);
+            const double gam = ar.div(grat_prev, bet_prev);
             bet_prev = bb - gam;
             pp_prev = ppk;
             AT(S0, k) = ppk;
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
         });
     // interface nk: pp = (dd[nk-1] - pp[nk-1]) / bet[nk-1], dd[nk-1] = 3*pe[nk-1]
     const double dd_prev = 3.0 * pe_prev;
-    AT(S0, nk) = (nk == 1) ? dd_prev / bet_prev : (dd_prev - pp_prev) / bet_prev;
+    AT(S0, nk) = ar.div((nk == 1) ? dd_prev : dd_prev - pp_prev, bet_prev);
   }
 
   // ---- pass B (backward): riem_pp_bwd, then aa (riem_w_fwd) -------------
@@ -131,16 +134,16 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
   {
     double ppn = AT(S0, nk);
     double gzn = gz[(nk - 1) * sk];
-    double dz_n = (gz[nk * sk] - gzn) / grav;          // dz(nk-1)
-    AT(S1, nk) = t1g / dz_n * (AT(S2, nk) + ppn);       // aa(nk)
+    double dz_n = ar.div(gz[nk * sk] - gzn, grav);          // dz(nk-1)
+    AT(S1, nk) = ar.div(t1g, dz_n) * (AT(S2, nk) + ppn);     // aa(nk)
     pipelined<PF, D1>(
         nk - 1, [&](int s) { return D1{gz[(nk - 2 - s) * sk]}; },  // k = nk-1-s: gz(k-1)
         [&](int s, const D1& v) {
           const int k = nk - 1 - s;
           const double ppk = AT(S0, k) - AT(S1, k) * ppn;
           AT(S0, k) = ppk;
-          const double dz_k = (gzn - v.x) / grav;                    // dz(k-1)
-          AT(S1, k) = t1g / (dz_k + dz_n) * (AT(S2, k) + ppk);      // aa(k) = t1g/(dz(k-1)+dz(k))*(pem+pp)
+          const double dz_k = ar.div(gzn - v.x, grav);                   // dz(k-1)
+          AT(S1, k) = ar.div(t1g, dz_k + dz_n) * (AT(S2, k) + ppk);     // aa(k) = t1g/(dz(k-1)+dz(k))*(pem+pp)
           dz_n = dz_k;
           ppn = ppk;
           gzn = v.x;
@@ -159,14 +162,14 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
           double w2l;
           if (l == 0) {
             bw = dml - aan;
-            w2l = (dml * wl + dt * AT(S0, 1)) / bw;
+            w2l = ar.div(dml * wl + dt * AT(S0, 1), bw);
           } else {
-            const double gw = aal / bw;
+            const double gw = ar.div(aal, bw);
             bw = dml - (aal + aan + aal * gw);
             if (l < nk - 1)
-              w2l = (dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aal * w2p) / bw;
+              w2l = ar.div(dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aal * w2p, bw);
             else
-              w2l = (dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aan * ws - aal * w2p) / bw;
+              w2l = ar.div(dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aan * ws - aal * w2p, bw);
             AT(S1, l) = gw;  // aa(l) no longer needed
           }
           AT(S2, l) = w2l;
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
         nk, [&](int s) { return D2{__ldg(dm + s * sk), __ldg(w + s * sk)}; },  // k = s+1: layer k-1
         [&](int s, const D2& v) {
           const int k = s + 1;
-          pe2 = pe2 + v.x * (AT(S2, k - 1) - v.y) / dt;
+          pe2 = pe2 + ar.div(v.x * (AT(S2, k - 1) - v.y), dt);
           pem = pem + v.x;
           AT(S0, k) = pe2;
           AT(S1, k) = pem;
@@ -213,19 +216,37 @@ __global__ void __launch_bounds__(NC) riem_kernel(const RiemArgs a) {
     double* go = a.gzo.ptr(i, j, 0);
     const int64_t so = a.gzo.sk;
     double gzn = gz[nk * sk];
-    go[nk * so] = gzn;
+    if (FAST) AT(S2, nk) = gzn; else go[nk * so] = gzn;
     pipelined<PF, D2>(
         nk, [&](int s) { return D2{__ldg(dm + (nk - 1 - s) * sk), __ldg(pt + (nk - 1 - s) * sk)}; },
         [&](int s, const D2& v) {
           const int l = nk - 1 - s;
           const double dml = v.x;
-          const double pm = dml / det_log(AT(S1, l + 1) / AT(S1, l));
-          const double g = gzn + dml * rdgas * v.y / np_max(a.p_fac * pm, pm + 0.5 * (AT(S0, l) + AT(S0, l + 1)));
-          go[l * so] = g;
+          const double pm = ar.div(dml, ar.log(ar.div(AT(S1, l + 1), AT(S1, l))));
+          const double g = gzn + ar.div(dml * rdgas * v.y, np_max(a.p_fac * pm, pm + 0.5 * (AT(S0, l) + AT(S0, l + 1))));
+          if (FAST) AT(S2, l) = g; else go[l * so] = g;
           gzn = g;
         });
   }
 #undef AT
+  return ar.ok;
+}
+
+__global__ void __launch_bounds__(NC_MAX) riem_kernel(const RiemArgs a) {
+  extern __shared__ double sm[];
+  const int c = threadIdx.x, NC = blockDim.x;
+  const int cidx = blockIdx.x * NC + c;
+  if (cidx >= a.ni_ext * a.nj_ext) return;
+  const int i = a.ilo + cidx % a.ni_ext;
+  const int j = a.jlo + cidx / a.ni_ext;
+  if (riem_column<true>(a, i, j, c, NC, sm)) {
+    const int nk = a.nk, L = nk + 1;
+    const double* S2 = sm + 2 * L * NC + c;
+    double* go = a.gzo.ptr(i, j, 0);
+    for (int l = 0; l <= nk; ++l) go[l * a.gzo.sk] = S2[l * NC];
+  } else {
+    riem_column<false>(a, i, j, c, NC, sm);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -243,13 +264,10 @@ struct RemapArgs {
   int nq, ni, nj, nk;  // nk layers (program domain nk+1)
 };
 
-__global__ void __launch_bounds__(NC) remap_kernel(const RemapArgs a) {
-  extern __shared__ double sm[];
+template <bool FAST>
+__device__ __forceinline__ bool remap_column(const RemapArgs& a, int i, int j, int c, int NC, double* sm) {
+  ColArith<FAST> ar;
   const int nk = a.nk, L = nk + 1;
-  const int c = threadIdx.x;
-  const int cidx = blockIdx.x * NC + c;
-  if (cidx >= a.ni * a.nj) return;
-  const int i = cidx % a.ni, j = cidx / a.ni;
   double* G = sm + c;           // gam (depends on delp only: shared by all tracers)
   double* E = sm + L * NC + c;  // qe
 #define AT(S, k) (S)[(k) * NC]
@@ -257,18 +275,18 @@ __global__ void __launch_bounds__(NC) remap_kernel(const RemapArgs a) {
   const double* __restrict__ dp = a.delp.ptr(i, j, 0);
   // gam of remap_edge_fwd, once per column
   const double dp0 = __ldg(dp), dp1 = __ldg(dp + sk);
-  const double grat0 = dp1 / dp0;
+  const double grat0 = ar.div(dp1, dp0);
   const double bet0 = grat0 * (grat0 + 0.5);
-  AT(G, 0) = (1.0 + grat0 * (grat0 + 1.5)) / bet0;
+  AT(G, 0) = ar.div(1.0 + grat0 * (grat0 + 1.5), bet0);
   double d4last = 0.0;
   {
     double dprev = dp0, gprev = AT(G, 0);
     pipelined<PF, D1>(
         nk - 1, [&](int s) { return D1{__ldg(dp + (s + 1) * sk)}; },
         [&](int s, const D1& v) {
-          const double d4 = dprev / v.x;
+          const double d4 = ar.div(dprev, v.x);
           const double bet = 2.0 + d4 + d4 - gprev;
-          gprev = d4 / bet;
+          gprev = ar.div(d4, bet);
           AT(G, s + 1) = gprev;
           dprev = v.x;
           d4last = d4;
@@ -278,24 +296,24 @@ __global__ void __launch_bounds__(NC) remap_kernel(const RemapArgs a) {
     const double* __restrict__ q = a.q[t] + off;
     // forward: remap_edge_fwd (qe)
     const double q0 = __ldg(q), q1 = __ldg(q + sk);
-    AT(E, 0) = ((grat0 + grat0) * (grat0 + 1.0) * q0 + q1) / bet0;
+    AT(E, 0) = ar.div((grat0 + grat0) * (grat0 + 1.0) * q0 + q1, bet0);
     {
       double dprev = dp0, qprev = q0, eprev = AT(E, 0);
       pipelined<PF, D2>(
           nk - 1, [&](int s) { return D2{__ldg(dp + (s + 1) * sk), __ldg(q + (s + 1) * sk)}; },
           [&](int s, const D2& v) {
             const int k = s + 1;
-            const double d4 = dprev / v.x;
+            const double d4 = ar.div(dprev, v.x);
             const double bet = 2.0 + d4 + d4 - AT(G, k - 1);
-            eprev = (3.0 * (qprev + d4 * v.y) - eprev) / bet;
+            eprev = ar.div(3.0 * (qprev + d4 * v.y) - eprev, bet);
             AT(E, k) = eprev;
             dprev = v.x;
             qprev = v.y;
           });
       const double d4p = d4last;
       const double abot = 1.0 + d4p * (d4p + 1.5);
-      AT(E, nk) = (2.0 * d4p * (d4p + 1.0) * qprev + __ldg(q + (nk - 2) * sk) - abot * eprev) /
-                  (d4p * (d4p + 0.5) - abot * AT(G, nk - 1));
+      AT(E, nk) = ar.div(2.0 * d4p * (d4p + 1.0) * qprev + __ldg(q + (nk - 2) * sk) - abot * eprev,
+                         d4p * (d4p + 0.5) - abot * AT(G, nk - 1));
     }
     // backward: remap_edge_bwd fused with remap_a4 for layer k
     double* o2 = a.a2[t] + off;
@@ -308,14 +326,14 @@ __global__ void __launch_bounds__(NC) remap_kernel(const RemapArgs a) {
           const int k = nk - 1 - s;
           const double qek = AT(E, k) - AT(G, k) * qen;
           const double qc = v.x;
-          const double al = qek, ar = qen;
-          const double ext = (ar - qc) * (qc - al);
-          const double da1 = ar - al;
-          const double a6 = 3.0 * (2.0 * qc - (al + ar));
+          const double al = qek, ar_ = qen;
+          const double ext = (ar_ - qc) * (qc - al);
+          const double da1 = ar_ - al;
+          const double a6 = 3.0 * (2.0 * qc - (al + ar_));
           const double a6da = a6 * da1;
           const double da2 = da1 * da1;
-          const double v2 = (ext <= 0.0) ? qc : ((a6da > da2) ? 3.0 * qc - 2.0 * ar : al);
-          const double v3 = (ext <= 0.0) ? qc : ((a6da < -da2) ? 3.0 * qc - 2.0 * al : ar);
+          const double v2 = (ext <= 0.0) ? qc : ((a6da > da2) ? 3.0 * qc - 2.0 * ar_ : al);
+          const double v3 = (ext <= 0.0) ? qc : ((a6da < -da2) ? 3.0 * qc - 2.0 * al : ar_);
           o2[k * sk] = v2;
           o3[k * sk] = v3;
           o4[k * sk] = 3.0 * (2.0 * qc - (v2 + v3));
@@ -323,6 +341,17 @@ __global__ void __launch_bounds__(NC) remap_kernel(const RemapArgs a) {
         });
   }
 #undef AT
+  return ar.ok;
+}
+
+__global__ void __launch_bounds__(NC_MAX) remap_kernel(const RemapArgs a) {
+  extern __shared__ double sm[];
+  const int c = threadIdx.x, NC = blockDim.x;
+  const int cidx = blockIdx.x * NC + c;
+  if (cidx >= a.ni * a.nj) return;
+  const int i = cidx % a.ni, j = cidx / a.ni;
+  // outputs never alias inputs: a failed fast evaluation is simply redone
+  if (!remap_column<true>(a, i, j, c, NC, sm)) remap_column<false>(a, i, j, c, NC, sm);
 }
 
 static int set_smem(const void* fn, size_t bytes) {
@@ -335,11 +364,33 @@ static int set_smem(const void* fn, size_t bytes) {
   return FV3B_OK;
 }
 
+// Columns per CTA (<= 32, one warp) for a column kernel staging
+// `bytes_per_col` of shared memory: maximise resident columns per SM with a
+// CTA count that is a multiple of the 4 SM sub-partitions, so every warp
+// scheduler owns the same number of recurrences.
+static int cols_per_cta(size_t bytes_per_col) {
+  const size_t per_sm = 228 * 1024, reserved = 1024;
+  int best_cols = 1, best_total = 0;
+  for (int m = 4; m <= 32; m += 4) {
+    const size_t avail = per_sm / m;
+    if (avail <= reserved) break;
+    int cols = (int)((avail - reserved) / bytes_per_col);
+    if (cols > NC_MAX) cols = NC_MAX;
+    if (cols >= 1 && cols * m > best_total) {
+      best_total = cols * m;
+      best_cols = cols;
+    }
+  }
+  return best_cols;
+}
+
 int launch_riem(const RiemArgs& a, cudaStream_t st) {
-  const size_t bytes = 3 * (size_t)(a.nk + 1) * NC * sizeof(double);
+  const size_t per_col = 3 * (size_t)(a.nk + 1) * sizeof(double);
+  const int nc = cols_per_cta(per_col);
+  const size_t bytes = per_col * nc;
   FV3B_TRY(set_smem((const void*)riem_kernel, bytes));
   const int cols = a.ni_ext * a.nj_ext;
-  riem_kernel<<<cdiv(cols, NC), NC, bytes, st>>>(a);
+  riem_kernel<<<cdiv(cols, nc), nc, bytes, st>>>(a);
   return check_launch("riem_solver_c");
 }
 
@@ -405,8 +456,10 @@ extern "C" int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, 
   a.nj = d->nj;
   a.nk = d->nk - 1;
   if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
-  const size_t bytes = 2 * (size_t)(a.nk + 1) * NC * sizeof(double);
+  const size_t per_col = 2 * (size_t)(a.nk + 1) * sizeof(double);
+  const int nc = cols_per_cta(per_col);
+  const size_t bytes = per_col * nc;
   FV3B_TRY(set_smem((const void*)remap_kernel, bytes));
-  remap_kernel<<<cdiv(a.ni * a.nj, NC), NC, bytes, (cudaStream_t)stream>>>(a);
+  remap_kernel<<<cdiv(a.ni * a.nj, nc), nc, bytes, (cudaStream_t)stream>>>(a);
   return check_launch("remap_profile");
 }
