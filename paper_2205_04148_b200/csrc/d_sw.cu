@@ -11,6 +11,9 @@
 // offset reads of u/v/w/delp/pt all precede their writes in the .stn).
 // All temporaries are shared-memory tiles computed over the rectangles the
 // later statements read (extents.py:128-164 restricted to the tile).
+#include <string.h>
+
+#include "dsw.cuh"
 #include "tile.cuh"
 
 namespace fv3b {
@@ -86,64 +89,6 @@ __device__ __forceinline__ void tp2d(const DswArgs& a, const Arr<G>& Q, const Ar
   __syncthreads();
   fill(FXO, 0, TI + 1, 0, TJ, [&](int i, int j) { return 0.5 * (FXO(i, j) + FX2(i, j)) * WX(i, j); });
   fill(FYO, 0, TI, 0, TJ + 1, [&](int i, int j) { return 0.5 * (FYO(i, j) + FY2(i, j)) * WY(i, j); });
-}
-
-__global__ void __launch_bounds__(DSW_NT, 1) d_sw_transport_kernel(const DswArgs a) {
-  extern __shared__ __align__(128) double smem[];
-  using G = GD;
-  constexpr int TI = G::TI, TJ = G::TJ;
-  int s = 0;
-  auto arr = [&]() { return Arr<G>{smem + (s++) * G::NA}; };
-  const Arr<G> CRX = arr(), XFX = arr(), CRY = arr(), YFX = arr(), DP = arr(), PT = arr(), WW = arr();
-  const Arr<G> FY2 = arr(), FX2 = arr(), QI = arr(), QJ = arr(), T1 = arr(), T2 = arr(), FXM = arr(), FYM = arr();
-  const int gi0 = blockIdx.x * TI, gj0 = blockIdx.y * TJ, k = blockIdx.z;
-  const int ni = a.ni, nj = a.nj;
-
-  load(DP, a.delp, gi0, gj0, k, -3, TI + 3, -3, TJ + 3, ni, nj, a.hx, a.hy);
-  load(PT, a.pt, gi0, gj0, k, -3, TI + 3, -3, TJ + 3, ni, nj, a.hx, a.hy);
-  load(WW, a.w, gi0, gj0, k, -3, TI + 3, -3, TJ + 3, ni, nj, a.hx, a.hy);
-  courant(a, CRX, XFX, CRY, YFX, gi0, gj0, k, -3, TJ + 3, -3, TI + 3);
-  __syncthreads();
-  // d_sw_mass: fv_tp_2d(delp) -> mass fluxes fxm, fym
-  tp2d(a, DP, CRX, XFX, CRY, YFX, XFX, YFX, FY2, FX2, QI, QJ, FXM, FYM, gi0, gj0);
-  __syncthreads();
-  // accumulators (pointwise) and delpn
-  auto delpn = [&](int i, int j) {
-    return DP(i, j) + (FXM(i, j) - FXM(i + 1, j) + FYM(i, j) - FYM(i, j + 1)) * met(a.rarea, gi0 + i, gj0 + j);
-  };
-  each(0, TI, 0, TJ, [&](int i, int j) {
-    const int gi = gi0 + i, gj = gj0 + j;
-    if (gi >= ni || gj >= nj) return;
-    *a.cxo.ptr(gi, gj, k) = *a.cx.ptr(gi, gj, k) + CRX(i, j);
-    *a.cyo.ptr(gi, gj, k) = *a.cy.ptr(gi, gj, k) + CRY(i, j);
-    *a.xfao.ptr(gi, gj, k) = *a.xfa.ptr(gi, gj, k) + XFX(i, j);
-    *a.yfao.ptr(gi, gj, k) = *a.yfa.ptr(gi, gj, k) + YFX(i, j);
-    *a.mfxo.ptr(gi, gj, k) = *a.mfx.ptr(gi, gj, k) + FXM(i, j);
-    *a.mfyo.ptr(gi, gj, k) = *a.mfy.ptr(gi, gj, k) + FYM(i, j);
-  });
-  // d_sw_heat: fv_tp_2d(pt) with mass fluxes
-  tp2d(a, PT, CRX, XFX, CRY, YFX, FXM, FYM, FY2, FX2, QI, QJ, T1, T2, gi0, gj0);
-  __syncthreads();
-  each(0, TI, 0, TJ, [&](int i, int j) {
-    const int gi = gi0 + i, gj = gj0 + j;
-    if (gi >= ni || gj >= nj) return;
-    *a.pto.ptr(gi, gj, k) = (PT(i, j) * DP(i, j) + (T1(i, j) - T1(i + 1, j) + T2(i, j) - T2(i, j + 1)) *
-                                                       met(a.rarea, gi, gj)) / delpn(i, j);
-  });
-  __syncthreads();
-  // d_sw_vert: fv_tp_2d(w) with mass fluxes + del2 damping
-  tp2d(a, WW, CRX, XFX, CRY, YFX, FXM, FYM, FY2, FX2, QI, QJ, T1, T2, gi0, gj0);
-  __syncthreads();
-  each(0, TI, 0, TJ, [&](int i, int j) {
-    const int gi = gi0 + i, gj = gj0 + j;
-    if (gi >= ni || gj >= nj) return;
-    const double wc = WW(i, j);
-    const double dn = delpn(i, j);
-    *a.wo.ptr(gi, gj, k) =
-        (wc * DP(i, j) + (T1(i, j) - T1(i + 1, j) + T2(i, j) - T2(i, j + 1)) * met(a.rarea, gi, gj)) / dn +
-        a.damp_w * (WW(i - 1, j) + WW(i + 1, j) + WW(i, j - 1) + WW(i, j + 1) - 4.0 * wc);
-    *a.delpo.ptr(gi, gj, k) = dn;
-  });
 }
 
 __global__ void __launch_bounds__(DSW_NT, 1) d_sw_momentum_kernel(const DswArgs a) {
@@ -257,17 +202,46 @@ extern "C" int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns, c
   a.p1 = s[0]; a.p2 = s[1]; a.dt = s[2]; a.dddmp = s[3]; a.d2_bg = s[4]; a.da_min = s[5]; a.damp_w = s[6];
   if (d->ni <= 0 || d->nj <= 0 || d->nk <= 0) return FV3B_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  // transport group (delp, pt, w, accumulators): TMA-pipelined level march
+  {
+    Geo g;
+    FV3B_TRY(geo_of(f[0], &g));
+    const int tma_fields[] = {2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 19, 20, 21};
+    for (int t : tma_fields) {
+      Geo h;
+      FV3B_TRY(geo_of(f[t], &h));
+      if (h.pitch != g.pitch || h.rows != g.rows || (f[t].rank == 3 && h.levels != g.levels) || h.i0 != g.i0 ||
+          h.j0 != g.j0)
+        return fail(FV3B_ELAYOUT, "fv3b_d_sw: field %d geometry differs from field 0", t);
+    }
+    DswTpArgs t;
+    memset(&t, 0, sizeof t);
+    const fv3b_field qb[5] = {f[3], f[4], f[2], f[5], f[6]};        // delp, pt, w, uc, vc
+    const fv3b_field ac[6] = {f[7], f[8], f[9], f[10], f[11], f[12]};  // cx, cy, xfa, yfa, mfx, mfy
+    const fv3b_field mt[5] = {f[13], f[14], f[19], f[20], f[21]};      // dx, dy, rdxa, rdya, area
+    FV3B_TRY(dsw_transport_maps(t, g, qb, ac, mt));
+    t.delpo = a.delpo.o;
+    t.pto = a.pto.o;
+    t.wo = a.wo.o;
+    View* ao[6] = {&a.cxo, &a.cyo, &a.xfao, &a.yfao, &a.mfxo, &a.mfyo};
+    for (int u = 0; u < 6; ++u) t.acco[u] = ao[u]->o;
+    t.rarea = a.rarea.o;
+    t.sj = a.u.sj;
+    t.sk = a.u.sk;
+    t.i0 = g.i0;
+    t.j0 = g.j0;
+    t.ni = d->ni; t.nj = d->nj; t.nk = d->nk;
+    t.p1 = a.p1; t.p2 = a.p2; t.dt = a.dt; t.damp_w = a.damp_w;
+    FV3B_TRY(launch_dsw_transport(t, st));
+  }
   static bool attr = false;
-  const size_t b1 = 15 * GD::NA * sizeof(double), b2 = 16 * GD::NA * sizeof(double);
+  const size_t b2 = 16 * GD::NA * sizeof(double);
   if (!attr) {
-    if (cudaFuncSetAttribute(d_sw_transport_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b1) != cudaSuccess ||
-        cudaFuncSetAttribute(d_sw_momentum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b2) != cudaSuccess)
+    if (cudaFuncSetAttribute(d_sw_momentum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b2) != cudaSuccess)
       return check_launch("d_sw smem attribute");
     attr = true;
   }
   dim3 grid(cdiv(d->ni, GD::TI), cdiv(d->nj, GD::TJ), d->nk);
-  d_sw_transport_kernel<<<grid, DSW_NT, b1, st>>>(a);
-  FV3B_TRY(check_launch("d_sw_transport"));
   d_sw_momentum_kernel<<<grid, DSW_NT, b2, st>>>(a);
   return check_launch("d_sw_momentum");
 }
