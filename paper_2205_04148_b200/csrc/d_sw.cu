@@ -1,25 +1,19 @@
-// K3 d_sw (programs/d_sw.stn; templates.d_sw_stencils).
+// K3 d_sw (programs/d_sw.stn; templates.d_sw_stencils): ABI entry point.
 //
-// Two fused kernels per level tile (32 x 16 columns, halo 4):
-//   d_sw_transport  d_sw_courant + d_sw_mass + d_sw_heat + d_sw_vert and the
-//                   delp / pt / w / accumulator statements of d_sw_update;
-//   d_sw_momentum   d_sw_courant + d_sw_ke + d_sw_vort + d_sw_damp and the
-//                   u / v statements of d_sw_update.
+// Two fused, TMA-pipelined level-marching kernels:
+//   dsw_transport.cu  d_sw_courant + d_sw_mass + d_sw_heat + d_sw_vert and the
+//                     delp / pt / w / accumulator statements of d_sw_update;
+//   dsw_momentum.cu   d_sw_courant + d_sw_ke + d_sw_vort + d_sw_damp and the
+//                     u / v statements of d_sw_update.
 // The split is exact: the transport group never reads u/v and the momentum
 // group never reads delp/pt/w, and every statement of d_sw_update reads the
 // pre-update values (RHS materialised before each store, reference.py:293-299;
 // offset reads of u/v/w/delp/pt all precede their writes in the .stn).
-// All temporaries are shared-memory tiles computed over the rectangles the
-// later statements read (extents.py:128-164 restricted to the tile).
 #include <string.h>
 
 #include "dsw.cuh"
-#include "tile.cuh"
 
 namespace fv3b {
-
-using GD = TileGeo<32, 16, 4, 4>;
-constexpr int DSW_NT = 256;
 
 struct DswArgs {
   View u, v, w, delp, pt, uc, vc;
@@ -29,134 +23,6 @@ struct DswArgs {
   int ni, nj, nk, hx, hy;
   double p1, p2, dt, dddmp, d2_bg, da_min, damp_w;
 };
-
-__device__ __forceinline__ double np_min(double a, double b) {
-  if (isnan(a) || isnan(b)) return a + b;
-  return b < a ? b : a;
-}
-__device__ __forceinline__ double np_max2(double a, double b) {
-  if (isnan(a) || isnan(b)) return a + b;
-  return b > a ? b : a;
-}
-
-// Courant numbers and area fluxes (d_sw_courant) on x faces [0, TI+1) x
-// rows [ja, jb) and y faces [0, TJ+1) x columns [ia, ib).
-template <class G>
-__device__ __forceinline__ void courant(const DswArgs& a, const Arr<G>& CRX, const Arr<G>& XFX, const Arr<G>& CRY,
-                                        const Arr<G>& YFX, int gi0, int gj0, int k, int ja, int jb, int ia, int ib) {
-  constexpr int TI = G::TI, TJ = G::TJ;
-  const double dt = a.dt;
-  each(0, TI + 1, ja, jb, [&](int i, int j) {
-    const int gi = gi0 + i, gj = gj0 + j;
-    const bool ok = gi >= -a.hx + 1 && gi < a.ni + a.hx && gj >= -a.hy && gj < a.nj + a.hy;
-    const double uc = ok ? __ldg(a.uc.ptr(gi, gj, k)) : 0.0;
-    XFX(i, j) = ok ? dt * uc * met(a.dy, gi, gj) : 0.0;
-    CRX(i, j) = ok ? (uc > 0.0 ? dt * uc * met(a.rdxa, gi - 1, gj) : dt * uc * met(a.rdxa, gi, gj)) : 0.0;
-  });
-  each(ia, ib, 0, TJ + 1, [&](int i, int j) {
-    const int gi = gi0 + i, gj = gj0 + j;
-    const bool ok = gi >= -a.hx && gi < a.ni + a.hx && gj >= -a.hy + 1 && gj < a.nj + a.hy;
-    const double vc = ok ? __ldg(a.vc.ptr(gi, gj, k)) : 0.0;
-    YFX(i, j) = ok ? dt * vc * met(a.dx, gi, gj) : 0.0;
-    CRY(i, j) = ok ? (vc > 0.0 ? dt * vc * met(a.rdya, gi, gj - 1) : dt * vc * met(a.rdya, gi, gj)) : 0.0;
-  });
-}
-
-// fv_tp_2d of Q (templates.fv_tp_2d) up to the per-face flux pair; results:
-// FXO faces [0, TI+1) x rows [0, TJ), FYO columns [0, TI) x faces [0, TJ+1),
-// weighted by WX / WY.  Scratch: FY2, FX2, QI, QJ.  Caller syncs before.
-template <class G>
-__device__ __forceinline__ void tp2d(const DswArgs& a, const Arr<G>& Q, const Arr<G>& CRX, const Arr<G>& XFX,
-                                     const Arr<G>& CRY, const Arr<G>& YFX, const Arr<G>& WX, const Arr<G>& WY,
-                                     const Arr<G>& FY2, const Arr<G>& FX2, const Arr<G>& QI, const Arr<G>& QJ,
-                                     const Arr<G>& FXO, const Arr<G>& FYO, int gi0, int gj0) {
-  constexpr int TI = G::TI, TJ = G::TJ;
-  const double p1 = a.p1, p2 = a.p2;
-  ppm_y(FY2, Q, CRY, -3, TI + 3, 0, TJ + 1, p1, p2);
-  ppm_x(FX2, Q, CRX, 0, TI + 1, -3, TJ + 3, p1, p2);
-  __syncthreads();
-  fill(QI, -3, TI + 3, 0, TJ, [&](int i, int j) {
-    const double ar = met(a.area, gi0 + i, gj0 + j);
-    return (Q(i, j) * ar + FY2(i, j) * YFX(i, j) - FY2(i, j + 1) * YFX(i, j + 1)) / (ar + YFX(i, j) - YFX(i, j + 1));
-  });
-  fill(QJ, 0, TI, -3, TJ + 3, [&](int i, int j) {
-    const double ar = met(a.area, gi0 + i, gj0 + j);
-    return (Q(i, j) * ar + FX2(i, j) * XFX(i, j) - FX2(i + 1, j) * XFX(i + 1, j)) / (ar + XFX(i, j) - XFX(i + 1, j));
-  });
-  __syncthreads();
-  ppm_x(FXO, QI, CRX, 0, TI + 1, 0, TJ, p1, p2);
-  ppm_y(FYO, QJ, CRY, 0, TI, 0, TJ + 1, p1, p2);
-  __syncthreads();
-  fill(FXO, 0, TI + 1, 0, TJ, [&](int i, int j) { return 0.5 * (FXO(i, j) + FX2(i, j)) * WX(i, j); });
-  fill(FYO, 0, TI, 0, TJ + 1, [&](int i, int j) { return 0.5 * (FYO(i, j) + FY2(i, j)) * WY(i, j); });
-}
-
-__global__ void __launch_bounds__(DSW_NT, 1) d_sw_momentum_kernel(const DswArgs a) {
-  extern __shared__ __align__(128) double smem[];
-  using G = GD;
-  constexpr int TI = G::TI, TJ = G::TJ;
-  int s = 0;
-  auto arr = [&]() { return Arr<G>{smem + (s++) * G::NA}; };
-  const Arr<G> CRX = arr(), XFX = arr(), CRY = arr(), YFX = arr(), U = arr(), V = arr();
-  const Arr<G> UB = arr(), CUB = arr(), VB = arr(), CVB = arr(), UU = arr(), VV = arr();
-  const Arr<G> WK = arr(), DDV = arr(), FY2 = arr(), FX2 = arr();
-  // dead after the KE statement: reused by the vorticity transport
-  const Arr<G> QI = CUB, QJ = CVB, FXV = UU, FYV = VV;
-  const int gi0 = blockIdx.x * TI, gj0 = blockIdx.y * TJ, k = blockIdx.z;
-  const int ni = a.ni, nj = a.nj;
-  const double dt = a.dt;
-
-  load(U, a.u, gi0, gj0, k, -3, TI + 3, -3, TJ + 4, ni, nj, a.hx, a.hy);
-  load(V, a.v, gi0, gj0, k, -3, TI + 4, -3, TJ + 3, ni, nj, a.hx, a.hy);
-  courant(a, CRX, XFX, CRY, YFX, gi0, gj0, k, -3, TJ + 3, -3, TI + 3);
-  // d_sw_ke: ub/cub, vb/cvb at corners [0, TI+1) x [0, TJ+1)
-  each(0, TI + 1, 0, TJ + 1, [&](int i, int j) {
-    const int gi = gi0 + i, gj = gj0 + j;
-    const double ub = 0.5 * dt * (__ldg(a.uc.ptr(gi, gj - 1, k)) + __ldg(a.uc.ptr(gi, gj, k)));
-    UB(i, j) = ub;
-    CUB(i, j) = ub > 0.0 ? ub * met(a.rdx, gi - 1, gj) : ub * met(a.rdx, gi, gj);
-    const double vb = 0.5 * dt * (__ldg(a.vc.ptr(gi - 1, gj, k)) + __ldg(a.vc.ptr(gi, gj, k)));
-    VB(i, j) = vb;
-    CVB(i, j) = vb > 0.0 ? vb * met(a.rdy, gi, gj - 1) : vb * met(a.rdy, gi, gj);
-  });
-  __syncthreads();
-  ppm_x(UU, U, CUB, 0, TI + 1, 0, TJ + 1, a.p1, a.p2);
-  ppm_y(VV, V, CVB, 0, TI + 1, 0, TJ + 1, a.p1, a.p2);
-  // d_sw_vort: absolute vorticity at centres over the transport halo
-  fill(WK, -3, TI + 3, -3, TJ + 3, [&](int i, int j) {
-    const int gi = gi0 + i, gj = gj0 + j;
-    return met(a.f0, gi, gj) + met(a.rarea, gi, gj) * (U(i, j) * met(a.dx, gi, gj) - U(i, j + 1) * met(a.dx, gi, gj + 1) +
-                                                       V(i + 1, j) * met(a.dy, gi + 1, gj) - V(i, j) * met(a.dy, gi, gj));
-  });
-  // d_sw_damp: Smagorinsky-scaled divergence damping at corners
-  fill(DDV, 0, TI + 1, 0, TJ + 1, [&](int i, int j) {
-    const int gi = gi0 + i, gj = gj0 + j;
-    const double rac = met(a.rarea_c, gi, gj);
-    const double ue = U(i, j) * met(a.dyc, gi, gj), uw = U(i - 1, j) * met(a.dyc, gi - 1, gj);
-    const double vn = V(i, j) * met(a.dxc, gi, gj), vs = V(i, j - 1) * met(a.dxc, gi, gj - 1);
-    const double divg = rac * (ue - uw + vn - vs);
-    const double tens = rac * (ue - uw - vn + vs);
-    const double smag = dt * sqrt(divg * divg + tens * tens);
-    const double dmp = a.da_min * np_max2(a.d2_bg, np_min(0.2, a.dddmp * smag));
-    return dmp * divg;
-  });
-  __syncthreads();
-  // ked = 0.5 * (ub * uu + vb * vv)   (into UB)
-  fill(UB, 0, TI + 1, 0, TJ + 1, [&](int i, int j) { return 0.5 * (UB(i, j) * UU(i, j) + VB(i, j) * VV(i, j)); });
-  __syncthreads();
-  // vorticity transport: fv_tp_2d(wk) -> fxv, fyv (area-flux weighted)
-  tp2d(a, WK, CRX, XFX, CRY, YFX, XFX, YFX, FY2, FX2, QI, QJ, FXV, FYV, gi0, gj0);
-  __syncthreads();
-  each(0, TI, 0, TJ, [&](int i, int j) {
-    const int gi = gi0 + i, gj = gj0 + j;
-    if (gi >= ni || gj >= nj) return;
-    const double rdx = met(a.rdx, gi, gj), rdy = met(a.rdy, gi, gj);
-    *a.uo.ptr(gi, gj, k) = (U(i, j) * met(a.dx, gi, gj) + UB(i, j) - UB(i + 1, j) + FYV(i, j)) * rdx +
-                           (DDV(i + 1, j) - DDV(i, j)) * rdx;
-    *a.vo.ptr(gi, gj, k) = (V(i, j) * met(a.dy, gi, gj) + UB(i, j) - UB(i, j + 1) - FXV(i, j)) * rdy +
-                           (DDV(i, j + 1) - DDV(i, j)) * rdy;
-  });
-}
 
 }  // namespace fv3b
 
@@ -206,7 +72,7 @@ extern "C" int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns, c
   {
     Geo g;
     FV3B_TRY(geo_of(f[0], &g));
-    const int tma_fields[] = {2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 19, 20, 21};
+    const int tma_fields[] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23, 24};
     for (int t : tma_fields) {
       Geo h;
       FV3B_TRY(geo_of(f[t], &h));
@@ -234,14 +100,22 @@ extern "C" int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns, c
     t.p1 = a.p1; t.p2 = a.p2; t.dt = a.dt; t.damp_w = a.damp_w;
     FV3B_TRY(launch_dsw_transport(t, st));
   }
-  static bool attr = false;
-  const size_t b2 = 16 * GD::NA * sizeof(double);
-  if (!attr) {
-    if (cudaFuncSetAttribute(d_sw_momentum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b2) != cudaSuccess)
-      return check_launch("d_sw smem attribute");
-    attr = true;
+  // momentum group (u, v): TMA-pipelined level march
+  DswMoArgs mo;
+  memset(&mo, 0, sizeof mo);
+  {
+    Geo g;
+    FV3B_TRY(geo_of(f[0], &g));
+    const fv3b_field mt[12] = {f[13], f[14], f[19], f[20], f[21], f[24], f[22], f[17], f[18], f[15], f[16], f[23]};
+    FV3B_TRY(dsw_momentum_maps(mo, g, f[0], f[1], f[5], f[6], mt));
+    mo.i0 = g.i0;
+    mo.j0 = g.j0;
   }
-  dim3 grid(cdiv(d->ni, GD::TI), cdiv(d->nj, GD::TJ), d->nk);
-  d_sw_momentum_kernel<<<grid, DSW_NT, b2, st>>>(a);
-  return check_launch("d_sw_momentum");
+  mo.uo = a.uo.o;
+  mo.vo = a.vo.o;
+  mo.sj = a.u.sj;
+  mo.sk = a.u.sk;
+  mo.ni = d->ni; mo.nj = d->nj; mo.nk = d->nk;
+  mo.p1 = a.p1; mo.p2 = a.p2; mo.dt = a.dt; mo.dddmp = a.dddmp; mo.d2_bg = a.d2_bg; mo.da_min = a.da_min;
+  return launch_dsw_momentum(mo, st);
 }

@@ -26,3 +26,23 @@ int dsw_transport_maps(DswTpArgs& a, const Geo& g, const fv3b_field* qbox5, cons
 int launch_dsw_transport(const DswTpArgs& a, cudaStream_t st);
 
 }  // namespace fv3b
+
+namespace fv3b {
+
+// d_sw momentum group: d_sw_courant + d_sw_ke + d_sw_vort + d_sw_damp and the
+// u / v statements of d_sw_update.
+struct DswMoArgs {
+  CUtensorMap u, v, uc, vc;  // u: q-box + 1 row; v, uc, vc: q-box
+  CUtensorMap met[12];       // dx (+1 row), dy, rdxa, rdya, area, f0, rarea, rdx, rdy, dxc, dyc, rarea_c
+  double* uo;
+  double* vo;
+  int64_t sj, sk;
+  int i0, j0, ni, nj, nk, kchunk;
+  double p1, p2, dt, dddmp, d2_bg, da_min;
+};
+
+int dsw_momentum_maps(DswMoArgs& a, const Geo& g, const fv3b_field& u, const fv3b_field& v, const fv3b_field& uc,
+                      const fv3b_field& vc, const fv3b_field* met12);
+int launch_dsw_momentum(const DswMoArgs& a, cudaStream_t st);
+
+}  // namespace fv3b
