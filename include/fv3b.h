@@ -147,6 +147,21 @@ int fv3b_halo_pack(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_halo_unpack(const fv3b_field* f, int nf, const double* s, int ns,
                      const fv3b_domain* d, void* stream);
 
+/*   fv3b_halo_pack_rects / fv3b_halo_unpack_rects  every edge and corner
+ *                       strip of one decomposed-domain halo update (up to 8
+ *                       rectangles, all levels, up to 32 fields sharing one
+ *                       level count) to / from one message buffer in one
+ *                       launch.  scalars: [buffer address as the bits of a
+ *                       double, nrect, then (i0, j0, w, h, element offset)
+ *                       per rectangle, interior-relative].  Rectangle r of
+ *                       field t, level k is at offset_r + (t*levels + k)*w*h,
+ *                       row-major.  Replaces the paper's Python halo updater
+ *                       pack/unpack. */
+int fv3b_halo_pack_rects(const fv3b_field* f, int nf, const double* s, int ns,
+                         const fv3b_domain* d, void* stream);
+int fv3b_halo_unpack_rects(const fv3b_field* f, int nf, const double* s, int ns,
+                           const fv3b_domain* d, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,6 +7,8 @@
 //    exchange of a decomposed domain (NCCL P2P moves the buffers).  A strip
 //    is a rectangle [i0, i0+w) x [j0, j0+h) x all levels of every field;
 //    buffer layout is field-major, then level, row, column.
+#include <string.h>
+
 #include "common.cuh"
 
 namespace fv3b {
@@ -20,16 +22,28 @@ struct HaloArgs {
   int nf, ni, nj, h;
 };
 
-// One thread per halo cell of a level: (i, j) enumerates the ring
-// [-h, n+h)^2 minus the interior; source = periodic wrap.
+// One thread per halo cell of a level: e enumerates the ring [-h, n+h)^2
+// minus the interior (the south and north bands of full width, then the west
+// and east bands of the interior rows); source = periodic wrap.
 __global__ void halo_periodic_kernel(const HaloArgs a) {
-  const int W = a.ni + 2 * a.h, H = a.nj + 2 * a.h;
+  const int W = a.ni + 2 * a.h, h = a.h;
   const int f = blockIdx.z, k = blockIdx.y;
   if (k >= a.levels[f]) return;
   double* o = a.o[f] + (int64_t)k * a.sk;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < W * H; e += gridDim.x * blockDim.x) {
-    const int i = e % W - a.h, j = e / W - a.h;
-    if (i >= 0 && i < a.ni && j >= 0 && j < a.nj) continue;
+  const int nband = W * h;           // one south / north band
+  const int nside = h * a.nj;        // one west / east band
+  const int n = 2 * nband + 2 * nside;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    int i, j;
+    if (e < 2 * nband) {
+      const int b = e / nband, r = e % nband;
+      i = r % W - h;
+      j = (b == 0 ? -h : a.nj) + r / W;
+    } else {
+      const int r0 = e - 2 * nband, b = r0 / nside, r = r0 % nside;
+      i = (b == 0 ? -h : a.ni) + r % h;
+      j = r / h;
+    }
     const int si = (i + a.ni) % a.ni, sj = (j + a.nj) % a.nj;
     o[i + (int64_t)j * a.sj] = o[si + (int64_t)sj * a.sj];
   }
@@ -84,6 +98,74 @@ static int collect(const fv3b_field* f, int nf, const fv3b_domain* d, int h, dou
   return FV3B_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Multi-rectangle pack / unpack: every edge / corner strip of a halo update
+// for a batch of fields in one launch (the decomposed-domain exchange,
+// parallel.DecomposedHalo).  Rectangle r of field t at level k lives at
+// buf[off_r + ((t * L) + k) * w_r * h_r + row * w_r + col], L = the fields'
+// level count (all fields of a call share it).
+// ---------------------------------------------------------------------------
+constexpr int RECT_MAX = 8;
+
+struct RectArgs {
+  double* o[HALO_MAXF];
+  int64_t sj, sk;
+  double* buf;
+  int i0[RECT_MAX], j0[RECT_MAX], w[RECT_MAX], h[RECT_MAX];
+  int64_t off[RECT_MAX];
+  int nrect, nf, levels;
+  bool unpack;
+};
+
+__global__ void rects_kernel(const RectArgs a) {
+  const int r = blockIdx.z % a.nrect, t = blockIdx.z / a.nrect, k = blockIdx.y;
+  const int w = a.w[r], n = w * a.h[r];
+  double* o = a.o[t] + (int64_t)k * a.sk;
+  double* b = a.buf + a.off[r] + ((int64_t)t * a.levels + k) * n;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    double* p = o + (a.i0[r] + e % w) + (int64_t)(a.j0[r] + e / w) * a.sj;
+    if (a.unpack)
+      *p = b[e];
+    else
+      b[e] = *p;
+  }
+}
+
+static int rects_call(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d, void* stream,
+                      bool unpack) {
+  // scalars: [buffer address bits, nrect, (i0, j0, w, h, offset) x nrect]
+  if (f == nullptr || d == nullptr || s == nullptr || ns < 2) return fail(FV3B_EINVAL, "halo rects: bad arguments");
+  RectArgs a;
+  uint64_t bits;
+  memcpy(&bits, &s[0], sizeof bits);
+  a.buf = reinterpret_cast<double*>(bits);
+  a.nrect = (int)s[1];
+  if (a.buf == nullptr || a.nrect < 1 || a.nrect > RECT_MAX || ns != 2 + 5 * a.nrect)
+    return fail(FV3B_EINVAL, "halo rects: 1..%d rectangles, 2 + 5*n scalars, non-null buffer", RECT_MAX);
+  int levels[HALO_MAXF];
+  FV3B_TRY(collect(f, nf, d, 0, a.o, levels, &a.sj, &a.sk));
+  for (int t = 1; t < nf; ++t)
+    if (levels[t] != levels[0]) return fail(FV3B_EINVAL, "halo rects: fields must share their level count");
+  a.levels = levels[0];
+  a.nf = nf;
+  a.unpack = unpack;
+  int maxn = 1;
+  for (int r = 0; r < a.nrect; ++r) {
+    const double* q = s + 2 + 5 * r;
+    a.i0[r] = (int)q[0];
+    a.j0[r] = (int)q[1];
+    a.w[r] = (int)q[2];
+    a.h[r] = (int)q[3];
+    a.off[r] = (int64_t)q[4];
+    if (a.w[r] <= 0 || a.h[r] <= 0) return fail(FV3B_EINVAL, "halo rects: empty rectangle %d", r);
+    maxn = a.w[r] * a.h[r] > maxn ? a.w[r] * a.h[r] : maxn;
+  }
+  dim3 grid(cdiv(maxn, 256) < 16 ? cdiv(maxn, 256) : 16, a.levels, a.nrect * nf);
+  rects_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch(unpack ? "fv3b_halo_unpack_rects" : "fv3b_halo_pack_rects");
+}
+
 }  // namespace fv3b
 
 using namespace fv3b;
@@ -102,7 +184,7 @@ extern "C" int fv3b_halo_periodic(const fv3b_field* f, int nf, const double* s, 
   a.nj = d->nj;
   int maxl = 1;
   for (int t = 0; t < nf; ++t) maxl = a.levels[t] > maxl ? a.levels[t] : maxl;
-  const int ring = (d->ni + 2 * a.h) * (d->nj + 2 * a.h);
+  const int ring = 2 * (d->ni + 2 * a.h) * a.h + 2 * a.h * d->nj;
   dim3 grid(cdiv(ring, 256) < 8 ? cdiv(ring, 256) : 8, maxl, nf);
   halo_periodic_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
   return check_launch("fv3b_halo_periodic");
@@ -145,4 +227,14 @@ extern "C" int fv3b_halo_pack(const fv3b_field* f, int nf, const double* s, int 
 extern "C" int fv3b_halo_unpack(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                                 void* stream) {
   return strip_call(f, nf, s, ns, d, stream, true);
+}
+
+extern "C" int fv3b_halo_pack_rects(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                    void* stream) {
+  return rects_call(f, nf, s, ns, d, stream, false);
+}
+
+extern "C" int fv3b_halo_unpack_rects(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                      void* stream) {
+  return rects_call(f, nf, s, ns, d, stream, true);
 }

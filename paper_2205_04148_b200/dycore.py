@@ -192,24 +192,32 @@ class Dycore:
             fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4")]
         self.launch("remap_tracers", "fv3b_remap_profile", fields, [], self.dom_ifaces)
 
-    def step(self) -> None:
-        """Enqueue one full timestep on the current stream."""
+    def phases(self):
+        """One timestep as a generator: enqueues the programs on the current
+        stream and yields, at each halo-update point, the fields to refresh
+        (the caller performs the update; a decomposed run exchanges them
+        between ranks, parallel.py)."""
         cfg = self.cfg
         for n in ACCUM:
             self.cur[n].zero_()
         self.cur["dp1"].copy_(self.cur["delp"])
         for _ in range(cfg.n_split):
-            self.halo.update(["u", "v", "w", "delp", "pt", "gz"])
+            yield ["u", "v", "w", "delp", "pt", "gz"]
             self.c_grid()
-            self.halo.update(["uc", "vc"])
+            yield ["uc", "vc"]
             self.d_sw()
             self.nh_d()
-            self.halo.update(["pef", "gz"])
+            yield ["pef", "gz"]
             self.p_grad_d()
-        self.halo.update(cfg.tracer_names() + list(ACCUM))
+        yield cfg.tracer_names() + list(ACCUM)
         self.tracer_2d()
         self.remap()
         self._parity ^= 1  # the tracers swap buffers once per step
+
+    def step(self) -> None:
+        """Enqueue one full timestep on the current stream."""
+        for names in self.phases():
+            self.halo.update(names)
 
     # -- CUDA graphs ---------------------------------------------------------
 

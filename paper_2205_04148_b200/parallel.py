@@ -1,0 +1,284 @@
+"""Decomposed doubly periodic domains: the halo update between ranks.
+
+The paper's dycore runs one horizontal block per GPU and refreshes halos with
+a Python halo updater that packs edge strips, exchanges them with
+non-blocking point-to-point messages and unpacks them (
+SURVEY 8e).  Here:
+
+* :class:`HaloPlan` — host logic only: the px x py block decomposition of a
+  doubly periodic domain (rank r owns block (r % px, r // px)), the eight
+  edge / corner strips each rank sends and receives, and the message layout
+  (one contiguous message per peer, strips in a fixed direction order) that
+  both sides derive independently.  Corners travel with the diagonal
+  neighbours, so one round of messages fills the whole halo ring, exactly the
+  values a single-domain periodic fill would write.
+* packers — move strips between the field tensors (device Layout,
+  ``device.Grid``) and message buffers: :class:`DevicePacker` runs the
+  ``fv3b_halo_pack_rects`` / ``fv3b_halo_unpack_rects`` CUDA kernels (one
+  launch per halo update for up to 32 fields); :class:`TorchPacker` does the
+  same with tensor slicing (CPU tests, the gloo path).
+* transports — :class:`DistTransport` posts one ``isend`` / ``irecv`` pair per
+  peer through ``torch.distributed.batch_isend_irecv`` (NCCL over NVLink on
+  the B200 box, gloo on CPU); messages to the rank itself (a periodic wrap
+  along an undecomposed axis) are device copies.
+* :class:`DecomposedHalo` — the halo object a :class:`~.dycore.Dycore` calls.
+* :class:`LoopbackCluster` — several ranks' dycores in one process on one
+  GPU, advanced in lockstep with device copies as the transport; it checks
+  the decomposed step against the single-domain step without a multi-GPU box.
+
+No region of the shipped programs fires on a doubly periodic block
+(placement all-False, ``lower.py:91-93``), so with correct halos every rank
+computes bitwise what the single domain computes on its cells.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+
+import torch
+
+DIRS = [(-1, -1), (0, -1), (1, -1), (-1, 0), (1, 0), (-1, 1), (0, 1), (1, 1)]  # (di, dj), message order
+MAX_FIELDS = 32
+
+
+@dataclass(frozen=True)
+class Rect:
+    """Interior-relative rectangle [i0, i0+w) x [j0, j0+h) (all levels)."""
+
+    i0: int
+    j0: int
+    w: int
+    h: int
+
+    @property
+    def cells(self) -> int:
+        return self.w * self.h
+
+
+def _span(d: int, n: int, h: int, send: bool) -> tuple[int, int]:
+    if d == 0:
+        return 0, n
+    if send:
+        return (0, h) if d < 0 else (n - h, h)
+    return (-h, h) if d < 0 else (n, h)
+
+
+class HaloPlan:
+    """Neighbour strips and message layout of one rank of a px x py
+    decomposition (uniform ni x nj blocks, halo width h)."""
+
+    def __init__(self, ni: int, nj: int, h: int, px: int, py: int, rank: int):
+        if not 0 <= rank < px * py:
+            raise ValueError(f"rank {rank} outside a {px}x{py} decomposition")
+        if h > ni or h > nj:
+            raise ValueError("halo wider than the block")
+        self.ni, self.nj, self.h, self.px, self.py, self.rank = ni, nj, h, px, py, rank
+        self.ri, self.rj = rank % px, rank // px
+        self.peer = [((self.ri + di) % px) + ((self.rj + dj) % py) * px for di, dj in DIRS]
+        self.send = []
+        self.recv = []
+        for di, dj in DIRS:
+            (si, wi), (sj, hj) = _span(di, ni, h, True), _span(dj, nj, h, True)
+            self.send.append(Rect(si, sj, wi, hj))
+            (ri, wi), (rj, hj) = _span(di, ni, h, False), _span(dj, nj, h, False)
+            self.recv.append(Rect(ri, rj, wi, hj))
+        self.peers = sorted(set(self.peer))
+        # send order: per peer (ascending), directions in DIRS order
+        self.send_order = [(p, [d for d in range(8) if self.peer[d] == p]) for p in self.peers]
+        # receive order: the sender lists its strips for me in its DIRS order;
+        # its direction is the negation of mine
+        neg = {d: DIRS.index((-DIRS[d][0], -DIRS[d][1])) for d in range(8)}
+        self.recv_order = [(p, sorted([e for e in range(8) if self.peer[e] == p], key=lambda e: neg[e]))
+                           for p in self.peers]
+
+    def layout(self, nfields: int, levels: int, recv: bool):
+        """[(peer, start, length, [(direction, rect, offset)])] in elements."""
+        out, off = [], 0
+        for p, dirs in (self.recv_order if recv else self.send_order):
+            start, items = off, []
+            for d in dirs:
+                r = (self.recv if recv else self.send)[d]
+                items.append((d, r, off))
+                off += r.cells * nfields * levels
+            out.append((p, start, off - start, items))
+        return out
+
+    def total(self, nfields: int, levels: int) -> int:
+        return sum(r.cells for r in self.send) * nfields * levels
+
+
+def grid_shape(world: int) -> tuple[int, int]:
+    """px x py of the weak-scaling decompositions (J split first)."""
+    return {1: (1, 1), 2: (1, 2), 4: (2, 2), 6: (2, 3), 8: (2, 4)}.get(world, (1, world))
+
+
+# ---------------------------------------------------------------------------
+# packers
+# ---------------------------------------------------------------------------
+
+class TorchPacker:
+    """Strip copies by tensor slicing (CPU tests; any device)."""
+
+    def __init__(self, grid):
+        self.grid = grid
+
+    def _view(self, t: torch.Tensor, r: Rect) -> torch.Tensor:
+        g = self.grid
+        return t[:, g.halo + r.j0 : g.halo + r.j0 + r.h, g.i0 + r.i0 : g.i0 + r.i0 + r.w]
+
+    def pack(self, tensors, rects, buf: torch.Tensor) -> None:
+        L = tensors[0].shape[0]
+        for r, off in rects:
+            n = r.cells
+            for t, x in enumerate(tensors):
+                buf[off + t * L * n : off + (t + 1) * L * n].view(L, r.h, r.w).copy_(self._view(x, r))
+
+    def unpack(self, tensors, rects, buf: torch.Tensor) -> None:
+        L = tensors[0].shape[0]
+        for r, off in rects:
+            n = r.cells
+            for t, x in enumerate(tensors):
+                self._view(x, r).copy_(buf[off + t * L * n : off + (t + 1) * L * n].view(L, r.h, r.w))
+
+
+class DevicePacker:
+    """``fv3b_halo_pack_rects`` / ``fv3b_halo_unpack_rects``: all strips of
+    a halo update for up to 32 fields in one launch each way."""
+
+    def __init__(self, grid, placement=(False, False, False, False)):
+        from . import _lib
+
+        self._lib = _lib
+        self.grid = grid
+        self.dom = grid.domain(placement)
+
+    def _call(self, entry, tensors, rects, buf):
+        bits = struct.unpack("d", struct.pack("Q", buf.data_ptr()))[0]
+        s = [bits, float(len(rects))]
+        for r, off in rects:
+            s += [float(r.i0), float(r.j0), float(r.w), float(r.h), float(off)]
+        fields = [self.grid.abi(t) for t in tensors]
+        self._lib.call(entry, fields, s, self.dom, torch.cuda.current_stream().cuda_stream)
+
+    def pack(self, tensors, rects, buf):
+        self._call("fv3b_halo_pack_rects", tensors, rects, buf)
+
+    def unpack(self, tensors, rects, buf):
+        self._call("fv3b_halo_unpack_rects", tensors, rects, buf)
+
+
+# ---------------------------------------------------------------------------
+# transports
+# ---------------------------------------------------------------------------
+
+class DistTransport:
+    """One message per peer through torch.distributed P2P (grouped
+    ncclSend/ncclRecv on NCCL); self messages are copies."""
+
+    def __init__(self, rank: int, group=None):
+        self.rank = rank
+        self.group = group
+
+    def exchange(self, send: list, recv: list) -> None:
+        """send / recv: [(peer, tensor)] in the plan's peer order."""
+        import torch.distributed as dist
+
+        ops = []
+        rbuf = dict(recv)
+        for p, t in send:
+            if p == self.rank:
+                rbuf[p].copy_(t)
+            else:
+                ops.append(dist.P2POp(dist.isend, t, p, self.group))
+                ops.append(dist.P2POp(dist.irecv, rbuf[p], p, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+
+# ---------------------------------------------------------------------------
+# the halo object of a decomposed dycore
+# ---------------------------------------------------------------------------
+
+class DecomposedHalo:
+    """Halo update of one rank; ``update(names)`` refreshes the I/J halos of
+    the named state fields of ``dycore`` (a :class:`~.dycore.Dycore`)."""
+
+    def __init__(self, dycore, px: int, py: int, rank: int, transport=None, packer=None):
+        self.d = dycore
+        g = dycore.grid
+        self.plan = HaloPlan(g.ni, g.nj, g.halo, px, py, rank)
+        self.transport = transport or DistTransport(rank)
+        self.packer = packer or (DevicePacker(g) if dycore.device != "cpu" else TorchPacker(g))
+        self._bufs: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
+
+    def _buffers(self, nf: int, levels: int, device) -> tuple[torch.Tensor, torch.Tensor]:
+        if nf not in self._bufs:
+            n = self.plan.total(nf, levels)
+            self._bufs[nf] = (torch.empty(n, dtype=torch.float64, device=device),
+                              torch.empty(n, dtype=torch.float64, device=device))
+        return self._bufs[nf]
+
+    def pack(self, names) -> list:
+        """Pack every chunk of <= 32 fields; returns per-chunk state for
+        :meth:`finish` (send / recv slices per peer)."""
+        chunks = []
+        for c in range(0, len(names), MAX_FIELDS):
+            tensors = [self.d.cur[n] for n in names[c : c + MAX_FIELDS]]
+            L = tensors[0].shape[0]
+            sbuf, rbuf = self._buffers(len(tensors), L, tensors[0].device)
+            slay = self.plan.layout(len(tensors), L, recv=False)
+            rlay = self.plan.layout(len(tensors), L, recv=True)
+            self.packer.pack(tensors, [(r, off) for _, _, _, items in slay for _, r, off in items], sbuf)
+            send = [(p, sbuf[s : s + n]) for p, s, n, _ in slay]
+            recv = [(p, rbuf[s : s + n]) for p, s, n, _ in rlay]
+            chunks.append((tensors, rlay, rbuf, send, recv))
+        return chunks
+
+    def finish(self, chunks) -> None:
+        for tensors, rlay, rbuf, _, _ in chunks:
+            self.packer.unpack(tensors, [(r, off) for _, _, _, items in rlay for _, r, off in items], rbuf)
+
+    def update(self, names) -> None:
+        timer = getattr(self.d, "timer", None)
+        if timer is not None:
+            timer.start("halo")
+        chunks = self.pack(list(names))
+        for _, _, _, send, recv in chunks:
+            self.transport.exchange(send, recv)
+        self.finish(chunks)
+        if timer is not None:
+            timer.stop("halo")
+
+
+class LoopbackCluster:
+    """px x py ranks' dycores in one process, stepped in lockstep; messages
+    are device copies between the ranks' buffers (tests / single-GPU
+    validation of the decomposed path)."""
+
+    def __init__(self, dycores, px: int, py: int):
+        self.d = dycores
+        self.halos = [DecomposedHalo(d, px, py, r, transport=self, packer=None) for r, d in enumerate(dycores)]
+        for d, h in zip(dycores, self.halos):
+            d.halo = h
+
+    def exchange(self, send, recv):  # transports run inside step(); see below
+        raise RuntimeError("LoopbackCluster exchanges all ranks at once (use step())")
+
+    def step(self) -> None:
+        gens = [d.phases() for d in self.d]
+        while True:
+            reqs = [next(g, None) for g in gens]
+            if all(r is None for r in reqs):
+                return
+            assert all(r is not None for r in reqs), "ranks out of lockstep"
+            chunks = [h.pack(names) for h, names in zip(self.halos, reqs)]
+            for r, ch in enumerate(chunks):
+                for c, (_, _, _, _, recv) in enumerate(ch):
+                    for p, rt in recv:
+                        # peer p's message to r
+                        sent = dict(chunks[p][c][3])[r]
+                        rt.copy_(sent)
+            for h, ch in zip(self.halos, chunks):
+                h.finish(ch)
