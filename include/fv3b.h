@@ -88,8 +88,9 @@ int fv3b_tracer_2d(const fv3b_field* f, int nf, const double* s, int ns,
 
 /* K4  riem_solver_c.stn — semi-implicit vertical acoustic solve per column.
  *     Program domain nk = interface levels (layers + 1).  fields: dm, pt, w
- *     (layers), gz (interfaces), ws (2-D), pef, gz_out (interfaces; gz_out
- *     may alias gz).  scalars: ptop, rdgas, grav, gama, p_fac, dt. */
+ *     (layers), gz (interfaces), ws (2-D), pef, gz_out (interfaces; the
+ *     outputs stage column intermediates and must not alias the inputs).
+ *     scalars: ptop, rdgas, grav, gama, p_fac, dt. */
 int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, int ns,
                        const fv3b_domain* d, void* stream);
 
@@ -123,7 +124,8 @@ int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns,
 
 /* nh_d.stn — D-grid vertical solve (riem_solver3 role), program domain
  *     nk = layers + 1.  fields: delp, pt, w, gz (3-D), ws (2-D), pef,
- *     gz_out, w_out (3-D).  scalars: ptop, rdgas, grav, gama, p_fac, dt. */
+ *     gz_out, w_out (3-D; outputs must not alias inputs).  scalars: ptop,
+ *     rdgas, grav, gama, p_fac, dt. */
 int fv3b_nh_d(const fv3b_field* f, int nf, const double* s, int ns,
               const fv3b_domain* d, void* stream);
 

@@ -346,7 +346,9 @@ extern "C" int fv3b_nh_d(const fv3b_field* f, int nf, const double* s, int ns, c
   FV3B_TRY(view_of(f[5], 3, *d, H0, "pef", &r.pef));
   FV3B_TRY(view_of(f[6], 3, *d, H0, "gz_out", &r.gzo));
   FV3B_TRY(view_of(f[7], 3, *d, H0, "w_out", &r.wout));
-  if (f[7].data == f[2].data) return fail(FV3B_EINVAL, "fv3b_nh_d: w_out must not alias w");
+  for (int t = 5; t < 8; ++t)
+    for (int u = 0; u < 4; ++u)
+      if (f[t].data == f[u].data) return fail(FV3B_EINVAL, "fv3b_nh_d: output %d aliases input %d", t, u);
   r.has_wout = true;
   r.ilo = 0; r.jlo = 0; r.ni_ext = d->ni; r.nj_ext = d->nj;
   r.nk = d->nk - 1;

@@ -67,39 +67,49 @@ constexpr int PF = 4;  // prefetch distance (levels)
 // Statement-for-statement restatement of templates.riem_stencils for one
 // column.  FAST: branch-free divisions/logs (fastdiv.cuh), returns false if
 // any of them left nvcc's fast-path range, in which case the caller
-// re-evaluates the column with EXACT.  In FAST mode the gz output is staged
-// in S2 and only written by the caller (gz may alias gz_out).
+// re-evaluates the column with EXACT.
+//
+// Shared memory holds two level arrays per column (S0, S1); the third value
+// the sweeps carry between passes lives in the column's own output slots,
+// which are rewritten with their final values later in the kernel:
+//   pef  holds pem (riem_pem) from pass A until pass E writes pe2 + pem;
+//   gzo  holds pmc (riem_layer) from pass A until pass F, which reads it
+//        instead of re-evaluating dm / log(pem[k+1] / pem[k]) (the same
+//        IEEE operations on the same operands, so the same bits).
+// gz_out must therefore not alias gz.
 template <bool FAST>
 __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int c, int NC, double* sm) {
   ColArith<FAST> ar;
   const int nk = a.nk, L = nk + 1;
-  double* S0 = sm + c;               // pp, later pe2
-  double* S1 = sm + L * NC + c;      // gam -> aa -> gw -> pem
-  double* S2 = sm + 2 * L * NC + c;  // pem -> w2 -> (FAST) gz
+  double* S0 = sm + c;           // pp -> w2 -> pe2 (shifted one level down)
+  double* S1 = sm + L * NC + c;  // gam -> aa -> gw -> pem
 #define AT(S, k) (S)[(k) * NC]
   const double dt = a.dt, ptop = a.ptop, rdgas = a.rdgas, grav = a.grav, gama = a.gama;
   const double* __restrict__ dm = a.dm.ptr(i, j, 0);
   const double* __restrict__ pt = a.pt.ptr(i, j, 0);
   const double* __restrict__ w = a.w.ptr(i, j, 0);
-  const double* gz = a.gz.ptr(i, j, 0);  // may alias gzo (read before pass F writes)
-  const int64_t sk = a.dm.sk;
+  const double* __restrict__ gz = a.gz.ptr(i, j, 0);
+  double* pf = a.pef.ptr(i, j, 0);
+  double* go = a.gzo.ptr(i, j, 0);
+  const int64_t sk = a.dm.sk, sp = a.pef.sk, sg = a.gzo.sk;
 
   // ---- pass A (forward): riem_pem, riem_layer, riem_coef, riem_pp_fwd ----
   {
     double pem0 = ptop;  // pem(k)
-    AT(S2, 0) = pem0;
+    pf[0] = pem0;
     double pe_prev = 0.0, grat_prev = 0.0, bet_prev = 0.0, pp_prev = 0.0;
-    double dm_k = __ldg(dm), gzk = gz[0];
+    double dm_k = __ldg(dm), gzk = __ldg(gz);
     pipelined<PF, D3>(
         nk,
         [&](int k) {  // dm(k+1), gz(k+1), pt(k)
-          return D3{(k + 1 < nk) ? __ldg(dm + (k + 1) * sk) : 0.0, gz[(k + 1) * sk], __ldg(pt + k * sk)};
+          return D3{(k + 1 < nk) ? __ldg(dm + (k + 1) * sk) : 0.0, __ldg(gz + (k + 1) * sk), __ldg(pt + k * sk)};
         },
         [&](int k, const D3& v) {
           const double dm_n = v.x, gzk1 = v.y;
           const double pem1 = pem0 + dm_k;  // pem(k+1) = pem + dm
-          AT(S2, k + 1) = pem1;
+          pf[(k + 1) * sp] = pem1;
           const double pmk = ar.div(dm_k, ar.log(ar.div(pem1, pem0)));
+          go[k * sg] = pmk;
           const double pek = ar.div(dm_k * rdgas * v.z, gzk - gzk1) - pmk;
           // layer k coefficients (riem_coef)
           const double grat = (k < nk - 1) ? ar.div(dm_k, dm_n) : 0.0;
@@ -133,24 +143,24 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   const double t1g = gama * 2.0 * dt * dt;
   {
     double ppn = AT(S0, nk);
-    double gzn = gz[(nk - 1) * sk];
-    double dz_n = ar.div(gz[nk * sk] - gzn, grav);          // dz(nk-1)
-    AT(S1, nk) = ar.div(t1g, dz_n) * (AT(S2, nk) + ppn);     // aa(nk)
-    pipelined<PF, D1>(
-        nk - 1, [&](int s) { return D1{gz[(nk - 2 - s) * sk]}; },  // k = nk-1-s: gz(k-1)
-        [&](int s, const D1& v) {
+    double gzn = __ldg(gz + (nk - 1) * sk);
+    double dz_n = ar.div(__ldg(gz + nk * sk) - gzn, grav);  // dz(nk-1)
+    AT(S1, nk) = ar.div(t1g, dz_n) * (pf[nk * sp] + ppn);   // aa(nk)
+    pipelined<PF, D2>(
+        nk - 1, [&](int s) { return D2{__ldg(gz + (nk - 2 - s) * sk), pf[(nk - 1 - s) * sp]}; },  // gz(k-1), pem(k)
+        [&](int s, const D2& v) {
           const int k = nk - 1 - s;
           const double ppk = AT(S0, k) - AT(S1, k) * ppn;
           AT(S0, k) = ppk;
-          const double dz_k = ar.div(gzn - v.x, grav);                   // dz(k-1)
-          AT(S1, k) = ar.div(t1g, dz_k + dz_n) * (AT(S2, k) + ppk);     // aa(k) = t1g/(dz(k-1)+dz(k))*(pem+pp)
+          const double dz_k = ar.div(gzn - v.x, grav);               // dz(k-1)
+          AT(S1, k) = ar.div(t1g, dz_k + dz_n) * (v.y + ppk);       // aa(k) = t1g/(dz(k-1)+dz(k))*(pem+pp)
           dz_n = dz_k;
           ppn = ppk;
           gzn = v.x;
         });
   }
 
-  // ---- pass C (forward): riem_w_sweep ----------------------------------
+  // ---- pass C (forward): riem_w_sweep (w2 replaces pp level by level) ----
   const double ws = a.ws(i, j, 0);
   {
     double bw = 0.0, w2p = 0.0;
@@ -172,20 +182,20 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
               w2l = ar.div(dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aan * ws - aal * w2p, bw);
             AT(S1, l) = gw;  // aa(l) no longer needed
           }
-          AT(S2, l) = w2l;
+          AT(S0, l) = w2l;  // pp(l) no longer needed
           w2p = w2l;
         });
   }
 
   // ---- pass D (backward): riem_w_back ----------------------------------
   {
-    double w2n = AT(S2, nk - 1);
+    double w2n = AT(S0, nk - 1);
     double* wo = a.has_wout ? a.wout.ptr(i, j, 0) : nullptr;
     const int64_t so = a.wout.sk;
     if (wo) wo[(nk - 1) * so] = w2n;
     for (int l = nk - 2; l >= 0; --l) {
-      const double w2l = AT(S2, l) - AT(S1, l + 1) * w2n;
-      AT(S2, l) = w2l;
+      const double w2l = AT(S0, l) - AT(S1, l + 1) * w2n;
+      AT(S0, l) = w2l;
       if (wo) wo[l * so] = w2l;
       w2n = w2l;
     }
@@ -194,37 +204,36 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   // ---- pass E (forward): riem_pe, riem_out (pem recomputed in order) -----
   {
     double pe2 = 0.0, pem = ptop;
-    double* pf = a.pef.ptr(i, j, 0);
-    const int64_t so = a.pef.sk;
-    AT(S0, 0) = 0.0;
     AT(S1, 0) = ptop;
     pf[0] = pe2 + pem;
     pipelined<PF, D2>(
         nk, [&](int s) { return D2{__ldg(dm + s * sk), __ldg(w + s * sk)}; },  // k = s+1: layer k-1
         [&](int s, const D2& v) {
           const int k = s + 1;
-          pe2 = pe2 + ar.div(v.x * (AT(S2, k - 1) - v.y), dt);
+          pe2 = pe2 + ar.div(v.x * (AT(S0, k - 1) - v.y), dt);
           pem = pem + v.x;
-          AT(S0, k) = pe2;
+          AT(S0, k - 1) = pe2;  // pe2(k) (w2(k-1) consumed)
           AT(S1, k) = pem;
-          pf[k * so] = pe2 + pem;
+          pf[k * sp] = pe2 + pem;
         });
   }
 
-  // ---- pass F (backward): riem_gz ---------------------------------------
+  // ---- pass F (backward): riem_gz (pmc from pass A, in gz_out) ------------
   {
-    double* go = a.gzo.ptr(i, j, 0);
-    const int64_t so = a.gzo.sk;
-    double gzn = gz[nk * sk];
-    if (FAST) AT(S2, nk) = gzn; else go[nk * so] = gzn;
-    pipelined<PF, D2>(
-        nk, [&](int s) { return D2{__ldg(dm + (nk - 1 - s) * sk), __ldg(pt + (nk - 1 - s) * sk)}; },
-        [&](int s, const D2& v) {
+    double gzn = __ldg(gz + nk * sk);
+    go[nk * sg] = gzn;
+    pipelined<PF, D3>(
+        nk,
+        [&](int s) {
           const int l = nk - 1 - s;
-          const double dml = v.x;
-          const double pm = ar.div(dml, ar.log(ar.div(AT(S1, l + 1), AT(S1, l))));
-          const double g = gzn + ar.div(dml * rdgas * v.y, np_max(a.p_fac * pm, pm + 0.5 * (AT(S0, l) + AT(S0, l + 1))));
-          if (FAST) AT(S2, l) = g; else go[l * so] = g;
+          return D3{__ldg(dm + l * sk), __ldg(pt + l * sk), go[l * sg]};
+        },
+        [&](int s, const D3& v) {
+          const int l = nk - 1 - s;
+          const double dml = v.x, pm = v.z;
+          const double pe2l = l > 0 ? AT(S0, l - 1) : 0.0, pe2n = AT(S0, l);
+          const double g = gzn + ar.div(dml * rdgas * v.y, np_max(a.p_fac * pm, pm + 0.5 * (pe2l + pe2n)));
+          go[l * sg] = g;
           gzn = g;
         });
   }
@@ -239,14 +248,8 @@ __global__ void __launch_bounds__(NC_MAX) riem_kernel(const RiemArgs a) {
   if (cidx >= a.ni_ext * a.nj_ext) return;
   const int i = a.ilo + cidx % a.ni_ext;
   const int j = a.jlo + cidx / a.ni_ext;
-  if (riem_column<true>(a, i, j, c, NC, sm)) {
-    const int nk = a.nk, L = nk + 1;
-    const double* S2 = sm + 2 * L * NC + c;
-    double* go = a.gzo.ptr(i, j, 0);
-    for (int l = 0; l <= nk; ++l) go[l * a.gzo.sk] = S2[l * NC];
-  } else {
-    riem_column<false>(a, i, j, c, NC, sm);
-  }
+  // outputs never alias inputs: a failed fast evaluation is simply redone
+  if (!riem_column<true>(a, i, j, c, NC, sm)) riem_column<false>(a, i, j, c, NC, sm);
 }
 
 // ---------------------------------------------------------------------------
@@ -385,7 +388,7 @@ static int cols_per_cta(size_t bytes_per_col) {
 }
 
 int launch_riem(const RiemArgs& a, cudaStream_t st) {
-  const size_t per_col = 3 * (size_t)(a.nk + 1) * sizeof(double);
+  const size_t per_col = 2 * (size_t)(a.nk + 1) * sizeof(double);
   const int nc = cols_per_cta(per_col);
   const size_t bytes = per_col * nc;
   FV3B_TRY(set_smem((const void*)riem_kernel, bytes));
@@ -399,7 +402,7 @@ int launch_riem(const RiemArgs& a, cudaStream_t st) {
 using namespace fv3b;
 
 // fields: dm, pt, w (layers), gz (interfaces), ws (2-D), pef, gz_out
-// (interfaces; gz_out may alias gz).  scalars: ptop, rdgas, grav, gama,
+// (interfaces; must not alias the inputs: gz_out and pef stage intermediates).  scalars: ptop, rdgas, grav, gama,
 // p_fac, dt.  Domain nk = interface levels (program domain, nk_layers + 1).
 extern "C" int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                                   void* stream) {
@@ -415,6 +418,9 @@ extern "C" int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, 
   FV3B_TRY(view_of(f[4], 2, *d, h0, "ws", &a.ws));
   FV3B_TRY(view_of(f[5], 3, *d, h0, "pef", &a.pef));
   FV3B_TRY(view_of(f[6], 3, *d, h0, "gz_out", &a.gzo));
+  for (int t = 5; t < 7; ++t)
+    for (int u = 0; u < 4; ++u)
+      if (f[t].data == f[u].data) return fail(FV3B_EINVAL, "fv3b_riem_solver_c: output %d aliases input %d", t, u);
   if (a.dm.sk != a.pt.sk || a.dm.sk != a.w.sk || a.dm.sk != a.gz.sk)
     return fail(FV3B_ELAYOUT, "fv3b_riem_solver_c: input K strides differ");
   a.has_wout = false;

@@ -54,7 +54,7 @@ class Dycore:
         names3 = STATE_3D + cfg.tracer_names() + [f"q{t}_{a}" for t in range(cfg.nq) for a in ("a2", "a3", "a4")]
         self.cur: dict[str, torch.Tensor] = {n: g.new3(device) for n in names3}
         self.cur.update({n: g.new2(device) for n in METRICS_2D})
-        self.alt: dict[str, torch.Tensor] = {n: g.new3(device) for n in list(PINGPONG) + cfg.tracer_names()}
+        self.alt: dict[str, torch.Tensor] = {n: g.new3(device) for n in list(PINGPONG) + ["gz"] + cfg.tracer_names()}
         self.scratch = {n: g.new3(device) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc")}
         self.halo = halo or PeriodicHalo(self)
         self.stream = None
@@ -168,10 +168,10 @@ class Dycore:
 
     def nh_d(self) -> None:
         c, dt = self.cfg.consts, self.cfg.dt_acoustic
-        fields = [self.f(n) for n in ("delp", "pt", "w", "gz", "ws")] + [self.f("pef"), self.f("gz"), self.a("w")]
+        fields = [self.f(n) for n in ("delp", "pt", "w", "gz", "ws")] + [self.f("pef"), self.a("gz"), self.a("w")]
         self.launch("nh_d", "fv3b_nh_d", fields, [c["ptop"], c["rdgas"], c["grav"], c["gama"], c["p_fac"], dt],
                     self.dom_ifaces)
-        self.swap("w")
+        self.swap("w", "gz")
 
     def p_grad_d(self) -> None:
         fields = [self.f(n) for n in ("u", "v", "pef", "gz", "rdx", "rdy")] + [self.a("u"), self.a("v")]
