@@ -2,21 +2,18 @@
 // (programs/c_grid.stn = c_sw + riem_solver_c + p_grad_c), plus the D-grid
 // nonhydrostatic pair (nh_d.stn, p_grad_d.stn).  templates.c_sw_stencils.
 //
-// c_sw kernel: one CTA = 32 x 16 columns of one level.  u, v, delp, pt, w
-// are staged with their halos; ua/va -> uct/vct -> ke/vort are shared-memory
-// temporaries computed over the rectangles the later statements read; the
-// transport (transportdelp) fluxes are evaluated per output cell.  In the
-// fused C-grid program the C-grid thickness / temperature / w are written
-// over the one-cell extension (-1) that p_grad_c needs, so the column solver
-// runs on the extended domain and no halo exchange separates the stages.
+// c_sw runs as the TMA level-march kernel of csw_tma.cu.  In the fused
+// C-grid program the C-grid thickness / temperature / w are written over the
+// one-cell extension (-1) that p_grad_c needs, so the column solver runs on
+// the extended domain and no halo exchange separates the stages.
+#include <string.h>
+
 #include "column.cuh"
+#include "csw.cuh"
 #include "tile.cuh"
 
 namespace fv3b {
 
-using GC = TileGeo<32, 16, 4, 4>;
-constexpr int CSW_NT = 256;
-constexpr int CSW_NARR = 11;
 
 struct CswArgs {
   View u, v, delp, pt, w;
@@ -26,108 +23,6 @@ struct CswArgs {
   bool own_is, own_ie, own_js, own_je;
   double dt2, a1, a2;
 };
-
-template <bool EXT>
-__global__ void __launch_bounds__(CSW_NT, 2) c_sw_kernel(const CswArgs a) {
-  extern __shared__ __align__(128) double smem[];
-  using G = GC;
-  constexpr int TI = G::TI, TJ = G::TJ;
-  const Arr<G> U{smem + 0 * G::NA}, V{smem + 1 * G::NA}, DP{smem + 2 * G::NA}, PT{smem + 3 * G::NA},
-      WW{smem + 4 * G::NA}, UA{smem + 5 * G::NA}, VA{smem + 6 * G::NA}, UCT{smem + 7 * G::NA},
-      VCT{smem + 8 * G::NA}, KE{smem + 9 * G::NA}, VO{smem + 10 * G::NA};
-  const int gi0 = blockIdx.x * TI, gj0 = blockIdx.y * TJ, k = blockIdx.z;
-  const int ni = a.ni, nj = a.nj;
-  const double dt2 = a.dt2, a1 = a.a1, a2 = a.a2;
-
-  load(U, a.u, gi0, gj0, k, -3, TI + 2, -2, TJ + 3, ni, nj, a.hx, a.hy);
-  load(V, a.v, gi0, gj0, k, -2, TI + 3, -3, TJ + 2, ni, nj, a.hx, a.hy);
-  load(DP, a.delp, gi0, gj0, k, -2, TI + 1, -2, TJ + 1, ni, nj, a.hx, a.hy);
-  load(PT, a.pt, gi0, gj0, k, -2, TI + 1, -2, TJ + 1, ni, nj, a.hx, a.hy);
-  load(WW, a.w, gi0, gj0, k, -2, TI + 1, -2, TJ + 1, ni, nj, a.hx, a.hy);
-  __syncthreads();
-  // c_sw_winds: d2a2c (orthogonal)
-  fill(UA, -3, TI + 2, -1, TJ + 1, [&](int i, int j) {
-    return a2 * (U(i, j - 1) + U(i, j + 2)) + a1 * (U(i, j) + U(i, j + 1));
-  });
-  fill(VA, -1, TI + 1, -3, TJ + 2, [&](int i, int j) {
-    return a2 * (V(i - 1, j) + V(i + 2, j)) + a1 * (V(i, j) + V(i + 1, j));
-  });
-  __syncthreads();
-  fill(UCT, -1, TI + 1, -1, TJ + 1, [&](int i, int j) {
-    return a2 * (UA(i - 2, j) + UA(i + 1, j)) + a1 * (UA(i - 1, j) + UA(i, j));
-  });
-  fill(VCT, -1, TI + 1, -1, TJ + 1, [&](int i, int j) {
-    return a2 * (VA(i, j - 2) + VA(i, j + 1)) + a1 * (VA(i, j - 1) + VA(i, j));
-  });
-  __syncthreads();
-  // c_sw_ke_vort
-  fill(KE, -1, TI, -1, TJ, [&](int i, int j) {
-    const double keu = UA(i, j) > 0.0 ? UCT(i, j) : UCT(i + 1, j);
-    const double kev = VA(i, j) > 0.0 ? VCT(i, j) : VCT(i, j + 1);
-    return 0.5 * dt2 * (UA(i, j) * keu + VA(i, j) * kev);
-  });
-  fill(VO, 0, TI + 1, 0, TJ + 1, [&](int i, int j) {
-    const int gi = gi0 + i, gj = gj0 + j;
-    const double fc = met(a.fc, gi, gj), rac = met(a.rarea_c, gi, gj);
-    const double ts = UCT(i, j - 1) * met(a.dxc, gi, gj - 1);  // south
-    const double tn = UCT(i, j) * met(a.dxc, gi, gj);          // north
-    const double te = VCT(i, j) * met(a.dyc, gi, gj);          // east
-    const double tw = VCT(i - 1, j) * met(a.dyc, gi - 1, gj);  // west
-    double v = fc + rac * (ts - tn + te - tw);
-    // tile-corner regions (fire only on owned edges, lower.py:91-93)
-    if (gi == 0 && gj == 0 && a.own_is && a.own_js) v = fc + rac * (te - tn - tw);
-    if (gi == ni && gj == 0 && a.own_ie && a.own_js) v = fc + rac * (ts - tn - tw);
-    if (gi == ni && gj == nj && a.own_ie && a.own_je) v = fc + rac * (ts + te - tw);
-    if (gi == 0 && gj == nj && a.own_is && a.own_je) v = fc + rac * (ts - tn + te);
-    return v;
-  });
-  // c_sw_transport (transportdelp), fluxes evaluated per output cell
-  {
-    // the first tile row/column also owns the -1 extension (EXT)
-    const int loi = (EXT && gi0 == 0) ? -1 : 0, loj = (EXT && gj0 == 0) ? -1 : 0;
-    each(loi, TI, loj, TJ, [&](int i, int j) {
-      const int gi = gi0 + i, gj = gj0 + j;
-      if (gi >= ni || gj >= nj) return;
-      auto xf = [&](int ii, double& f, double& fp, double& fw) {
-        const double utc = dt2 * UCT(ii, j) * met(a.dy, gi0 + ii, gj);
-        const bool up = utc > 0.0;
-        f = utc * (up ? DP(ii - 1, j) : DP(ii, j));
-        fp = f * (up ? PT(ii - 1, j) : PT(ii, j));
-        fw = f * (up ? WW(ii - 1, j) : WW(ii, j));
-      };
-      auto yf = [&](int jj, double& f, double& fp, double& fw) {
-        const double vtc = dt2 * VCT(i, jj) * met(a.dx, gi, gj0 + jj);
-        const bool up = vtc > 0.0;
-        f = vtc * (up ? DP(i, jj - 1) : DP(i, jj));
-        fp = f * (up ? PT(i, jj - 1) : PT(i, jj));
-        fw = f * (up ? WW(i, jj - 1) : WW(i, jj));
-      };
-      double fx0, fxp0, fxw0, fx1, fxp1, fxw1, fy0, fyp0, fyw0, fy1, fyp1, fyw1;
-      xf(i, fx0, fxp0, fxw0);
-      xf(i + 1, fx1, fxp1, fxw1);
-      yf(j, fy0, fyp0, fyw0);
-      yf(j + 1, fy1, fyp1, fyw1);
-      const double ra = met(a.rarea, gi, gj);
-      const double dp = DP(i, j);
-      const double dpc = dp + (fx0 - fx1 + fy0 - fy1) * ra;
-      *a.delpc.ptr(gi, gj, k) = dpc;
-      *a.ptc.ptr(gi, gj, k) = (PT(i, j) * dp + (fxp0 - fxp1 + fyp0 - fyp1) * ra) / dpc;
-      *a.wc.ptr(gi, gj, k) = (WW(i, j) * dp + (fxw0 - fxw1 + fyw0 - fyw1) * ra) / dpc;
-    });
-  }
-  __syncthreads();
-  // c_sw_update
-  each(0, TI, 0, TJ, [&](int i, int j) {
-    const int gi = gi0 + i, gj = gj0 + j;
-    if (gi >= ni || gj >= nj) return;
-    const double fy1c = dt2 * V(i, j);
-    *a.uc.ptr(gi, gj, k) = UCT(i, j) + fy1c * (fy1c > 0.0 ? VO(i, j) : VO(i, j + 1)) +
-                           met(a.rdxc, gi, gj) * (KE(i - 1, j) - KE(i, j));
-    const double fx1c = dt2 * U(i, j);
-    *a.vc.ptr(gi, gj, k) = VCT(i, j) - fx1c * (fx1c > 0.0 ? VO(i, j) : VO(i + 1, j)) +
-                           met(a.rdyc, gi, gj) * (KE(i, j - 1) - KE(i, j));
-  });
-}
 
 // p_grad_c (c_grid.stn, nk+1 domain): uc/vc += C-grid pressure gradient from
 // the solver's interface pressure pkc and geopotential gzc (extended by one
@@ -195,18 +90,29 @@ __global__ void p_grad_d_kernel(const PgdArgs a) {
   }
 }
 
-template <bool EXT>
-static int launch_c_sw(const CswArgs& a, cudaStream_t st) {
-  const size_t bytes = CSW_NARR * GC::NA * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(c_sw_kernel<EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
-      return check_launch("c_sw smem attribute");
-    attr = true;
+// c_sw through the TMA level-march kernel (csw_tma.cu).  in5: u, v, delp,
+// pt, w; met9: dx, dy, dxc, dyc, rdxc, rdyc, rarea, rarea_c, fc.
+static int run_csw(const fv3b_field* in5, const fv3b_field* met9, const CswArgs& a, bool ext, cudaStream_t st) {
+  Geo g;
+  FV3B_TRY(geo_of(in5[0], &g));
+  for (int t = 0; t < 14; ++t) {
+    Geo h;
+    const fv3b_field& f = t < 5 ? in5[t] : met9[t - 5];
+    FV3B_TRY(geo_of(f, &h));
+    if (h.pitch != g.pitch || h.rows != g.rows || (f.rank == 3 && h.levels != g.levels) || h.i0 != g.i0 ||
+        h.j0 != g.j0)
+      return fail(FV3B_ELAYOUT, "c_sw: field %d geometry differs from u", t);
   }
-  dim3 grid(cdiv(a.ni, GC::TI), cdiv(a.nj, GC::TJ), a.nk);
-  c_sw_kernel<EXT><<<grid, CSW_NT, bytes, st>>>(a);
-  return check_launch("c_sw");
+  CswTmaArgs t;
+  memset(&t, 0, sizeof t);
+  FV3B_TRY(csw_maps(t, g, in5, met9));
+  t.uc = a.uc.o; t.vc = a.vc.o; t.delpc = a.delpc.o; t.ptc = a.ptc.o; t.wc = a.wc.o;
+  t.sj = a.u.sj; t.sk = a.u.sk;
+  t.i0 = g.i0; t.j0 = g.j0;
+  t.ni = a.ni; t.nj = a.nj; t.nk = a.nk;
+  t.own_is = a.own_is; t.own_ie = a.own_ie; t.own_js = a.own_js; t.own_je = a.own_je;
+  t.dt2 = a.dt2; t.a1 = a.a1; t.a2 = a.a2;
+  return launch_csw(t, ext, st);
 }
 
 static int check_same(const View* v, int n, const char* what) { return same_strides(v, n, what); }
@@ -269,7 +175,10 @@ extern "C" int fv3b_c_sw(const fv3b_field* f, int nf, const double* s, int ns, c
   a.nk = d->nk;
   a.dt2 = s[0];
   if (d->ni <= 0 || d->nj <= 0 || d->nk <= 0) return FV3B_OK;
-  return launch_c_sw<false>(a, (cudaStream_t)stream);
+  for (int t = 14; t < 19; ++t)
+    for (int u = 0; u < 5; ++u)
+      if (f[t].data == f[u].data) return fail(FV3B_EINVAL, "fv3b_c_sw: output %d aliases input %d", t, u);
+  return run_csw(f, f + 5, a, false, (cudaStream_t)stream);
 }
 
 // c_grid.stn (program domain nk = layers + 1).  fields: u, v, delp, pt, w,
@@ -312,7 +221,7 @@ extern "C" int fv3b_c_grid(const fv3b_field* f, int nf, const double* s, int ns,
   a.wc = wcc;
   a.nk = nkl;
   a.dt2 = s[0];
-  FV3B_TRY(launch_c_sw<true>(a, st));
+  FV3B_TRY(run_csw(cf, cf + 5, a, true, st));
   // 2) riem_solver_c on the extended columns [-1, n) x [-1, n)
   RiemArgs r;
   r.dm = delpcc; r.pt = ptcc; r.w = wcc; r.gz = gz; r.ws = ws; r.pef = pkc; r.gzo = gzc;
