@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define FV3B_ABI_VERSION 1
+#define FV3B_ABI_VERSION 2
 
 enum {
   FV3B_OK = 0,
@@ -88,8 +88,9 @@ int fv3b_tracer_2d(const fv3b_field* f, int nf, const double* s, int ns,
 
 /* K4  riem_solver_c.stn — semi-implicit vertical acoustic solve per column.
  *     Program domain nk = interface levels (layers + 1).  fields: dm, pt, w
- *     (layers), gz (interfaces), ws (2-D), pef, gz_out (interfaces; the
- *     outputs stage column intermediates and must not alias the inputs).
+ *     (layers), gz (interfaces), ws (2-D), pef, gz_out (interfaces), scratch
+ *     (3-D, one level array per column).  The outputs and the scratch stage
+ *     column intermediates and must not alias the inputs.
  *     scalars: ptop, rdgas, grav, gama, p_fac, dt. */
 int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, int ns,
                        const fv3b_domain* d, void* stream);
@@ -109,7 +110,7 @@ int fv3b_c_sw(const fv3b_field* f, int nf, const double* s, int ns,
 /* K2+K4  c_grid.stn — c_sw + riem_solver_c + p_grad_c fused (program domain
  *     nk = layers + 1).  fields: u, v, delp, pt, w, gz (3-D); the 9 c_sw
  *     metrics, ws (2-D); uc, vc (3-D outputs); scratch delpcc, ptcc, wcc, pkc,
- *     gzc (3-D, >= 1-cell halo).  scalars: dt2, ptop, rdgas, grav, gama,
+ *     gzc, riem (3-D, >= 1-cell halo).  scalars: dt2, ptop, rdgas, grav, gama,
  *     p_fac. */
 int fv3b_c_grid(const fv3b_field* f, int nf, const double* s, int ns,
                 const fv3b_domain* d, void* stream);
@@ -124,8 +125,8 @@ int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns,
 
 /* nh_d.stn — D-grid vertical solve (riem_solver3 role), program domain
  *     nk = layers + 1.  fields: delp, pt, w, gz (3-D), ws (2-D), pef,
- *     gz_out, w_out (3-D; outputs must not alias inputs).  scalars: ptop,
- *     rdgas, grav, gama, p_fac, dt. */
+ *     gz_out, w_out, scratch (3-D; outputs and scratch must not alias
+ *     inputs).  scalars: ptop, rdgas, grav, gama, p_fac, dt. */
 int fv3b_nh_d(const fv3b_field* f, int nf, const double* s, int ns,
               const fv3b_domain* d, void* stream);
 

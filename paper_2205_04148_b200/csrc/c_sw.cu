@@ -188,8 +188,8 @@ extern "C" int fv3b_c_sw(const fv3b_field* f, int nf, const double* s, int ns, c
 // p_fac.
 extern "C" int fv3b_c_grid(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                            void* stream) {
-  if (f == nullptr || d == nullptr || s == nullptr || nf != 23 || ns != 6)
-    return fail(FV3B_EINVAL, "fv3b_c_grid: expects 23 fields, 6 scalars (got %d, %d)", nf, ns);
+  if (f == nullptr || d == nullptr || s == nullptr || nf != 24 || ns != 6)
+    return fail(FV3B_EINVAL, "fv3b_c_grid: expects 24 fields, 6 scalars (got %d, %d)", nf, ns);
   if (d->nk < 4) return fail(FV3B_EDOMAIN, "fv3b_c_grid: program domain nk=%d below minimum 4", d->nk);
   // c_sw part: f[0..4] = u, v, delp, pt, w; metrics at f[6..14]
   fv3b_field cf[14];
@@ -198,7 +198,7 @@ extern "C" int fv3b_c_grid(const fv3b_field* f, int nf, const double* s, int ns,
   CswArgs a;
   FV3B_TRY(c_sw_common(cf, d, a, 5));
   const Halo h1 = {1, 0, 1, 0, 0, 0};
-  View gz, ws, uc, vc, delpcc, ptcc, wcc, pkc, gzc;
+  View gz, ws, uc, vc, delpcc, ptcc, wcc, pkc, gzc, rsc;
   FV3B_TRY(view_of(f[5], 3, *d, h1, "gz", &gz));
   FV3B_TRY(view_of(f[15], 2, *d, h1, "ws", &ws));
   FV3B_TRY(view_of(f[16], 3, *d, H0, "uc", &uc));
@@ -208,8 +208,9 @@ extern "C" int fv3b_c_grid(const fv3b_field* f, int nf, const double* s, int ns,
   FV3B_TRY(view_of(f[20], 3, *d, h1, "wcc", &wcc));
   FV3B_TRY(view_of(f[21], 3, *d, h1, "pkc", &pkc));
   FV3B_TRY(view_of(f[22], 3, *d, h1, "gzc", &gzc));
-  const View v3[14] = {a.u, a.v, a.delp, a.pt, a.w, gz, uc, vc, delpcc, ptcc, wcc, pkc, gzc, a.u};
-  FV3B_TRY(check_same(v3, 13, "fv3b_c_grid"));
+  FV3B_TRY(view_of(f[23], 3, *d, h1, "riem scratch", &rsc));
+  const View v3[14] = {a.u, a.v, a.delp, a.pt, a.w, gz, uc, vc, delpcc, ptcc, wcc, pkc, gzc, rsc};
+  FV3B_TRY(check_same(v3, 14, "fv3b_c_grid"));
   const int nkl = d->nk - 1;
   if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -224,7 +225,7 @@ extern "C" int fv3b_c_grid(const fv3b_field* f, int nf, const double* s, int ns,
   FV3B_TRY(run_csw(cf, cf + 5, a, true, st));
   // 2) riem_solver_c on the extended columns [-1, n) x [-1, n)
   RiemArgs r;
-  r.dm = delpcc; r.pt = ptcc; r.w = wcc; r.gz = gz; r.ws = ws; r.pef = pkc; r.gzo = gzc;
+  r.dm = delpcc; r.pt = ptcc; r.w = wcc; r.gz = gz; r.ws = ws; r.pef = pkc; r.gzo = gzc; r.scr = rsc;
   r.has_wout = false;
   r.ilo = -1; r.jlo = -1; r.ni_ext = d->ni + 1; r.nj_ext = d->nj + 1;
   r.nk = nkl;
@@ -243,8 +244,8 @@ extern "C" int fv3b_c_grid(const fv3b_field* f, int nf, const double* s, int ns,
 // fields: delp, pt, w, gz (3-D), ws (2-D), pef, gz_out, w_out (3-D).
 // scalars: ptop, rdgas, grav, gama, p_fac, dt.
 extern "C" int fv3b_nh_d(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d, void* stream) {
-  if (f == nullptr || d == nullptr || s == nullptr || nf != 8 || ns != 6)
-    return fail(FV3B_EINVAL, "fv3b_nh_d: expects 8 fields, 6 scalars (got %d, %d)", nf, ns);
+  if (f == nullptr || d == nullptr || s == nullptr || nf != 9 || ns != 6)
+    return fail(FV3B_EINVAL, "fv3b_nh_d: expects 9 fields, 6 scalars (got %d, %d)", nf, ns);
   if (d->nk < 4) return fail(FV3B_EDOMAIN, "fv3b_nh_d: program domain nk=%d below minimum 4", d->nk);
   RiemArgs r;
   FV3B_TRY(view_of(f[0], 3, *d, H0, "delp", &r.dm));
@@ -255,7 +256,8 @@ extern "C" int fv3b_nh_d(const fv3b_field* f, int nf, const double* s, int ns, c
   FV3B_TRY(view_of(f[5], 3, *d, H0, "pef", &r.pef));
   FV3B_TRY(view_of(f[6], 3, *d, H0, "gz_out", &r.gzo));
   FV3B_TRY(view_of(f[7], 3, *d, H0, "w_out", &r.wout));
-  for (int t = 5; t < 8; ++t)
+  FV3B_TRY(view_of(f[8], 3, *d, H0, "scratch", &r.scr));
+  for (int t = 5; t < 9; ++t)
     for (int u = 0; u < 4; ++u)
       if (f[t].data == f[u].data) return fail(FV3B_EINVAL, "fv3b_nh_d: output %d aliases input %d", t, u);
   r.has_wout = true;

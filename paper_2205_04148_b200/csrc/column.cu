@@ -69,20 +69,23 @@ constexpr int PF = 4;  // prefetch distance (levels)
 // any of them left nvcc's fast-path range, in which case the caller
 // re-evaluates the column with EXACT.
 //
-// Shared memory holds two level arrays per column (S0, S1); the third value
-// the sweeps carry between passes lives in the column's own output slots,
-// which are rewritten with their final values later in the kernel:
+// One level array per column lives in shared memory (S0); the others the
+// sweeps carry between passes live in global memory in the column's own
+// slots (L2-resident: written and re-read by the same thread within the
+// kernel, prefetched through the register ring like every other operand):
+//   scr  gam (riem_pp_fwd) -> aa (riem_w_fwd) -> gw (riem_w_sweep);
 //   pef  holds pem (riem_pem) from pass A until pass E writes pe2 + pem;
 //   gzo  holds pmc (riem_layer) from pass A until pass F, which reads it
 //        instead of re-evaluating dm / log(pem[k+1] / pem[k]) (the same
 //        IEEE operations on the same operands, so the same bits).
-// gz_out must therefore not alias gz.
+// With 648 B of shared memory per column every column of a C2 call is
+// resident at once.  Outputs and scratch must not alias the inputs.
 template <bool FAST>
 __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int c, int NC, double* sm) {
   ColArith<FAST> ar;
   const int nk = a.nk, L = nk + 1;
-  double* S0 = sm + c;           // pp -> w2 -> pe2 (shifted one level down)
-  double* S1 = sm + L * NC + c;  // gam -> aa -> gw -> pem
+  double* S0 = sm + c;  // pp -> w2 -> pe2 (shifted one level down)
+  (void)L;
 #define AT(S, k) (S)[(k) * NC]
   const double dt = a.dt, ptop = a.ptop, rdgas = a.rdgas, grav = a.grav, gama = a.gama;
   const double* __restrict__ dm = a.dm.ptr(i, j, 0);
@@ -91,7 +94,8 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   const double* __restrict__ gz = a.gz.ptr(i, j, 0);
   double* pf = a.pef.ptr(i, j, 0);
   double* go = a.gzo.ptr(i, j, 0);
-  const int64_t sk = a.dm.sk, sp = a.pef.sk, sg = a.gzo.sk;
+  double* S1 = a.scr.ptr(i, j, 0);  // gam -> aa -> gw
+  const int64_t sk = a.dm.sk, sp = a.pef.sk, sg = a.gzo.sk, s1 = a.scr.sk;
 
   // ---- pass A (forward): riem_pem, riem_layer, riem_coef, riem_pp_fwd ----
   {
@@ -126,7 +130,7 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
             bet_prev = bb - gam;
             pp_prev = ppk;
             AT(S0, k) = ppk;
-            AT(S1, k) = gam;
+            S1[k * s1] = gam;
           }
           pe_prev = pek;
           grat_prev = grat;
@@ -145,15 +149,18 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
     double ppn = AT(S0, nk);
     double gzn = __ldg(gz + (nk - 1) * sk);
     double dz_n = ar.div(__ldg(gz + nk * sk) - gzn, grav);  // dz(nk-1)
-    AT(S1, nk) = ar.div(t1g, dz_n) * (pf[nk * sp] + ppn);   // aa(nk)
-    pipelined<PF, D2>(
-        nk - 1, [&](int s) { return D2{__ldg(gz + (nk - 2 - s) * sk), pf[(nk - 1 - s) * sp]}; },  // gz(k-1), pem(k)
-        [&](int s, const D2& v) {
+    S1[nk * s1] = ar.div(t1g, dz_n) * (pf[nk * sp] + ppn);   // aa(nk)
+    pipelined<PF, D3>(
+        nk - 1,
+        [&](int s) {  // gz(k-1), pem(k), gam(k)
+          return D3{__ldg(gz + (nk - 2 - s) * sk), pf[(nk - 1 - s) * sp], S1[(nk - 1 - s) * s1]};
+        },
+        [&](int s, const D3& v) {
           const int k = nk - 1 - s;
-          const double ppk = AT(S0, k) - AT(S1, k) * ppn;
+          const double ppk = AT(S0, k) - v.z * ppn;
           AT(S0, k) = ppk;
           const double dz_k = ar.div(gzn - v.x, grav);               // dz(k-1)
-          AT(S1, k) = ar.div(t1g, dz_k + dz_n) * (v.y + ppk);       // aa(k) = t1g/(dz(k-1)+dz(k))*(pem+pp)
+          S1[k * s1] = ar.div(t1g, dz_k + dz_n) * (v.y + ppk);      // aa(k) = t1g/(dz(k-1)+dz(k))*(pem+pp)
           dz_n = dz_k;
           ppn = ppk;
           gzn = v.x;
@@ -163,12 +170,12 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   // ---- pass C (forward): riem_w_sweep (w2 replaces pp level by level) ----
   const double ws = a.ws(i, j, 0);
   {
-    double bw = 0.0, w2p = 0.0;
-    pipelined<PF, D2>(
-        nk, [&](int l) { return D2{__ldg(dm + l * sk), __ldg(w + l * sk)}; },
-        [&](int l, const D2& v) {
+    double bw = 0.0, w2p = 0.0, aal = S1[0];
+    pipelined<PF, D3>(
+        nk, [&](int l) { return D3{__ldg(dm + l * sk), __ldg(w + l * sk), S1[(l + 1) * s1]}; },
+        [&](int l, const D3& v) {
           const double dml = v.x, wl = v.y;
-          const double aal = AT(S1, l), aan = AT(S1, l + 1);
+          const double aan = v.z;  // aa(l+1); aa(l) carried from the previous level
           double w2l;
           if (l == 0) {
             bw = dml - aan;
@@ -180,10 +187,11 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
               w2l = ar.div(dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aal * w2p, bw);
             else
               w2l = ar.div(dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aan * ws - aal * w2p, bw);
-            AT(S1, l) = gw;  // aa(l) no longer needed
+            S1[l * s1] = gw;  // aa(l) no longer needed
           }
           AT(S0, l) = w2l;  // pp(l) no longer needed
           w2p = w2l;
+          aal = aan;
         });
   }
 
@@ -193,18 +201,20 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
     double* wo = a.has_wout ? a.wout.ptr(i, j, 0) : nullptr;
     const int64_t so = a.wout.sk;
     if (wo) wo[(nk - 1) * so] = w2n;
-    for (int l = nk - 2; l >= 0; --l) {
-      const double w2l = AT(S0, l) - AT(S1, l + 1) * w2n;
-      AT(S0, l) = w2l;
-      if (wo) wo[l * so] = w2l;
-      w2n = w2l;
-    }
+    pipelined<PF, D1>(
+        nk - 1, [&](int s) { return D1{S1[(nk - 1 - s) * s1]}; },  // l = nk-2-s: gw(l+1)
+        [&](int s, const D1& v) {
+          const int l = nk - 2 - s;
+          const double w2l = AT(S0, l) - v.x * w2n;
+          AT(S0, l) = w2l;
+          if (wo) wo[l * so] = w2l;
+          w2n = w2l;
+        });
   }
 
   // ---- pass E (forward): riem_pe, riem_out (pem recomputed in order) -----
   {
     double pe2 = 0.0, pem = ptop;
-    AT(S1, 0) = ptop;
     pf[0] = pe2 + pem;
     pipelined<PF, D2>(
         nk, [&](int s) { return D2{__ldg(dm + s * sk), __ldg(w + s * sk)}; },  // k = s+1: layer k-1
@@ -213,7 +223,6 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
           pe2 = pe2 + ar.div(v.x * (AT(S0, k - 1) - v.y), dt);
           pem = pem + v.x;
           AT(S0, k - 1) = pe2;  // pe2(k) (w2(k-1) consumed)
-          AT(S1, k) = pem;
           pf[k * sp] = pe2 + pem;
         });
   }
@@ -371,14 +380,19 @@ static int set_smem(const void* fn, size_t bytes) {
 // `bytes_per_col` of shared memory: maximise resident columns per SM with a
 // CTA count that is a multiple of the 4 SM sub-partitions, so every warp
 // scheduler owns the same number of recurrences.
-static int cols_per_cta(size_t bytes_per_col) {
+static int cols_per_cta(size_t bytes_per_col, int64_t columns) {
   const size_t per_sm = 228 * 1024, reserved = 1024;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t need = (columns + sms - 1) / sms;  // columns per SM for a single wave
   int best_cols = 1, best_total = 0;
   for (int m = 4; m <= 32; m += 4) {
     const size_t avail = per_sm / m;
     if (avail <= reserved) break;
     int cols = (int)((avail - reserved) / bytes_per_col);
     if (cols > NC_MAX) cols = NC_MAX;
+    if (cols == NC_MAX && cols * m >= need) return NC_MAX;  // full warps, one wave
     if (cols >= 1 && cols * m > best_total) {
       best_total = cols * m;
       best_cols = cols;
@@ -388,8 +402,8 @@ static int cols_per_cta(size_t bytes_per_col) {
 }
 
 int launch_riem(const RiemArgs& a, cudaStream_t st) {
-  const size_t per_col = 2 * (size_t)(a.nk + 1) * sizeof(double);
-  const int nc = cols_per_cta(per_col);
+  const size_t per_col = (size_t)(a.nk + 1) * sizeof(double);
+  const int nc = cols_per_cta(per_col, (int64_t)a.ni_ext * a.nj_ext);
   const size_t bytes = per_col * nc;
   FV3B_TRY(set_smem((const void*)riem_kernel, bytes));
   const int cols = a.ni_ext * a.nj_ext;
@@ -406,8 +420,8 @@ using namespace fv3b;
 // p_fac, dt.  Domain nk = interface levels (program domain, nk_layers + 1).
 extern "C" int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                                   void* stream) {
-  if (f == nullptr || d == nullptr || s == nullptr || nf != 7 || ns != 6)
-    return fail(FV3B_EINVAL, "fv3b_riem_solver_c: expects 7 fields, 6 scalars (got %d, %d)", nf, ns);
+  if (f == nullptr || d == nullptr || s == nullptr || nf != 8 || ns != 6)
+    return fail(FV3B_EINVAL, "fv3b_riem_solver_c: expects 8 fields, 6 scalars (got %d, %d)", nf, ns);
   if (d->nk < 4) return fail(FV3B_EDOMAIN, "fv3b_riem_solver_c: program domain nk=%d below minimum 4", d->nk);
   RiemArgs a;
   const Halo h0 = {0, 0, 0, 0, 0, 0};
@@ -418,7 +432,8 @@ extern "C" int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, 
   FV3B_TRY(view_of(f[4], 2, *d, h0, "ws", &a.ws));
   FV3B_TRY(view_of(f[5], 3, *d, h0, "pef", &a.pef));
   FV3B_TRY(view_of(f[6], 3, *d, h0, "gz_out", &a.gzo));
-  for (int t = 5; t < 7; ++t)
+  FV3B_TRY(view_of(f[7], 3, *d, h0, "scratch", &a.scr));
+  for (int t = 5; t < 8; ++t)
     for (int u = 0; u < 4; ++u)
       if (f[t].data == f[u].data) return fail(FV3B_EINVAL, "fv3b_riem_solver_c: output %d aliases input %d", t, u);
   if (a.dm.sk != a.pt.sk || a.dm.sk != a.w.sk || a.dm.sk != a.gz.sk)
@@ -463,7 +478,7 @@ extern "C" int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, 
   a.nk = d->nk - 1;
   if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
   const size_t per_col = 2 * (size_t)(a.nk + 1) * sizeof(double);
-  const int nc = cols_per_cta(per_col);
+  const int nc = cols_per_cta(per_col, (int64_t)a.ni * a.nj);
   const size_t bytes = per_col * nc;
   FV3B_TRY(set_smem((const void*)remap_kernel, bytes));
   remap_kernel<<<cdiv(a.ni * a.nj, nc), nc, bytes, (cudaStream_t)stream>>>(a);

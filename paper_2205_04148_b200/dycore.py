@@ -55,7 +55,7 @@ class Dycore:
         self.cur: dict[str, torch.Tensor] = {n: g.new3(device) for n in names3}
         self.cur.update({n: g.new2(device) for n in METRICS_2D})
         self.alt: dict[str, torch.Tensor] = {n: g.new3(device) for n in list(PINGPONG) + ["gz"] + cfg.tracer_names()}
-        self.scratch = {n: g.new3(device) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc")}
+        self.scratch = {n: g.new3(device) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc", "riem_scr")}
         self.halo = halo or PeriodicHalo(self)
         self.stream = None
         self.launches = 0
@@ -154,7 +154,7 @@ class Dycore:
     def c_grid(self) -> None:
         c, dt = self.cfg.consts, self.cfg.dt_acoustic
         fields = [self.f(n) for n in ("u", "v", "delp", "pt", "w", "gz")] + [self.f(m) for m in C_METRICS]
-        fields += [self.f("ws"), self.f("uc"), self.f("vc")] + [self.s(n) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc")]
+        fields += [self.f("ws"), self.f("uc"), self.f("vc")] + [self.s(n) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc", "riem_scr")]
         self.launch("c_grid", "fv3b_c_grid", fields,
                     [0.5 * dt, c["ptop"], c["rdgas"], c["grav"], c["gama"], c["p_fac"]], self.dom_ifaces)
 
@@ -168,7 +168,7 @@ class Dycore:
 
     def nh_d(self) -> None:
         c, dt = self.cfg.consts, self.cfg.dt_acoustic
-        fields = [self.f(n) for n in ("delp", "pt", "w", "gz", "ws")] + [self.f("pef"), self.a("gz"), self.a("w")]
+        fields = [self.f(n) for n in ("delp", "pt", "w", "gz", "ws")] + [self.f("pef"), self.a("gz"), self.a("w"), self.s("riem_scr")]
         self.launch("nh_d", "fv3b_nh_d", fields, [c["ptop"], c["rdgas"], c["grav"], c["gama"], c["p_fac"], dt],
                     self.dom_ifaces)
         self.swap("w", "gz")

@@ -134,7 +134,8 @@ class RiemSolverCPlan(Plan):
     def run(self, prog, ctx):
         s = prog.scalars(prog.trace[0][1])
         ctx.call("riem_pem_0", "fv3b_riem_solver_c",
-                 [ctx.f("dm"), ctx.f("pt"), ctx.f("w"), ctx.f("gz"), ctx.f("ws", 2), ctx.o("pef"), ctx.o("gz")],
+                 [ctx.f("dm"), ctx.f("pt"), ctx.f("w"), ctx.f("gz"), ctx.f("ws", 2), ctx.o("pef"), ctx.o("gz"),
+                  ctx.scratch("riem_scr")],
                  [s["ptop"], s["rdgas"], s["grav"], s["gama"], s["p_fac"], s["dt"]])
 
 
@@ -196,7 +197,7 @@ class CGridPlan(Plan):
         s = prog.scalars(prog.trace[0][1])
         fields = [ctx.f(n) for n in ("u", "v", "delp", "pt", "w", "gz")] + [ctx.f(m, 2) for m in C_METRICS]
         fields += [ctx.f("ws", 2), ctx.o("uc"), ctx.o("vc")]
-        fields += [ctx.scratch(n) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc")]
+        fields += [ctx.scratch(n) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc", "riem_scr")]
         ctx.call("c_sw_winds_0", "fv3b_c_grid", fields,
                  [s["dt2"], s["ptop"], s["rdgas"], s["grav"], s["gama"], s["p_fac"]])
 
@@ -220,7 +221,7 @@ class NhDPlan(Plan):
     def run(self, prog, ctx):
         s = prog.scalars(prog.trace[0][1])
         fields = [ctx.f(n) for n in ("delp", "pt", "w", "gz")] + [ctx.f("ws", 2)]
-        fields += [ctx.o("pef"), ctx.o("gz"), ctx.o("w")]
+        fields += [ctx.o("pef"), ctx.o("gz"), ctx.o("w"), ctx.scratch("riem_scr")]
         ctx.call("riem_pem_d_0", "fv3b_nh_d", fields,
                  [s["ptop"], s["rdgas"], s["grav"], s["gama"], s["p_fac"], s["dt"]])
 
