@@ -62,7 +62,8 @@ struct D1 { double x; };
 struct D2 { double x, y; };
 struct D3 { double x, y, z; };
 
-constexpr int PF = 4;  // prefetch distance (levels)
+constexpr int PF = 4;   // prefetch distance (levels), riem
+constexpr int PFR = 8;  // remap: short per-level bodies need a deeper ring
 
 // Statement-for-statement restatement of templates.riem_stencils for one
 // column.  FAST: branch-free divisions/logs (fastdiv.cuh), returns false if
@@ -272,6 +273,7 @@ struct RemapArgs {
   double* a2[16];
   double* a3[16];
   double* a4[16];
+  double* gam;  // scratch: gam per column (interior origin, strides sj / sk)
   int64_t sj, sk;
   int nq, ni, nj, nk;  // nk layers (program domain nk+1)
 };
@@ -280,26 +282,27 @@ template <bool FAST>
 __device__ __forceinline__ bool remap_column(const RemapArgs& a, int i, int j, int c, int NC, double* sm) {
   ColArith<FAST> ar;
   const int nk = a.nk, L = nk + 1;
-  double* G = sm + c;           // gam (depends on delp only: shared by all tracers)
-  double* E = sm + L * NC + c;  // qe
+  double* E = sm + c;  // qe (shared memory)
+  (void)L;
 #define AT(S, k) (S)[(k) * NC]
   const int64_t off = i + (int64_t)j * a.sj, sk = a.sk;
+  double* G = a.gam + off;  // gam depends on delp only: computed once, shared by all tracers (L1/L2-resident)
   const double* __restrict__ dp = a.delp.ptr(i, j, 0);
   // gam of remap_edge_fwd, once per column
   const double dp0 = __ldg(dp), dp1 = __ldg(dp + sk);
   const double grat0 = ar.div(dp1, dp0);
   const double bet0 = grat0 * (grat0 + 0.5);
-  AT(G, 0) = ar.div(1.0 + grat0 * (grat0 + 1.5), bet0);
+  G[0] = ar.div(1.0 + grat0 * (grat0 + 1.5), bet0);
   double d4last = 0.0;
   {
-    double dprev = dp0, gprev = AT(G, 0);
-    pipelined<PF, D1>(
+    double dprev = dp0, gprev = G[0];
+    pipelined<PFR, D1>(
         nk - 1, [&](int s) { return D1{__ldg(dp + (s + 1) * sk)}; },
         [&](int s, const D1& v) {
           const double d4 = ar.div(dprev, v.x);
           const double bet = 2.0 + d4 + d4 - gprev;
           gprev = ar.div(d4, bet);
-          AT(G, s + 1) = gprev;
+          G[(s + 1) * sk] = gprev;
           dprev = v.x;
           d4last = d4;
         });
@@ -311,12 +314,12 @@ __device__ __forceinline__ bool remap_column(const RemapArgs& a, int i, int j, i
     AT(E, 0) = ar.div((grat0 + grat0) * (grat0 + 1.0) * q0 + q1, bet0);
     {
       double dprev = dp0, qprev = q0, eprev = AT(E, 0);
-      pipelined<PF, D2>(
-          nk - 1, [&](int s) { return D2{__ldg(dp + (s + 1) * sk), __ldg(q + (s + 1) * sk)}; },
-          [&](int s, const D2& v) {
+      pipelined<PFR, D3>(
+          nk - 1, [&](int s) { return D3{__ldg(dp + (s + 1) * sk), __ldg(q + (s + 1) * sk), G[s * sk]}; },
+          [&](int s, const D3& v) {
             const int k = s + 1;
             const double d4 = ar.div(dprev, v.x);
-            const double bet = 2.0 + d4 + d4 - AT(G, k - 1);
+            const double bet = 2.0 + d4 + d4 - v.z;  // gam(k-1)
             eprev = ar.div(3.0 * (qprev + d4 * v.y) - eprev, bet);
             AT(E, k) = eprev;
             dprev = v.x;
@@ -325,18 +328,18 @@ __device__ __forceinline__ bool remap_column(const RemapArgs& a, int i, int j, i
       const double d4p = d4last;
       const double abot = 1.0 + d4p * (d4p + 1.5);
       AT(E, nk) = ar.div(2.0 * d4p * (d4p + 1.0) * qprev + __ldg(q + (nk - 2) * sk) - abot * eprev,
-                         d4p * (d4p + 0.5) - abot * AT(G, nk - 1));
+                         d4p * (d4p + 0.5) - abot * G[(nk - 1) * sk]);
     }
     // backward: remap_edge_bwd fused with remap_a4 for layer k
     double* o2 = a.a2[t] + off;
     double* o3 = a.a3[t] + off;
     double* o4 = a.a4[t] + off;
     double qen = AT(E, nk);
-    pipelined<PF, D1>(
-        nk, [&](int s) { return D1{__ldg(q + (nk - 1 - s) * sk)}; },
-        [&](int s, const D1& v) {
+    pipelined<PFR, D2>(
+        nk, [&](int s) { return D2{__ldg(q + (nk - 1 - s) * sk), G[(nk - 1 - s) * sk]}; },
+        [&](int s, const D2& v) {
           const int k = nk - 1 - s;
-          const double qek = AT(E, k) - AT(G, k) * qen;
+          const double qek = AT(E, k) - v.y * qen;
           const double qc = v.x;
           const double al = qek, ar_ = qen;
           const double ext = (ar_ - qc) * (qc - al);
@@ -449,18 +452,27 @@ extern "C" int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, 
   return launch_riem(a, (cudaStream_t)stream);
 }
 
-// fields: delp, then per tracer t: q_t, a2_t, a3_t, a4_t.  Domain nk =
+// fields: delp, then per tracer t: q_t, a2_t, a3_t, a4_t, then a 3-D scratch
+// (gam).  Domain nk =
 // interface levels (program domain).  No scalars.
 extern "C" int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                                   void* stream) {
   (void)s;
-  if (f == nullptr || d == nullptr || nf < 5 || (nf - 1) % 4 != 0 || (nf - 1) / 4 > 16 || ns != 0)
-    return fail(FV3B_EINVAL, "fv3b_remap_profile: expects 1 + 4*nq fields (nq <= 16), 0 scalars");
+  if (f == nullptr || d == nullptr || nf < 6 || (nf - 2) % 4 != 0 || (nf - 2) / 4 > 16 || ns != 0)
+    return fail(FV3B_EINVAL, "fv3b_remap_profile: expects 1 + 4*nq + 1 fields (nq <= 16), 0 scalars");
   if (d->nk < 3) return fail(FV3B_EDOMAIN, "fv3b_remap_profile: program domain nk=%d below minimum 3", d->nk);
   RemapArgs a;
   const Halo h0 = {0, 0, 0, 0, 0, 0};
   FV3B_TRY(view_of(f[0], 3, *d, h0, "delp", &a.delp));
-  a.nq = (nf - 1) / 4;
+  a.nq = (nf - 2) / 4;
+  {
+    View g;
+    FV3B_TRY(view_of(f[nf - 1], 3, *d, h0, "scratch", &g));
+    if (g.sj != a.delp.sj || g.sk != a.delp.sk) return fail(FV3B_ELAYOUT, "fv3b_remap_profile: scratch strides differ");
+    a.gam = g.o;
+    for (int t = 0; t < nf - 1; ++t)
+      if (f[t].data == f[nf - 1].data) return fail(FV3B_EINVAL, "fv3b_remap_profile: scratch aliases field %d", t);
+  }
   for (int t = 0; t < a.nq; ++t) {
     View v[4];
     for (int u = 0; u < 4; ++u) FV3B_TRY(view_of(f[1 + 4 * t + u], 3, *d, h0, "remap field", &v[u]));
@@ -477,7 +489,7 @@ extern "C" int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, 
   a.nj = d->nj;
   a.nk = d->nk - 1;
   if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
-  const size_t per_col = 2 * (size_t)(a.nk + 1) * sizeof(double);
+  const size_t per_col = (size_t)(a.nk + 1) * sizeof(double);
   const int nc = cols_per_cta(per_col, (int64_t)a.ni * a.nj);
   const size_t bytes = per_col * nc;
   FV3B_TRY(set_smem((const void*)remap_kernel, bytes));
