@@ -166,6 +166,20 @@ int fv3b_halo_pack_rects(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_halo_unpack_rects(const fv3b_field* f, int nf, const double* s, int ns,
                            const fv3b_domain* d, void* stream);
 
+/*   fv3b_halo_gather / fv3b_halo_scatter  index-list halo movement for the
+ *                       cubed-sphere update (edge strips arrive rotated and,
+ *                       for vector pairs, component-swapped with a sign;
+ *                       corner fill).  scalars: [buffer address bits, device
+ *                       int32 index-list address bits, n].  Gather entries
+ *                       are (field slot, interior-relative cell offset);
+ *                       scatter entries (field slot, offset, sign +/-1).
+ *                       Level k of entry s is buf[k*n + s]; all levels of up
+ *                       to 32 fields sharing one level count. */
+int fv3b_halo_gather(const fv3b_field* f, int nf, const double* s, int ns,
+                     const fv3b_domain* d, void* stream);
+int fv3b_halo_scatter(const fv3b_field* f, int nf, const double* s, int ns,
+                      const fv3b_domain* d, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

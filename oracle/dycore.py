@@ -98,7 +98,9 @@ class OracleDycore:
         for n in names:
             periodic_fill(self.state[n], self._h)
 
-    def step(self) -> None:
+    def phases(self):
+        """One timestep; yields the field lists to halo-update (the caller
+        performs the update), mirroring ``Dycore.phases``."""
         cfg, st = self.cfg, self.state
         c = dict(cfg.consts)
         dt = cfg.dt_acoustic
@@ -106,16 +108,20 @@ class OracleDycore:
             st[n][...] = 0.0
         st["dp1"][...] = st["delp"]
         for _ in range(cfg.n_split):
-            self.halo(["u", "v", "w", "delp", "pt", "gz"])
+            yield ["u", "v", "w", "delp", "pt", "gz"]
             self.call("c_grid", {**c, "dt2": 0.5 * dt})
-            self.halo(["uc", "vc"])
+            yield ["uc", "vc"]
             self.call("d_sw", {**c, "dt": dt})
             self.call("nh_d", {**c, "dt": dt})
-            self.halo(["pef", "gz"])
+            yield ["pef", "gz"]
             self.call("p_grad_d", {**c, "dt": dt})
-        self.halo(cfg.tracer_names() + ["cx", "cy", "xfa", "yfa", "mfx", "mfy"])
+        yield cfg.tracer_names() + ["cx", "cy", "xfa", "yfa", "mfx", "mfy"]
         self.call("tracer_2d", c)
         self.call("remap_tracers", c)
+
+    def step(self) -> None:
+        for names in self.phases():
+            self.halo(names)
 
 
 PROGNOSTIC = ["u", "v", "w", "delp", "pt", "gz"]

@@ -166,6 +166,62 @@ static int rects_call(const fv3b_field* f, int nf, const double* s, int ns, cons
   return check_launch(unpack ? "fv3b_halo_unpack_rects" : "fv3b_halo_pack_rects");
 }
 
+// ---------------------------------------------------------------------------
+// Index-list gather / scatter: the cubed-sphere halo update (cubesphere.py),
+// whose strips arrive rotated and component-swapped.  Entry s of a gather
+// list is (field slot, interior-relative cell offset); of a scatter list
+// (field slot, cell offset, sign).  The message holds level k of entry s at
+// buf[k * n + s] (consecutive threads touch consecutive slots).
+// ---------------------------------------------------------------------------
+struct IdxArgs {
+  double* o[HALO_MAXF];
+  int64_t sk;
+  double* buf;
+  const int* idx;
+  int n, levels;
+  bool scatter;
+};
+
+__global__ void idx_kernel(const IdxArgs a) {
+  const int k = blockIdx.y;
+  double* b = a.buf + (int64_t)k * a.n;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < a.n; s += gridDim.x * blockDim.x) {
+    if (a.scatter) {
+      const int f = a.idx[3 * s], off = a.idx[3 * s + 1], sg = a.idx[3 * s + 2];
+      const double v = b[s];
+      a.o[f][off + (int64_t)k * a.sk] = sg < 0 ? -v : v;
+    } else {
+      const int f = a.idx[2 * s], off = a.idx[2 * s + 1];
+      b[s] = a.o[f][off + (int64_t)k * a.sk];
+    }
+  }
+}
+
+static int idx_call(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d, void* stream,
+                    bool scatter) {
+  // scalars: [buffer address bits, index-list address bits, n]
+  if (f == nullptr || d == nullptr || s == nullptr || ns != 3) return fail(FV3B_EINVAL, "halo gather/scatter: 3 scalars");
+  IdxArgs a;
+  uint64_t bits;
+  memcpy(&bits, &s[0], sizeof bits);
+  a.buf = reinterpret_cast<double*>(bits);
+  memcpy(&bits, &s[1], sizeof bits);
+  a.idx = reinterpret_cast<const int*>(bits);
+  a.n = (int)s[2];
+  a.scatter = scatter;
+  if (a.buf == nullptr || a.idx == nullptr || a.n < 0) return fail(FV3B_EINVAL, "halo gather/scatter: null buffer or index list");
+  int levels[HALO_MAXF];
+  int64_t sj;
+  FV3B_TRY(collect(f, nf, d, 0, a.o, levels, &sj, &a.sk));
+  for (int t = 1; t < nf; ++t)
+    if (levels[t] != levels[0]) return fail(FV3B_EINVAL, "halo gather/scatter: fields must share their level count");
+  a.levels = levels[0];
+  if (a.n == 0) return FV3B_OK;
+  dim3 grid(cdiv(a.n, 256) < 32 ? cdiv(a.n, 256) : 32, a.levels);
+  idx_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch(scatter ? "fv3b_halo_scatter" : "fv3b_halo_gather");
+}
+
 }  // namespace fv3b
 
 using namespace fv3b;
@@ -237,4 +293,14 @@ extern "C" int fv3b_halo_pack_rects(const fv3b_field* f, int nf, const double* s
 extern "C" int fv3b_halo_unpack_rects(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                                       void* stream) {
   return rects_call(f, nf, s, ns, d, stream, true);
+}
+
+extern "C" int fv3b_halo_gather(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                void* stream) {
+  return idx_call(f, nf, s, ns, d, stream, false);
+}
+
+extern "C" int fv3b_halo_scatter(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                 void* stream) {
+  return idx_call(f, nf, s, ns, d, stream, true);
 }

@@ -257,14 +257,28 @@ class LoopbackCluster:
     are device copies between the ranks' buffers (tests / single-GPU
     validation of the decomposed path)."""
 
-    def __init__(self, dycores, px: int, py: int):
+    def __init__(self, dycores, px: int = 1, py: int = 1, halos=None):
+        """``halos``: per-rank halo objects exposing pack / finish (default:
+        a px x py doubly periodic decomposition; cubesphere.CubeHalo for
+        the six tiles of a cube)."""
         self.d = dycores
-        self.halos = [DecomposedHalo(d, px, py, r, transport=self, packer=None) for r, d in enumerate(dycores)]
+        self.halos = halos or [DecomposedHalo(d, px, py, r, transport=self, packer=None)
+                               for r, d in enumerate(dycores)]
         for d, h in zip(dycores, self.halos):
             d.halo = h
 
     def exchange(self, send, recv):  # transports run inside step(); see below
         raise RuntimeError("LoopbackCluster exchanges all ranks at once (use step())")
+
+    def exchange_all(self, reqs) -> None:
+        """One halo update on every rank (``reqs[r]``: rank r's field list)."""
+        chunks = [h.pack(names) for h, names in zip(self.halos, reqs)]
+        for r, ch in enumerate(chunks):
+            for c, (_, _, _, _, recv) in enumerate(ch):
+                for p, rt in recv:
+                    rt.copy_(dict(chunks[p][c][3])[r])  # peer p's message to r
+        for h, ch in zip(self.halos, chunks):
+            h.finish(ch)
 
     def step(self) -> None:
         gens = [d.phases() for d in self.d]
@@ -273,12 +287,4 @@ class LoopbackCluster:
             if all(r is None for r in reqs):
                 return
             assert all(r is not None for r in reqs), "ranks out of lockstep"
-            chunks = [h.pack(names) for h, names in zip(self.halos, reqs)]
-            for r, ch in enumerate(chunks):
-                for c, (_, _, _, _, recv) in enumerate(ch):
-                    for p, rt in recv:
-                        # peer p's message to r
-                        sent = dict(chunks[p][c][3])[r]
-                        rt.copy_(sent)
-            for h, ch in zip(self.halos, chunks):
-                h.finish(ch)
+            self.exchange_all(reqs)
