@@ -90,7 +90,11 @@ extern "C" int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns, c
     t.pto = a.pto.o;
     t.wo = a.wo.o;
     View* ao[6] = {&a.cxo, &a.cyo, &a.xfao, &a.yfao, &a.mfxo, &a.mfyo};
-    for (int u = 0; u < 6; ++u) t.acco[u] = ao[u]->o;
+    View* ai[6] = {&a.cx, &a.cy, &a.xfa, &a.yfa, &a.mfx, &a.mfy};
+    for (int u = 0; u < 6; ++u) {
+      t.acco[u] = ao[u]->o;
+      t.acci[u] = ai[u]->o;
+    }
     t.rarea = a.rarea.o;
     t.sj = a.u.sj;
     t.sk = a.u.sk;

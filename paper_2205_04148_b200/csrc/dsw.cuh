@@ -8,12 +8,12 @@ namespace fv3b {
 
 struct DswTpArgs {
   CUtensorMap qbox[5];  // delp, pt, w, uc, vc     (q-box: i in [-4, TI+6), j in [-3, TJ+3))
-  CUtensorMap acc[6];   // cx, cy, xfa, yfa, mfx, mfy (interior tile)
   CUtensorMap met[5];   // dx, dy, rdxa, rdya, area (q-box, level 0)
   double* delpo;
   double* pto;
   double* wo;
-  double* acco[6];      // interior origins of the accumulator outputs (may alias inputs)
+  const double* acci[6];  // interior origins of cx, cy, xfa, yfa, mfx, mfy
+  double* acco[6];        // and of their outputs (may alias the inputs)
   const double* rarea;  // interior origin (2-D)
   int64_t sj, sk;
   int i0, j0;           // allocated column / row of the interior origin

@@ -27,7 +27,8 @@ namespace fv3b {
 namespace {
 
 constexpr int SEG = 4;
-constexpr int MO_NT = 352;
+template <int TJ> constexpr int nt_of() { return TJ >= 16 ? 352 : 256; }
+template <int TJ> constexpr int cps_of() { return TJ >= 16 ? 1 : 2; }
 
 __host__ __device__ constexpr int a16(int n) { return (n + 15) / 16 * 16; }
 
@@ -78,7 +79,7 @@ struct MoLayout {
 };
 
 template <int TI, int TJ>
-__global__ void __launch_bounds__(MO_NT, 1) dsw_momentum_kernel(const __grid_constant__ DswMoArgs a) {
+__global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel(const __grid_constant__ DswMoArgs a) {
   using L = MoLayout<TI, TJ>;
   extern __shared__ __align__(128) double smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::total);
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(MO_NT, 1) dsw_momentum_kernel(const __grid_con
 
   constexpr int NSEG = TI / SEG;
   constexpr int NX2 = TJ * NSEG, NY2 = TI * (TJ / SEG);
-  static_assert(NX2 + NY2 <= MO_NT, "one item per thread in phase B");
+  static_assert(NX2 + NY2 <= nt_of<TJ>(), "one item per thread in phase B");
   const bool yth = tid >= NX2 && tid < NX2 + NY2;
   const int ci2 = yth ? (tid - NX2) % TI : 0;
   const int jb2 = yth ? ((tid - NX2) / TI) * SEG : 0;
@@ -352,10 +353,10 @@ int launch_dsw_momentum(const DswMoArgs& a0, cudaStream_t st) {
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int chunks = std::max(1, std::min(a.nk, (4 * sms + tiles - 1) / tiles));
+  const int chunks = std::max(1, std::min(a.nk, (4 * cps_of<MO_TJ>() * sms + tiles - 1) / tiles));
   a.kchunk = std::max(2, cdiv(a.nk, chunks));
   dim3 grid(cdiv(a.ni, MO_TI), cdiv(a.nj, MO_TJ), cdiv(a.nk, a.kchunk));
-  dsw_momentum_kernel<MO_TI, MO_TJ><<<grid, MO_NT, L::bytes, st>>>(a);
+  dsw_momentum_kernel<MO_TI, MO_TJ><<<grid, nt_of<MO_TJ>(), L::bytes, st>>>(a);
   return check_launch("d_sw momentum");
 }
 

@@ -30,7 +30,10 @@ namespace fv3b {
 namespace {
 
 constexpr int SEG = 4;
-constexpr int DT_NT = 352;
+// threads per CTA / CTAs per SM by tile height: 32x16 tiles run one CTA of 11
+// warps per SM, 32x8 tiles two CTAs of 8 warps (<= 128 registers per thread)
+template <int TJ> constexpr int nt_of() { return TJ >= 16 ? 352 : 256; }
+template <int TJ> constexpr int cps_of() { return TJ >= 16 ? 1 : 2; }
 
 __host__ __device__ constexpr int a16(int n) { return (n + 15) / 16 * 16; }
 
@@ -45,8 +48,9 @@ struct DtLayout {
   static constexpr int n_x = a16(XW * XH), n_y = a16(YW * YH);
   static constexpr int n_mx = a16(XW * TJ), n_my = a16(TI * YH);
   static constexpr int n_qi = a16(QW * TJ), n_qj = a16(JW * QH);
-  // stage: delp, pt, w, uc, vc (q-box) + cx, cy, xfa, yfa, mfx, mfy (interior)
-  static constexpr int n_stage = 5 * n_q + 6 * n_c;
+  // stage: delp, pt, w, uc, vc (q-box); the six accumulators are read by the
+  // threads that update them (register prefetch at the level start)
+  static constexpr int n_stage = 5 * n_q;
   static constexpr int o_stage = 0;
   static constexpr int o_met = o_stage + 2 * n_stage;  // dx, dy, rdxa, rdya, area (q-box)
   static constexpr int o_crx = o_met + 5 * n_q;
@@ -65,12 +69,12 @@ struct DtLayout {
   static constexpr size_t bytes = total * sizeof(double) + 64;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
   static_assert(TJ % SEG == 0 && TI % SEG == 0 && QW % 4 == 2 && XW % 4 == 2 && JW % 4 == 2, "tile shape");
-  static constexpr uint32_t tx_stage = (5 * QW * QH + 6 * TI * TJ) * 8;
+  static constexpr uint32_t tx_stage = 5 * QW * QH * 8;
   static constexpr uint32_t tx_met = 5 * QW * QH * 8;
 };
 
 template <int TI, int TJ>
-__global__ void __launch_bounds__(DT_NT, 1) dsw_transport_kernel(const __grid_constant__ DswTpArgs a) {
+__global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_transport_kernel(const __grid_constant__ DswTpArgs a) {
   using L = DtLayout<TI, TJ>;
   extern __shared__ __align__(128) double smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::total);  // [0],[1] level stages, [2] metrics
@@ -88,8 +92,6 @@ __global__ void __launch_bounds__(DT_NT, 1) dsw_transport_kernel(const __grid_co
     mbar_expect_tx(&bar[b], L::tx_stage);
 #pragma unroll
     for (int f = 0; f < 5; ++f) tma_load3(st + f * L::n_q, &a.qbox[f], xq, yq, k, &bar[b]);
-#pragma unroll
-    for (int f = 0; f < 6; ++f) tma_load3(st + 5 * L::n_q + f * L::n_c, &a.acc[f], xx, yy, k, &bar[b]);
   };
 
   if (tid == 0) {
@@ -128,9 +130,9 @@ __global__ void __launch_bounds__(DT_NT, 1) dsw_transport_kernel(const __grid_co
   if (k1 > k0) mbar_wait(&bar[2], 0);
 
   constexpr int NSEG = TI / SEG;
-  static_assert((TI + 6) * (TJ / SEG) + (TJ + 6) * (TI / SEG) <= DT_NT, "one phase-A item per thread");
+  static_assert((TI + 6) * (TJ / SEG) + (TJ + 6) * (TI / SEG) <= nt_of<TJ>(), "one phase-A item per thread");
   constexpr int NX2 = TJ * NSEG, NY2 = TI * (TJ / SEG);
-  static_assert(NX2 + NY2 <= DT_NT, "one item per thread in phase B");
+  static_assert(NX2 + NY2 <= nt_of<TJ>(), "one item per thread in phase B");
   // phase-B y threads own a column segment for the whole CTA (as the tracer)
   const bool yth = tid >= NX2 && tid < NX2 + NY2;
   const int ci2 = yth ? (tid - NX2) % TI : 0;
@@ -144,6 +146,8 @@ __global__ void __launch_bounds__(DT_NT, 1) dsw_transport_kernel(const __grid_co
   }
   double fy[SEG + 1], dpa[SEG], dpb[SEG];
   int pend_k = -1, pend_q = 0;  // step whose cell update is pending
+  constexpr int NT = nt_of<TJ>(), NACC = (6 * TI * TJ + NT - 1) / NT;
+  double accv[NACC];  // this thread's accumulator cells of the current level
   const int64_t sj = a.sj, sk = a.sk;
 
   // cell updates of the previous step (y threads; reads sfx / stage tiles)
@@ -173,11 +177,19 @@ __global__ void __launch_bounds__(DT_NT, 1) dsw_transport_kernel(const __grid_co
     const double* sdp = st;
     const double* suc = st + 3 * L::n_q;
     const double* svc = st + 4 * L::n_q;
-    const double* sacc = st + 5 * L::n_q;
     for (int q = 0; q < 3; ++q) {
       const double* Q = st + q * L::n_q;
       if (q == 0) {
-        // ---- level start: previous level's w update; this level's courant --
+        // ---- level start: accumulator prefetch; previous level's w update;
+        //      this level's courant ------------------------------------------
+#pragma unroll
+        for (int m = 0; m < NACC; ++m) {
+          const int e = tid + m * NT;
+          const int f = e / (TI * TJ), c = e % (TI * TJ);
+          const int gi = gi0 + c % TI, gj = gj0 + c / TI;
+          accv[m] = (e < 6 * TI * TJ && gi < a.ni && gj < a.nj) ? a.acci[f < 6 ? f : 0][gi + gj * sj + (int64_t)k * sk]
+                                                                : 0.0;
+        }
         write_pending();
         mbar_wait(&bar[(k - k0) & 1], ((k - k0) >> 1) & 1);
         // d_sw_courant: xfx = dt*uc*dy ; crx = select(uc > 0, dt*uc*rdxa[-1,0], dt*uc*rdxa)
@@ -214,10 +226,12 @@ __global__ void __launch_bounds__(DT_NT, 1) dsw_transport_kernel(const __grid_co
           }
         }
         // cx += crx, cy += cry, xfa += xfx, yfa += yfx, mfx += fxm, mfy += fym
-        for (int e = tid; e < 6 * TI * TJ; e += blockDim.x) {
+#pragma unroll
+        for (int m = 0; m < NACC; ++m) {
+          const int e = tid + m * NT;
           const int f = e / (TI * TJ), c = e % (TI * TJ);
           const int i = c % TI, j = c / TI, gi = gi0 + i, gj = gj0 + j;
-          if (gi >= a.ni || gj >= a.nj) continue;
+          if (e >= 6 * TI * TJ || gi >= a.ni || gj >= a.nj) continue;
           double d;
           switch (f) {
             case 0: d = *CX(scrx, i, j); break;
@@ -227,7 +241,7 @@ __global__ void __launch_bounds__(DT_NT, 1) dsw_transport_kernel(const __grid_co
             case 4: d = sfxm[j * L::XW + i]; break;
             default: d = sfym[j * TI + i]; break;
           }
-          a.acco[f][gi + gj * sj + (int64_t)k * sk] = sacc[f * L::n_c + c] + d;
+          a.acco[f][gi + gj * sj + (int64_t)k * sk] = accv[m] + d;
         }
       } else {
         write_pending();  // pt
@@ -322,7 +336,7 @@ __global__ void __launch_bounds__(DT_NT, 1) dsw_transport_kernel(const __grid_co
 
 }  // namespace
 
-constexpr int DT_TI = 32, DT_TJ = 16;
+constexpr int DT_TI = 32, DT_TJ = 8;
 
 int launch_dsw_transport(const DswTpArgs& a0, cudaStream_t st) {
   using L = DtLayout<DT_TI, DT_TJ>;
@@ -339,10 +353,10 @@ int launch_dsw_transport(const DswTpArgs& a0, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // ~4 waves of one CTA per SM, at least 2 levels per CTA so the prefetch overlaps
-  const int chunks = std::max(1, std::min(a.nk, (4 * sms + tiles - 1) / tiles));
+  const int chunks = std::max(1, std::min(a.nk, (4 * cps_of<DT_TJ>() * sms + tiles - 1) / tiles));
   a.kchunk = std::max(2, cdiv(a.nk, chunks));
   dim3 grid(cdiv(a.ni, DT_TI), cdiv(a.nj, DT_TJ), cdiv(a.nk, a.kchunk));
-  dsw_transport_kernel<DT_TI, DT_TJ><<<grid, DT_NT, L::bytes, st>>>(a);
+  dsw_transport_kernel<DT_TI, DT_TJ><<<grid, nt_of<DT_TJ>(), L::bytes, st>>>(a);
   return check_launch("d_sw transport");
 }
 
@@ -350,7 +364,6 @@ int dsw_transport_maps(DswTpArgs& a, const Geo& g, const fv3b_field* qbox5, cons
                        const fv3b_field* met5) {
   using L = DtLayout<DT_TI, DT_TJ>;
   for (int f = 0; f < 5; ++f) FV3B_TRY(tensor_map(qbox5[f].data, g.pitch, g.rows, g.levels, L::QW, L::QH, &a.qbox[f]));
-  for (int f = 0; f < 6; ++f) FV3B_TRY(tensor_map(acc6[f].data, g.pitch, g.rows, g.levels, DT_TI, DT_TJ, &a.acc[f]));
   for (int f = 0; f < 5; ++f) FV3B_TRY(tensor_map(met5[f].data, g.pitch, g.rows, 1, L::QW, L::QH, &a.met[f]));
   return FV3B_OK;
 }

@@ -32,7 +32,10 @@ namespace fv3b {
 
 constexpr int NQMAX = 16;
 constexpr int SEG = 4;  // cells per sliding-window segment
-constexpr int TP_NT = 352;  // threads per CTA (11 warps): >= phase-A items
+// threads per CTA / CTAs per SM by tile height (>= phase-A items): 32x16
+// tiles one CTA of 11 warps, 32x8 tiles two CTAs of 8 warps
+template <int TJ> constexpr int nt_of() { return TJ >= 16 ? 352 : 256; }
+template <int TJ, bool MASS> constexpr int cps_of() { return TJ >= 16 ? (MASS ? 1 : 2) : 2; }
 
 struct TpArgs {
   CUtensorMap q[NQMAX];
@@ -88,7 +91,7 @@ struct TpLayout {
 };
 
 template <int TI, int TJ, bool MASS>
-__global__ void __launch_bounds__(TP_NT, MASS ? 1 : 2) tp_kernel(const __grid_constant__ TpArgs a) {
+__global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(const __grid_constant__ TpArgs a) {
   using L = TpLayout<TI, TJ, MASS>;
   extern __shared__ __align__(128) double smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::total);  // [0],[1] step stages, [2] area
@@ -146,9 +149,9 @@ __global__ void __launch_bounds__(TP_NT, MASS ? 1 : 2) tp_kernel(const __grid_co
   if (nsteps > 0) mbar_wait(&bar[2], 0);
 
   constexpr int NSEG = TI / SEG;
-  static_assert((TI + 6) * (TJ / SEG) + (TJ + 6) * (TI / SEG) <= TP_NT, "one phase-A item per thread");
+  static_assert((TI + 6) * (TJ / SEG) + (TJ + 6) * (TI / SEG) <= nt_of<TJ>(), "one phase-A item per thread");
   constexpr int NX2 = TJ * NSEG, NY2 = TI * (TJ / SEG);
-  static_assert(NX2 + NY2 <= TP_NT, "one item per thread in phase 2");
+  static_assert(NX2 + NY2 <= nt_of<TJ>(), "one item per thread in phase 2");
   // Phase-2 y threads own a fixed column segment for the whole CTA: they
   // keep rarea, and the previous step's fy / q / dp in registers and write
   // that step's result while the next step's phase 1 runs (2 barriers/level).
@@ -316,10 +319,10 @@ static int launch_tp(const TpArgs& a0, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   // ~4 waves of one CTA per SM; at least 2 levels per CTA so the pipeline overlaps
-  const int chunks = std::max(1, std::min(a.nk, ((MASS ? 4 : 8) * sms + tiles - 1) / tiles));
+  const int chunks = std::max(1, std::min(a.nk, (4 * cps_of<TJ, MASS>() * sms + tiles - 1) / tiles));
   a.kchunk = std::max(MASS ? 1 : 2, cdiv(a.nk, chunks));
   dim3 grid(cdiv(a.ni, TI), cdiv(a.nj, TJ), cdiv(a.nk, a.kchunk));
-  tp_kernel<TI, TJ, MASS><<<grid, TP_NT, L::bytes, st>>>(a);
+  tp_kernel<TI, TJ, MASS><<<grid, nt_of<TJ>(), L::bytes, st>>>(a);
   return check_launch(MASS ? "tracer_2d" : "fv_tp_2d");
 }
 
@@ -397,7 +400,7 @@ extern "C" int fv3b_fv_tp_2d(const fv3b_field* f, int nf, const double* s, int n
   return launch_tp<TP_TI, TP_TJ, false>(a, (cudaStream_t)stream);
 }
 
-static constexpr int TR_TI = 32, TR_TJ = 16;
+static constexpr int TR_TI = 32, TR_TJ = 8;
 
 extern "C" int fv3b_tracer_2d(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                               void* stream) {
