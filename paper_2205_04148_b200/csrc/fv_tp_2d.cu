@@ -159,6 +159,9 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(c
   const int ci2 = yth ? (tid - NX2) % TI : 0;
   const int jb2 = yth ? ((tid - NX2) / TI) * SEG : 0;
   const int gi2 = gi0 + ci2;
+  // phase-A worker slot: the y threads (which also write the pending cell
+  // updates in phase A) take items only after every other thread has one
+  const int wslot = tid < NX2 ? tid : (yth ? nt_of<TJ>() - NY2 + (tid - NX2) : tid - NY2);
   double ra[SEG];
 #pragma unroll
   for (int u = 0; u < SEG; ++u) {
@@ -185,8 +188,8 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(c
     }
   };
 
-  for (int step = 0; step < nsteps; ++step) {
-    const int k = k0 + step / a.nq, t = step % a.nq;
+  int k = k0, t = 0;  // level / tracer of `step`, advanced incrementally
+  for (int step = 0; step < nsteps; ++step, (++t == a.nq ? (t = 0, ++k) : 0)) {
     const int b = step & 1;
     if (tid == 0 && step + 1 < nsteps) {
       fence_async_smem();
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(c
       constexpr int NCY = TI + 6, NSY = TJ / SEG;  // columns i in [-3, TI+3)
       constexpr int NRX = TJ + 6, NSX = TI / SEG;  // rows j in [-3, TJ+3)
       constexpr int NY = NCY * NSY, NX = NRX * NSX;
-      for (int item = tid; item < NY + NX; item += blockDim.x) {
+      for (int item = wslot; item < NY + NX; item += blockDim.x) {
         if (item < NY) {
           const int ci = item % NCY - 3, jb = (item / NCY) * SEG;
           double f[SEG + 1];
