@@ -21,7 +21,8 @@ namespace fv3b {
 
 namespace {
 
-constexpr int CS_NT = 352;
+// 32x8 tiles: two CTAs of 8 warps per SM (112 KB of shared memory each)
+constexpr int CS_NT = 256;
 
 __host__ __device__ constexpr int a16(int n) { return (n + 15) / 16 * 16; }
 
@@ -40,7 +41,7 @@ struct CsLayout {
 };
 
 template <int TI, int TJ, bool EXT>
-__global__ void __launch_bounds__(CS_NT, 1) csw_kernel(const __grid_constant__ CswTmaArgs a) {
+__global__ void __launch_bounds__(CS_NT, 2) csw_kernel(const __grid_constant__ CswTmaArgs a) {
   using L = CsLayout<TI, TJ>;
   extern __shared__ __align__(128) double smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::total);
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(CS_NT, 1) csw_kernel(const __grid_constant__ C
 
 }  // namespace
 
-constexpr int CS_TI = 32, CS_TJ = 16;
+constexpr int CS_TI = 32, CS_TJ = 8;
 
 int csw_maps(CswTmaArgs& a, const Geo& g, const fv3b_field* in5, const fv3b_field* met9) {
   using L = CsLayout<CS_TI, CS_TJ>;
@@ -230,7 +231,7 @@ static int launch_t(const CswTmaArgs& a0, cudaStream_t st) {
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int chunks = std::max(1, std::min(a.nk, (4 * sms + tiles - 1) / tiles));
+  const int chunks = std::max(1, std::min(a.nk, (8 * sms + tiles - 1) / tiles));
   a.kchunk = std::max(2, cdiv(a.nk, chunks));
   dim3 grid(cdiv(a.ni, CS_TI), cdiv(a.nj, CS_TJ), cdiv(a.nk, a.kchunk));
   csw_kernel<CS_TI, CS_TJ, EXT><<<grid, CS_NT, L::bytes, st>>>(a);
