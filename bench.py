@@ -210,7 +210,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     from paper_2205_04148_b200.dycore import Dycore, kernels_per_step
     from paper_2205_04148_b200.parallel import DecomposedHalo, grid_shape
     from paper_2205_04148_b200.state import initial_state
-    from paper_2205_04148_b200.traffic import compulsory_bytes
+    from paper_2205_04148_b200 import perf_model
 
     torch.cuda.set_device(local)
     _lib.lib()  # no CPU fallback: fail loudly if the library is missing
@@ -304,25 +304,26 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     cells = cfg.cells * world
     value = cells / (ms * 1e-3)
     node_total = {n: sum(v) for n, v in per_node.items()}
-    top = max(node_total, key=node_total.get)
-    nk_prog = {"c_grid": cfg.nk + 1, "nh_d": cfg.nk + 1, "p_grad_d": cfg.nk + 1, "remap_tracers": cfg.nk + 1}
-    prog = {"halo": None}.get(top, top)
-    algo = compulsory_bytes(prog, (cfg.ni, cfg.nj, nk_prog.get(top, cfg.nk)))
-    mean_launch = statistics.mean(per_node[top])
+    # the Fig. 10 model-augmented report (perf_model): first-touch compulsory
+    # bytes per launch / measured peak HBM bandwidth vs the CUDA-event times
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
+    nk_prog = {"c_grid": cfg.nk + 1, "nh_d": cfg.nk + 1, "p_grad_d": cfg.nk + 1, "remap_tracers": cfg.nk + 1}
+    progs = [n for n in per_node if n != "halo"]
+    report = perf_model.build_report({n: per_node[n] for n in progs},
+                                     {n: (cfg.ni, cfg.nj, nk_prog.get(n, cfg.nk)) for n in progs}, peak * 1e9)
+    by = {e.kernel: e for e in report.entries}
+    top = max(progs, key=lambda n: node_total[n])
+    algo = by[top].unique_bytes
+    mean_launch = statistics.mean(per_node[top])
     achieved = algo / mean_launch / 1e9
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         traffic = json.loads(tf.read_text()).get(top)
-    step_bytes = 0
-    for n, v in per_node.items():
-        if n != "halo":
-            step_bytes += compulsory_bytes(n, (cfg.ni, cfg.nj, nk_prog.get(n, cfg.nk))) * len(v) / args.steps
-
+    step_bytes = sum(by[n].unique_bytes * len(per_node[n]) for n in progs) / args.steps
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:
         v, cores, sample = cpu_run(1)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
 
@@ -340,7 +341,13 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "algo_bytes_per_launch": algo,
                      "mean_launch_s": mean_launch, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)",
+                     "algo_bytes_source": by[top].source,
                      "step_algo_bytes": step_bytes, "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak},
+        "report": {e.kernel: {"invocations_per_step": e.invocations // args.steps,
+                              "measured_us": round(e.measured_time * 1e6, 2),
+                              "bound_us": round(e.bound_time * 1e6, 2),
+                              "utilization": round(e.utilization, 4)} for e in report.entries},
+        "hotspots": perf_model.hotspot_list(report, 3),
         "kernels_ms_per_step": {n: round(v * 1e3 / args.steps, 4) for n, v in
                                 sorted(node_total.items(), key=lambda x: -x[1])},
         "eager_launches_per_step": eager_launches / args.steps,
