@@ -7,7 +7,9 @@ has ``nk + 1`` levels and a 4-cell I/J halo, so layer programs (domain nk)
 and interface programs (domain nk + 1) address the same buffers.  Fields a
 kernel reads at horizontal offsets and rewrites (u, v, w, delp, pt, tracers)
 are ping-ponged between two buffers; pointwise accumulators and in-place
-column outputs are updated in place.
+column outputs are updated in place.  The state is the interior (layer fields
+on levels < nk, interface fields on all nk + 1 levels): the halos and the
+unused top slot of a ping-pong layer field are scratch between halo updates.
 
 The CPU counterpart is ``oracle/dycore.py`` (tests only); the two agree
 bitwise (tests/test_gpu_dycore.py).

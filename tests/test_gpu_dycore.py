@@ -11,6 +11,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 FIELDS = ["u", "v", "w", "delp", "pt", "gz", "pef", "q0", "q7", "q3_a4", "mfx", "cy"]
+INTERFACE = ("gz", "pef")
 
 
 def _run(cfg, steps, graph):
@@ -44,9 +45,40 @@ def test_dycore_10_steps_bitwise_vs_oracle(graph):
         ref.step()
     h = cfg.halo
     for n in FIELDS:
-        a = gpu[n][h:-h, h:-h]
-        b = st[n][h:-h, h:-h]
+        # the state is the interior: layer fields on levels < nk, interface
+        # fields (gz, pef) on all nk + 1 (halos and the unused top slot of
+        # ping-pong layer fields are scratch between halo updates)
+        top = cfg.nk + 1 if n in INTERFACE else cfg.nk
+        a = gpu[n][h:-h, h:-h, :top]
+        b = st[n][h:-h, h:-h, :top]
         assert np.isfinite(b).all(), n
         if not np.array_equal(a, b):
             err = np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))
             raise AssertionError(f"{n}: differs after 10 steps, max rel err {err:.3e}")
+
+
+def test_checkpoint_restart_is_bitwise(tmp_path):
+    """save_state / load_state (reference field-file format) restart a run
+    exactly: 2 steps + checkpoint + 1 step == 3 steps."""
+    import torch
+
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.dycore import Dycore
+    from paper_2205_04148_b200.fieldio import load_state, save_state
+    from paper_2205_04148_b200.state import initial_state
+
+    cfg = RunConfig(ni=32, nj=24, nk=10, n_split=3, dt_atmos=45.0)
+    a = Dycore(cfg, initial_state(cfg))
+    for _ in range(2):
+        a.step()
+    save_state(a, tmp_path / "ckpt")
+    a.step()
+    conf, st = load_state(tmp_path / "ckpt")
+    assert RunConfig(**conf) == cfg
+    b = Dycore(RunConfig(**conf), st)
+    b.step()
+    torch.cuda.synchronize()
+    h = cfg.halo
+    for n in ["u", "v", "w", "delp", "pt", "gz", "q0", "q5_a3"]:
+        top = cfg.nk + 1 if n in INTERFACE else cfg.nk
+        assert np.array_equal(a.download([n])[n][h:-h, h:-h, :top], b.download([n])[n][h:-h, h:-h, :top]), n
