@@ -39,6 +39,19 @@ int check_launch(const char* what);
 
 inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
+// Levels per CTA of a level-marching tile kernel: a single wave when the
+// tiles fit the resident CTA slots (every CTA gets an equal chunk of levels,
+// no tail wave), otherwise one whole column of levels per CTA.
+inline int level_chunk(int tiles, int nk, int ctas_per_sm) {
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int slots = sms * ctas_per_sm;
+  int per_tile = tiles >= slots ? 1 : slots / tiles;
+  if (per_tile > nk) per_tile = nk;
+  return cdiv(nk, per_tile);
+}
+
 // Tile-local shared-memory array covering [i0, i1) x [j0, j1) (tile coords).
 struct STile {
   double* p;

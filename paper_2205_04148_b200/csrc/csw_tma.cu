@@ -231,8 +231,8 @@ static int launch_t(const CswTmaArgs& a0, cudaStream_t st) {
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int chunks = std::max(1, std::min(a.nk, (8 * sms + tiles - 1) / tiles));
-  a.kchunk = std::max(2, cdiv(a.nk, chunks));
+  (void)sms;
+  a.kchunk = level_chunk(tiles, a.nk, 2);
   dim3 grid(cdiv(a.ni, CS_TI), cdiv(a.nj, CS_TJ), cdiv(a.nk, a.kchunk));
   csw_kernel<CS_TI, CS_TJ, EXT><<<grid, CS_NT, L::bytes, st>>>(a);
   return check_launch("c_sw");

@@ -353,8 +353,8 @@ int launch_dsw_momentum(const DswMoArgs& a0, cudaStream_t st) {
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int chunks = std::max(1, std::min(a.nk, (4 * cps_of<MO_TJ>() * sms + tiles - 1) / tiles));
-  a.kchunk = std::max(2, cdiv(a.nk, chunks));
+  (void)sms;
+  a.kchunk = level_chunk(tiles, a.nk, cps_of<MO_TJ>());
   dim3 grid(cdiv(a.ni, MO_TI), cdiv(a.nj, MO_TJ), cdiv(a.nk, a.kchunk));
   dsw_momentum_kernel<MO_TI, MO_TJ><<<grid, nt_of<MO_TJ>(), L::bytes, st>>>(a);
   return check_launch("d_sw momentum");

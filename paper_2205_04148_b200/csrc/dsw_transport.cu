@@ -356,8 +356,8 @@ int launch_dsw_transport(const DswTpArgs& a0, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // ~4 waves of one CTA per SM, at least 2 levels per CTA so the prefetch overlaps
-  const int chunks = std::max(1, std::min(a.nk, (4 * cps_of<DT_TJ>() * sms + tiles - 1) / tiles));
-  a.kchunk = std::max(2, cdiv(a.nk, chunks));
+  (void)sms;
+  a.kchunk = level_chunk(tiles, a.nk, cps_of<DT_TJ>());
   dim3 grid(cdiv(a.ni, DT_TI), cdiv(a.nj, DT_TJ), cdiv(a.nk, a.kchunk));
   dsw_transport_kernel<DT_TI, DT_TJ><<<grid, nt_of<DT_TJ>(), L::bytes, st>>>(a);
   return check_launch("d_sw transport");

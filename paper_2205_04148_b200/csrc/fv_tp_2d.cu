@@ -322,8 +322,8 @@ static int launch_tp(const TpArgs& a0, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   // ~4 waves of one CTA per SM; at least 2 levels per CTA so the pipeline overlaps
-  const int chunks = std::max(1, std::min(a.nk, (4 * cps_of<TJ, MASS>() * sms + tiles - 1) / tiles));
-  a.kchunk = std::max(MASS ? 1 : 2, cdiv(a.nk, chunks));
+  (void)sms;
+  a.kchunk = level_chunk(tiles, a.nk, cps_of<TJ, MASS>());
   dim3 grid(cdiv(a.ni, TI), cdiv(a.nj, TJ), cdiv(a.nk, a.kchunk));
   tp_kernel<TI, TJ, MASS><<<grid, nt_of<TJ>(), L::bytes, st>>>(a);
   return check_launch(MASS ? "tracer_2d" : "fv_tp_2d");
