@@ -42,15 +42,17 @@ __device__ __forceinline__ void ppm_line(const double* q, int s, const double* c
   }
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
-    // branch-free: both upwind candidates, then selects (the reference's
-    // select() evaluates both branches too, reference.py:250-252)
+    // Only the selected upwind candidate is evaluated (select() has no side
+    // effects, so dropping the other branch changes nothing), with operand
+    // selects instead of two evaluations: for cc > 0 the candidate is
+    // (1 - cc) * (br[f] - cc * b0[f]) = (1 + m) * (br[f] + m * b0[f]) with
+    // m = -cc, exactly (x - y == x + (-y) and (-cc) * b == -(cc * b) in IEEE).
     const double cc = c[f * cs];
     const bool smooth = sm[f] || sm[f + 1];  // cells f-1, f
-    const double tp = (1.0 - cc) * (br[f] - cc * b0[f]);
-    const double tn = (1.0 + cc) * (bl[f + 1] + cc * b0[f + 1]);
     const bool pos = cc > 0.0;
+    const double m = pos ? -cc : cc;
+    const double t = (1.0 + m) * ((pos ? br[f] : bl[f + 1]) + m * (pos ? b0[f] : b0[f + 1]));
     const double base = pos ? qv[f + 2] : qv[f + 3];
-    const double t = pos ? tp : tn;
     out[f] = base + (smooth ? t : 0.0);
   }
 }
