@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from ..device import DEFAULT_HALO, Grid
-from ..program import Program, as_program
+from ..program import Program, as_program, is_graph
 from .plans import LaunchCtx, plan_for
 
 FULL_TILE = (True, True, True, True)
@@ -70,7 +70,12 @@ class Uploaded:
 
 
 def upload(program, inputs: dict, domain, placement=None, device="cuda") -> Uploaded:
-    """Validate and copy a program's inputs into the device layout."""
+    """Validate and copy a program's inputs into the device layout.  A
+    lowered reference ``DataflowGraph`` brings its own domain and
+    ``RankPlacement`` (``ir/graph.py:257-268``) when none are given."""
+    if is_graph(program):
+        domain = program.domain if domain is None else domain
+        placement = program.placement if placement is None else placement
     prog = as_program(program)
     domain = tuple(int(x) for x in domain)
     prog.check_domain(domain)

@@ -12,7 +12,7 @@ on B200 measurements.
   (``SPEC.md:634``).
 
 The bytes are the first-touch compulsory bytes of SURVEY 8d (the reference
-AccessRecorder rule): brute-force values from ``programs/traffic.json``
+AccessRecorder rule): brute-force values from ``traffic_table.json``
 (tools/traffic_table.py) when the configuration is tabulated, else the
 box model of :mod:`.traffic` (an upper bound: whole halo boxes).
 """
@@ -25,7 +25,7 @@ from pathlib import Path
 
 from .traffic import compulsory_bytes
 
-_TABLE = Path(__file__).resolve().parent / "programs" / "traffic.json"
+_TABLE = Path(__file__).resolve().parent / "traffic_table.json"
 
 
 def unique_bytes(program: str, domain) -> tuple[int, str]:

@@ -226,6 +226,8 @@ class Program:
 
     @property
     def trace(self) -> list[tuple[str, dict[str, float]]]:
+        if "trace" in self.canon:  # a lowered graph's resolved execution trace
+            return [(n, dict(kw)) for n, kw in self.canon["trace"]]
         return resolve_trace(self.canon)
 
     def scalars(self, invoke_kwargs: dict[str, float]) -> dict[str, float]:
@@ -294,8 +296,65 @@ def known_programs_names() -> list[str]:
     return sorted(p.stem for p in PROGRAM_DIR.glob("*.json"))
 
 
+def _structure_fp(canon: dict) -> str:
+    """Fingerprint of fields + stencil blocks, without stencil parameter
+    lists (a lowered graph does not carry them)."""
+    st = [{"name": s["name"], "blocks": s["blocks"]} for s in canon["stencils"]]
+    doc = json.dumps({"fields": canon["fields"], "stencils": st}, sort_keys=True)
+    return hashlib.sha256(doc.encode()).hexdigest()[:16]
+
+
+def is_graph(obj: Any) -> bool:
+    return all(hasattr(obj, a) for a in ("arrays", "states", "execution_trace"))
+
+
+def canonicalize_graph(graph) -> dict:
+    """Canonical tree of a reference ``DataflowGraph`` (``ir/graph.py:257-355``,
+    as produced by ``lower``): fields from its array catalog, stencils from
+    its StencilNodes (node name ``<stencil>_<block>``, ``graph.py:138-143``)
+    and the resolved invocation trace from ``execution_trace``
+    (``graph.py:299-329``), the order ``run_reference_graph`` executes
+    (``reference.py:342-365``).  Fused nodes (``a+b``) are not accepted."""
+    fields = [{"name": n, "dims": list(a.dims), "dtype": a.dtype, "temporary": bool(a.transient)}
+              for n, a in graph.arrays.items()]
+    blocks: dict[str, dict[int, dict]] = {}
+    order: list[str] = []
+    by_state = {s.name: s for s in graph.states}
+    trace = []
+    for sname, env in graph.execution_trace():
+        cur = None
+        for node in by_state[sname].sequence:
+            if "+" in node.name or len(node.blocks) != 1:
+                raise KeyError(f"fused graph node {node.name!r} has no B200 kernel plan")
+            stencil, bi = node.name.rsplit("_", 1)
+            b = node.blocks[0]
+            iv = b.interval
+            stmts = []
+            for st in b.statements:
+                region = None
+                if st.region is not None:
+                    region = {"i": _axis(st.region.i), "j": _axis(st.region.j)}
+                stmts.append({"target": st.target, "expr": canon_expr(st.expr), "region": region})
+            if stencil not in blocks:
+                blocks[stencil] = {}
+                order.append(stencil)
+            blocks[stencil][int(bi)] = {
+                "policy": b.policy,
+                "interval": [[iv.start.anchor, int(iv.start.offset)], [iv.end.anchor, int(iv.end.offset)]],
+                "statements": stmts,
+            }
+            kw = {k: float(_eval_driver(canon_expr(v), dict(env))) for k, v in sorted(node.kwargs.items())}
+            if cur is None or cur[0] != stencil:
+                cur = (stencil, kw)
+                trace.append(cur)
+    stencils = [{"name": n, "params": [], "blocks": [blocks[n][i] for i in sorted(blocks[n])]} for n in order]
+    consts = [[k, float(v)] for k, v in getattr(graph, "symbols", {}).items()]
+    return {"consts": consts, "fields": fields, "stencils": stencils, "driver": [], "trace": trace}
+
+
 def as_program(program: Any) -> Program:
-    """Accept a :class:`Program`, a manifest name, or a reference AST.
+    """Accept a :class:`Program`, a manifest name, a reference AST or a
+    lowered reference ``DataflowGraph``.
 
     A reference ``StencilProgram`` is matched to a shipped manifest by
     structural fingerprint; its own constants and driver are kept.
@@ -305,6 +364,15 @@ def as_program(program: Any) -> Program:
         return program
     if isinstance(program, str):
         return load_program(program)
+    if is_graph(program):
+        canon = canonicalize_graph(program)
+        fp = _structure_fp(canon)
+        known = {_structure_fp(p.canon): p for p in known_programs().values()}
+        if fp not in known:
+            raise KeyError(f"no B200 kernel plan for graph structure {fp}")
+        base = known[fp]
+        return Program(name=base.name, canon=canon, fields=base.fields, extension=base.extension,
+                       min_domain=base.min_domain, consts={n: v for n, v in canon["consts"]}, fp=base.fp)
     canon = canonicalize(program)
     fp = fingerprint(canon)
     known = known_programs()

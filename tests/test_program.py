@@ -108,3 +108,22 @@ def test_library_loads_and_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(h, s), f"{s} declared in include/fv3b.h but not exported"
     assert _lib.lib().fv3b_abi_version() == _lib.ABI_VERSION
+
+
+@pytest.mark.skipif(not _ref.available(), reason="reference not importable")
+@pytest.mark.parametrize("name", ["copy", "fv_tp_2d", "tracer_2d", "c_sw", "c_grid", "d_sw", "nh_d", "p_grad_d",
+                                  "riem_solver_c", "remap_profile", "remap_tracers"])
+def test_lowered_graph_intake_matches_program(name):
+    """run_scheduled(graph, ...) contract: a DataflowGraph
+    from the reference ``lower`` maps to the same kernel plan and the same
+    resolved invocation trace as the StencilProgram it was lowered from."""
+    from paper_2205_04148_b200.program import PROGRAM_DIR, as_program
+
+    R = _ref.load()
+    from stencilkit.ir.lower import lower
+
+    prog = R.parse_program((PROGRAM_DIR / f"{name}.stn").read_text())
+    g = lower(prog, (16, 16, 9), R.RankPlacement(False, False, False, False))
+    pa, pg = as_program(prog), as_program(g)
+    assert pg.name == pa.name == name
+    assert pg.trace == pa.trace

@@ -1,7 +1,7 @@
 """First-touch compulsory bytes of every dycore program at the
 bench sizes, by brute force: the oracle interpreter with the FirstTouch
 recorder (the reference AccessRecorder rule) on seeded inputs.  Writes
-paper_2205_04148_b200/programs/traffic.json, which bench.py uses for the
+paper_2205_04148_b200/traffic_table.json, which bench.py uses for the
 roofline's algorithmic bytes.
 
     python tools/traffic_table.py [ni]
@@ -21,7 +21,7 @@ ni = int(sys.argv[1]) if len(sys.argv) > 1 else 192
 nk = 80
 PROGS = [("c_grid", nk + 1), ("d_sw", nk), ("nh_d", nk + 1), ("p_grad_d", nk + 1), ("tracer_2d", nk),
          ("remap_tracers", nk + 1)]
-out_path = ROOT / "paper_2205_04148_b200" / "programs" / "traffic.json"
+out_path = ROOT / "paper_2205_04148_b200" / "traffic_table.json"
 table = json.loads(out_path.read_text()) if out_path.exists() else {}
 for name, k in PROGS:
     dom = (ni, ni, k)
