@@ -13,6 +13,8 @@
 // oracle extension, detmath.cuh).
 #include <math.h>
 
+#include <type_traits>
+
 #include "column.cuh"
 #include "detmath.cuh"
 #include "fastdiv.cuh"
@@ -99,49 +101,63 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   const int64_t sk = a.dm.sk, sp = a.pef.sk, sg = a.gzo.sk, s1 = a.scr.sk;
 
   // ---- pass A (forward): riem_pem, riem_layer, riem_coef, riem_pp_fwd ----
+  // Level 0 and level nk-1 are peeled so the pipelined body is branch-free
+  // (the scheduler interleaves the independent logs / divisions of
+  // consecutive levels around the bet / pp recurrence).  For k >= 1 the
+  // statement ppc = (ddc[k-1] - ppc[k-1]) / betp[k-1] also covers k = 1,
+  // where the reference has ddc[0] / betp[0]: ppc[0] = 0 and x - 0.0 == x.
   {
     double pem0 = ptop;  // pem(k)
     pf[0] = pem0;
     double pe_prev = 0.0, grat_prev = 0.0, bet_prev = 0.0, pp_prev = 0.0;
     double dm_k = __ldg(dm), gzk = __ldg(gz);
+    auto level = [&](int k, const D3& v, auto first, auto last) {
+      const double dm_n = v.x, gzk1 = v.y;
+      const double pem1 = pem0 + dm_k;  // pem(k+1) = pem + dm
+      pf[(k + 1) * sp] = pem1;
+      const double pmk = ar.div(dm_k, ar.log(ar.div(pem1, pem0)));
+      go[k * sg] = pmk;
+      const double pek = ar.div(dm_k * rdgas * v.z, gzk - gzk1) - pmk;
+      // layer k coefficients (riem_coef)
+      double grat = 0.0, bb = 2.0;
+      if constexpr (!decltype(last)::value) {
+        grat = ar.div(dm_k, dm_n);
+        bb = 2.0 * (1.0 + grat);
+      }
+      // interface k of riem_pp_fwd (uses layer k-1's dd, needing pe(k))
+      if constexpr (decltype(first)::value) {
+        bet_prev = bb;
+        pp_prev = 0.0;
+        AT(S0, 0) = 0.0;
+      } else {
+        const double dd_prev = 3.0 * (pe_prev + grat_prev * pek);
+        const double rb = ar.rcp(bet_prev);
+        const double ppk = ar.div_r(dd_prev - pp_prev, bet_prev, rb);
+        const double gam = ar.div_r(grat_prev, bet_prev, rb);
+        bet_prev = bb - gam;
+        pp_prev = ppk;
+        AT(S0, k) = ppk;
+        S1[k * s1] = gam;
+      }
+      pe_prev = pek;
+      grat_prev = grat;
+      pem0 = pem1;
+      dm_k = dm_n;
+      gzk = gzk1;
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    level(0, D3{__ldg(dm + sk), __ldg(gz + sk), __ldg(pt)}, T_{}, F_{});
     pipelined<PF, D3>(
-        nk,
-        [&](int k) {  // dm(k+1), gz(k+1), pt(k)
-          return D3{(k + 1 < nk) ? __ldg(dm + (k + 1) * sk) : 0.0, __ldg(gz + (k + 1) * sk), __ldg(pt + k * sk)};
+        nk - 2,
+        [&](int s) {  // k = s + 1: dm(k+1), gz(k+1), pt(k)
+          return D3{__ldg(dm + (s + 2) * sk), __ldg(gz + (s + 2) * sk), __ldg(pt + (s + 1) * sk)};
         },
-        [&](int k, const D3& v) {
-          const double dm_n = v.x, gzk1 = v.y;
-          const double pem1 = pem0 + dm_k;  // pem(k+1) = pem + dm
-          pf[(k + 1) * sp] = pem1;
-          const double pmk = ar.div(dm_k, ar.log(ar.div(pem1, pem0)));
-          go[k * sg] = pmk;
-          const double pek = ar.div(dm_k * rdgas * v.z, gzk - gzk1) - pmk;
-          // layer k coefficients (riem_coef)
-          const double grat = (k < nk - 1) ? ar.div(dm_k, dm_n) : 0.0;
-          const double bb = (k < nk - 1) ? 2.0 * (1.0 + grat) : 2.0;
-          // interface k of riem_pp_fwd (uses layer k-1's dd, needing pe(k))
-          if (k == 0) {
-            bet_prev = bb;
-            pp_prev = 0.0;
-            AT(S0, 0) = 0.0;
-          } else {
-            const double dd_prev = (k - 1 < nk - 1) ? 3.0 * (pe_prev + grat_prev * pek) : 3.0 * pe_prev;
-            const double ppk = ar.div((k == 1) ? dd_prev : dd_prev - pp_prev, bet_prev);
-            const double gam = ar.div(grat_prev, bet_prev);
-            bet_prev = bb - gam;
-            pp_prev = ppk;
-            AT(S0, k) = ppk;
-            S1[k * s1] = gam;
-          }
-          pe_prev = pek;
-          grat_prev = grat;
-          pem0 = pem1;
-          dm_k = dm_n;
-          gzk = gzk1;
-        });
+        [&](int s, const D3& v) { level(s + 1, v, F_{}, F_{}); });
+    level(nk - 1, D3{0.0, __ldg(gz + nk * sk), __ldg(pt + (nk - 1) * sk)}, F_{}, T_{});
     // interface nk: pp = (dd[nk-1] - pp[nk-1]) / bet[nk-1], dd[nk-1] = 3*pe[nk-1]
     const double dd_prev = 3.0 * pe_prev;
-    AT(S0, nk) = ar.div((nk == 1) ? dd_prev : dd_prev - pp_prev, bet_prev);
+    AT(S0, nk) = ar.div(dd_prev - pp_prev, bet_prev);
   }
 
   // ---- pass B (backward): riem_pp_bwd, then aa (riem_w_fwd) -------------
@@ -149,7 +165,8 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   {
     double ppn = AT(S0, nk);
     double gzn = __ldg(gz + (nk - 1) * sk);
-    double dz_n = ar.div(__ldg(gz + nk * sk) - gzn, grav);  // dz(nk-1)
+    const double rgrav = ar.rcp(grav);
+    double dz_n = ar.div_r(__ldg(gz + nk * sk) - gzn, grav, rgrav);  // dz(nk-1)
     S1[nk * s1] = ar.div(t1g, dz_n) * (pf[nk * sp] + ppn);   // aa(nk)
     pipelined<PF, D3>(
         nk - 1,
@@ -160,7 +177,7 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
           const int k = nk - 1 - s;
           const double ppk = AT(S0, k) - v.z * ppn;
           AT(S0, k) = ppk;
-          const double dz_k = ar.div(gzn - v.x, grav);               // dz(k-1)
+          const double dz_k = ar.div_r(gzn - v.x, grav, rgrav);      // dz(k-1)
           S1[k * s1] = ar.div(t1g, dz_k + dz_n) * (v.y + ppk);      // aa(k) = t1g/(dz(k-1)+dz(k))*(pem+pp)
           dz_n = dz_k;
           ppn = ppk;
@@ -169,31 +186,38 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   }
 
   // ---- pass C (forward): riem_w_sweep (w2 replaces pp level by level) ----
+  // (levels 0 and nk-1 peeled: their statements differ)
   const double ws = a.ws(i, j, 0);
   {
-    double bw = 0.0, w2p = 0.0, aal = S1[0];
-    pipelined<PF, D3>(
-        nk, [&](int l) { return D3{__ldg(dm + l * sk), __ldg(w + l * sk), S1[(l + 1) * s1]}; },
-        [&](int l, const D3& v) {
-          const double dml = v.x, wl = v.y;
-          const double aan = v.z;  // aa(l+1); aa(l) carried from the previous level
-          double w2l;
-          if (l == 0) {
-            bw = dml - aan;
-            w2l = ar.div(dml * wl + dt * AT(S0, 1), bw);
-          } else {
-            const double gw = ar.div(aal, bw);
-            bw = dml - (aal + aan + aal * gw);
-            if (l < nk - 1)
-              w2l = ar.div(dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aal * w2p, bw);
-            else
-              w2l = ar.div(dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aan * ws - aal * w2p, bw);
-            S1[l * s1] = gw;  // aa(l) no longer needed
-          }
-          AT(S0, l) = w2l;  // pp(l) no longer needed
-          w2p = w2l;
-          aal = aan;
-        });
+    double bw = 0.0, w2p = 0.0, aal = S1[0], rbw = 0.0;
+    auto level = [&](int l, const D3& v, auto first, auto last) {
+      const double dml = v.x, wl = v.y;
+      const double aan = v.z;  // aa(l+1); aa(l) carried from the previous level
+      double w2l;
+      if constexpr (decltype(first)::value) {
+        bw = dml - aan;
+        rbw = ar.rcp(bw);
+        w2l = ar.div_r(dml * wl + dt * AT(S0, 1), bw, rbw);
+      } else {
+        const double gw = ar.div_r(aal, bw, rbw);
+        bw = dml - (aal + aan + aal * gw);
+        rbw = ar.rcp(bw);
+        if constexpr (decltype(last)::value)
+          w2l = ar.div_r(dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aan * ws - aal * w2p, bw, rbw);
+        else
+          w2l = ar.div_r(dml * wl + dt * (AT(S0, l + 1) - AT(S0, l)) - aal * w2p, bw, rbw);
+        S1[l * s1] = gw;  // aa(l) no longer needed
+      }
+      AT(S0, l) = w2l;  // pp(l) no longer needed
+      w2p = w2l;
+      aal = aan;
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    auto ld = [&](int l) { return D3{__ldg(dm + l * sk), __ldg(w + l * sk), S1[(l + 1) * s1]}; };
+    level(0, ld(0), T_{}, F_{});
+    pipelined<PF, D3>(nk - 2, [&](int s) { return ld(s + 1); }, [&](int s, const D3& v) { level(s + 1, v, F_{}, F_{}); });
+    level(nk - 1, ld(nk - 1), F_{}, T_{});
   }
 
   // ---- pass D (backward): riem_w_back ----------------------------------
@@ -216,12 +240,13 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   // ---- pass E (forward): riem_pe, riem_out (pem recomputed in order) -----
   {
     double pe2 = 0.0, pem = ptop;
+    const double rdt = ar.rcp(dt);
     pf[0] = pe2 + pem;
     pipelined<PF, D2>(
         nk, [&](int s) { return D2{__ldg(dm + s * sk), __ldg(w + s * sk)}; },  // k = s+1: layer k-1
         [&](int s, const D2& v) {
           const int k = s + 1;
-          pe2 = pe2 + ar.div(v.x * (AT(S0, k - 1) - v.y), dt);
+          pe2 = pe2 + ar.div_r(v.x * (AT(S0, k - 1) - v.y), dt, rdt);
           pem = pem + v.x;
           AT(S0, k - 1) = pe2;  // pe2(k) (w2(k-1) consumed)
           pf[k * sp] = pe2 + pem;
