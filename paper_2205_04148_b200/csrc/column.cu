@@ -64,7 +64,8 @@ struct D1 { double x; };
 struct D2 { double x, y; };
 struct D3 { double x, y, z; };
 
-constexpr int PF = 4;   // prefetch distance (levels), riem
+constexpr int PF = 4;   // prefetch distance (levels), riem passes with long bodies (A, C)
+constexpr int PFS = 12; // riem passes with short bodies (B, D, E, F): L2-resident staging reads
 constexpr int PFR = 8;  // remap: short per-level bodies need a deeper ring
 
 // Statement-for-statement restatement of templates.riem_stencils for one
@@ -168,7 +169,7 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
     const double rgrav = ar.rcp(grav);
     double dz_n = ar.div_r(__ldg(gz + nk * sk) - gzn, grav, rgrav);  // dz(nk-1)
     S1[nk * s1] = ar.div(t1g, dz_n) * (pf[nk * sp] + ppn);   // aa(nk)
-    pipelined<PF, D3>(
+    pipelined<PFS, D3>(
         nk - 1,
         [&](int s) {  // gz(k-1), pem(k), gam(k)
           return D3{__ldg(gz + (nk - 2 - s) * sk), pf[(nk - 1 - s) * sp], S1[(nk - 1 - s) * s1]};
@@ -226,7 +227,7 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
     double* wo = a.has_wout ? a.wout.ptr(i, j, 0) : nullptr;
     const int64_t so = a.wout.sk;
     if (wo) wo[(nk - 1) * so] = w2n;
-    pipelined<PF, D1>(
+    pipelined<PFS, D1>(
         nk - 1, [&](int s) { return D1{S1[(nk - 1 - s) * s1]}; },  // l = nk-2-s: gw(l+1)
         [&](int s, const D1& v) {
           const int l = nk - 2 - s;
@@ -242,7 +243,7 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
     double pe2 = 0.0, pem = ptop;
     const double rdt = ar.rcp(dt);
     pf[0] = pe2 + pem;
-    pipelined<PF, D2>(
+    pipelined<PFS, D2>(
         nk, [&](int s) { return D2{__ldg(dm + s * sk), __ldg(w + s * sk)}; },  // k = s+1: layer k-1
         [&](int s, const D2& v) {
           const int k = s + 1;
@@ -257,7 +258,7 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   {
     double gzn = __ldg(gz + nk * sk);
     go[nk * sg] = gzn;
-    pipelined<PF, D3>(
+    pipelined<PFS, D3>(
         nk,
         [&](int s) {
           const int l = nk - 1 - s;
