@@ -32,8 +32,8 @@ namespace {
 constexpr int SEG = 4;
 // threads per CTA / CTAs per SM by tile height: 32x16 tiles run one CTA of 11
 // warps per SM, 32x8 tiles two CTAs of 8 warps (<= 128 registers per thread)
-template <int TJ> constexpr int nt_of() { return TJ >= 16 ? 352 : 256; }
-template <int TJ> constexpr int cps_of() { return TJ >= 16 ? 1 : 2; }
+template <int TI, int TJ> constexpr int nt_of() { return TI * TJ >= 512 ? 352 : 256; }
+template <int TI, int TJ> constexpr int cps_of() { return TI * TJ >= 512 ? 1 : 2; }
 
 __host__ __device__ constexpr int a16(int n) { return (n + 15) / 16 * 16; }
 
@@ -74,7 +74,7 @@ struct DtLayout {
 };
 
 template <int TI, int TJ>
-__global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_transport_kernel(const __grid_constant__ DswTpArgs a) {
+__global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transport_kernel(const __grid_constant__ DswTpArgs a) {
   using L = DtLayout<TI, TJ>;
   extern __shared__ __align__(128) double smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::total);  // [0],[1] level stages, [2] metrics
@@ -130,9 +130,9 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_transport_kerne
   if (k1 > k0) mbar_wait(&bar[2], 0);
 
   constexpr int NSEG = TI / SEG;
-  static_assert((TI + 6) * (TJ / SEG) + (TJ + 6) * (TI / SEG) <= nt_of<TJ>(), "one phase-A item per thread");
+  static_assert((TI + 6) * (TJ / SEG) + (TJ + 6) * (TI / SEG) <= nt_of<TI, TJ>(), "one phase-A item per thread");
   constexpr int NX2 = TJ * NSEG, NY2 = TI * (TJ / SEG);
-  static_assert(NX2 + NY2 <= nt_of<TJ>(), "one item per thread in phase B");
+  static_assert(NX2 + NY2 <= nt_of<TI, TJ>(), "one item per thread in phase B");
   // phase-B y threads own a column segment for the whole CTA (as the tracer)
   const bool yth = tid >= NX2 && tid < NX2 + NY2;
   const int ci2 = yth ? (tid - NX2) % TI : 0;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_transport_kerne
   const int gi2 = gi0 + ci2;
   // phase-A worker slot: the y threads (which also write the pending cell
   // updates in phase A) take items only after every other thread has one
-  const int wslot = tid < NX2 ? tid : (yth ? nt_of<TJ>() - NY2 + (tid - NX2) : tid - NY2);
+  const int wslot = tid < NX2 ? tid : (yth ? nt_of<TI, TJ>() - NY2 + (tid - NX2) : tid - NY2);
   double ra[SEG];
 #pragma unroll
   for (int u = 0; u < SEG; ++u) {
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_transport_kerne
   }
   double fy[SEG + 1], dpa[SEG], dpb[SEG];
   int pend_k = -1, pend_q = 0;  // step whose cell update is pending
-  constexpr int NT = nt_of<TJ>(), NACC = (6 * TI * TJ + NT - 1) / NT;
+  constexpr int NT = nt_of<TI, TJ>(), NACC = (6 * TI * TJ + NT - 1) / NT;
   double accv[NACC];  // this thread's accumulator cells of the current level
   const int64_t sj = a.sj, sk = a.sk;
 
@@ -357,9 +357,9 @@ int launch_dsw_transport(const DswTpArgs& a0, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // ~4 waves of one CTA per SM, at least 2 levels per CTA so the prefetch overlaps
   (void)sms;
-  a.kchunk = level_chunk(tiles, a.nk, cps_of<DT_TJ>());
+  a.kchunk = level_chunk(tiles, a.nk, cps_of<DT_TI, DT_TJ>());
   dim3 grid(cdiv(a.ni, DT_TI), cdiv(a.nj, DT_TJ), cdiv(a.nk, a.kchunk));
-  dsw_transport_kernel<DT_TI, DT_TJ><<<grid, nt_of<DT_TJ>(), L::bytes, st>>>(a);
+  dsw_transport_kernel<DT_TI, DT_TJ><<<grid, nt_of<DT_TI, DT_TJ>(), L::bytes, st>>>(a);
   return check_launch("d_sw transport");
 }
 
