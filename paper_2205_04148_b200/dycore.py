@@ -127,6 +127,62 @@ class Dycore:
             st.copy_(self._window(self.cur[n]))
             dst.copy_(st, non_blocking=True)
 
+    def _io_stages(self, names) -> tuple[dict, dict]:
+        if getattr(self, "_io", None) is None or set(self._io[0]) != set(names):
+            h, c = self.cfg.halo, self.cfg
+            shape = (c.ni + 2 * h, c.nj + 2 * h, c.nk + 1)
+            mk = lambda: {n: torch.empty(shape, dtype=torch.float64, device=self.device) for n in names}
+            self._io = (mk(), mk())
+        return self._io
+
+    def step_host(self, h_in: dict[str, torch.Tensor], h_out: dict[str, torch.Tensor],
+                  copy_stream: torch.cuda.Stream | None = None) -> None:
+        """One timestep from pinned host state to pinned host state, with the
+        transfers overlapped with the compute they do not feed: the tracers'
+        host->device copies run during the acoustic substeps (first needed by
+        tracer_2d), the dynamics fields' device->host copies during the tracer
+        advection and remapping (their values are final after the last
+        substep), the tracers' during remapping.  Copies run on ``copy_stream``; the current stream waits for
+        them before returning, so an event recorded afterwards covers the
+        whole step."""
+        comp = torch.cuda.current_stream()
+        cs = copy_stream or getattr(self, "_copy_stream", None)
+        if cs is None:
+            cs = self._copy_stream = torch.cuda.Stream()
+        trc = [n for n in h_in if n in self.cfg.tracer_names()]
+        dyn = [n for n in h_in if n not in trc]
+        sin, sout = self._io_stages(list(h_in))
+        cs.wait_stream(comp)  # staging buffers are free (previous step done)
+        with torch.cuda.stream(cs):
+            for n in dyn:
+                sin[n].copy_(h_in[n], non_blocking=True)
+            e_dyn = cs.record_event()
+            for n in trc:
+                sin[n].copy_(h_in[n], non_blocking=True)
+            e_trc = cs.record_event()
+        comp.wait_event(e_dyn)
+        for n in dyn:
+            self._window(self.cur[n]).copy_(sin[n])
+        def out(names):  # device transpose on the compute stream, download on the copy stream
+            for n in names:
+                sout[n].copy_(self._window(self.cur[n]))
+            e_out = comp.record_event()
+            with torch.cuda.stream(cs):
+                cs.wait_event(e_out)
+                for n in names:
+                    h_out[n].copy_(sout[n], non_blocking=True)
+
+        for names in self.phases(after_tracers=(lambda: out(trc)) if trc else None):
+            if trc and trc[0] in names:
+                comp.wait_event(e_trc)
+                for n in trc:
+                    self._window(self.cur[n]).copy_(sin[n])
+                out(dyn)
+            self.halo.update(names)
+        if not trc:
+            out(dyn)
+        comp.wait_stream(cs)
+
     # -- launch helpers -----------------------------------------------------
 
     def f(self, name: str) -> _lib.Field:
@@ -195,7 +251,7 @@ class Dycore:
         fields.append(self.s("remap_gam"))
         self.launch("remap_tracers", "fv3b_remap_profile", fields, [], self.dom_ifaces)
 
-    def phases(self):
+    def phases(self, after_tracers=None):
         """One timestep as a generator: enqueues the programs on the current
         stream and yields, at each halo-update point, the fields to refresh
         (the caller performs the update; a decomposed run exchanges them
@@ -214,6 +270,8 @@ class Dycore:
             self.p_grad_d()
         yield cfg.tracer_names() + list(ACCUM)
         self.tracer_2d()
+        if after_tracers is not None:  # the advected tracers are final (remap only reads them)
+            after_tracers()
         self.remap()
         self._parity ^= 1  # the tracers swap buffers once per step
 

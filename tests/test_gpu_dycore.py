@@ -82,3 +82,29 @@ def test_checkpoint_restart_is_bitwise(tmp_path):
     for n in ["u", "v", "w", "delp", "pt", "gz", "q0", "q5_a3"]:
         top = cfg.nk + 1 if n in INTERFACE else cfg.nk
         assert np.array_equal(a.download([n])[n][h:-h, h:-h, :top], b.download([n])[n][h:-h, h:-h, :top]), n
+
+
+def test_step_host_overlapped_io_matches_step():
+    """Dycore.step_host (overlapped pinned-host transfers) == load + step + store."""
+    import torch
+
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.dycore import Dycore
+    from paper_2205_04148_b200.state import initial_state
+
+    cfg = RunConfig(ni=32, nj=24, nk=10, n_split=3, dt_atmos=45.0)
+    st = initial_state(cfg)
+    a, b = Dycore(cfg, st), Dycore(cfg, st)
+    hin, oa, ob = a.host_buffers(), a.host_buffers(), b.host_buffers()
+    for n, t in hin.items():
+        t.copy_(torch.from_numpy(st[n]))
+    for _ in range(2):
+        a.step_host(hin, oa)
+        b.load_host(hin)
+        b.step()
+        b.store_host(ob)
+    torch.cuda.synchronize()
+    h = cfg.halo
+    for n in hin:
+        top = cfg.nk + 1 if n in INTERFACE else cfg.nk
+        assert torch.equal(oa[n][h:-h, h:-h, :top], ob[n][h:-h, h:-h, :top]), n
