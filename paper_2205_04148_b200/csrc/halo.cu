@@ -26,10 +26,14 @@ struct HaloArgs {
 // minus the interior (the south and north bands of full width, then the west
 // and east bands of the interior rows); source = periodic wrap.
 __global__ void halo_periodic_kernel(const HaloArgs a) {
+  // each thread copies one ring cell on HALO_KU consecutive levels: the
+  // independent loads are issued together (the copy is latency-bound)
+  constexpr int HALO_KU = 8;
   const int W = a.ni + 2 * a.h, h = a.h;
-  const int f = blockIdx.z, k = blockIdx.y;
-  if (k >= a.levels[f]) return;
-  double* o = a.o[f] + (int64_t)k * a.sk;
+  const int f = blockIdx.z, kb = blockIdx.y * HALO_KU;
+  const int nl = min(HALO_KU, a.levels[f] - kb);
+  if (nl <= 0) return;
+  double* o = a.o[f] + (int64_t)kb * a.sk;
   const int nband = W * h;           // one south / north band
   const int nside = h * a.nj;        // one west / east band
   const int n = 2 * nband + 2 * nside;
@@ -45,7 +49,14 @@ __global__ void halo_periodic_kernel(const HaloArgs a) {
       j = r / h;
     }
     const int si = (i + a.ni) % a.ni, sj = (j + a.nj) % a.nj;
-    o[i + (int64_t)j * a.sj] = o[si + (int64_t)sj * a.sj];
+    const int64_t dst = i + (int64_t)j * a.sj, src = si + (int64_t)sj * a.sj;
+    double v[HALO_KU];
+#pragma unroll
+    for (int k = 0; k < HALO_KU; ++k)
+      if (k < nl) v[k] = o[src + k * a.sk];
+#pragma unroll
+    for (int k = 0; k < HALO_KU; ++k)
+      if (k < nl) o[dst + k * a.sk] = v[k];
   }
 }
 
@@ -241,7 +252,7 @@ extern "C" int fv3b_halo_periodic(const fv3b_field* f, int nf, const double* s, 
   int maxl = 1;
   for (int t = 0; t < nf; ++t) maxl = a.levels[t] > maxl ? a.levels[t] : maxl;
   const int ring = 2 * (d->ni + 2 * a.h) * a.h + 2 * a.h * d->nj;
-  dim3 grid(cdiv(ring, 256) < 8 ? cdiv(ring, 256) : 8, maxl, nf);
+  dim3 grid(cdiv(ring, 256) < 16 ? cdiv(ring, 256) : 16, cdiv(maxl, 8), nf);
   halo_periodic_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
   return check_launch("fv3b_halo_periodic");
 }
