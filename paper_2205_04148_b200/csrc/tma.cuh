@@ -52,7 +52,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
-// Box load of (x, y, z) (allocated-element coordinates) into smem.
+// Box load of (x, y, z) (allocated-element coordinates) into smem.  The box's
+// first element must be 16-B aligned in global memory: for fp64 fields x is
+// even (measured on B200: an odd x raises an illegal-instruction fault).
 __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
