@@ -22,8 +22,9 @@
 //  * temporaries are recomputed over the tile halo exactly where the
 //    reference extends them (extents.py:128-164), so outputs are bitwise the
 //    interpreter's.
-// The tracer variant walks (level, tracer) steps so the shared Courant
-// numbers / fluxes / dp1 are fetched once per level for all tracers.
+// tracer_2d (tracer2_kernel) walks (level, group of TG tracers) steps so the
+// shared Courant numbers / fluxes / dp1 are fetched once per level for all
+// tracers and every barrier interval carries TG tracers' work.
 #include "common.cuh"
 #include "ppm.cuh"
 #include "tma.cuh"
@@ -35,7 +36,7 @@ constexpr int SEG = 4;  // cells per sliding-window segment
 // threads per CTA / CTAs per SM by tile height (>= phase-A items): 32x16
 // tiles one CTA of 11 warps, 32x8 tiles two CTAs of 8 warps
 template <int TJ> constexpr int nt_of() { return TJ >= 16 ? 352 : 256; }
-template <int TJ, bool MASS> constexpr int cps_of() { return TJ >= 16 ? (MASS ? 1 : 2) : 2; }
+template <int TJ> constexpr int cps_of() { return 2; }
 
 struct TpArgs {
   CUtensorMap q[NQMAX];
@@ -90,8 +91,9 @@ struct TpLayout {
   static constexpr uint32_t tx_area = QW * QH * 8;
 };
 
-template <int TI, int TJ, bool MASS>
-__global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(const __grid_constant__ TpArgs a) {
+template <int TI, int TJ>
+__global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ>())) tp_kernel(const __grid_constant__ TpArgs a) {
+  constexpr bool MASS = false;  // tracer_2d: tracer2_kernel
   using L = TpLayout<TI, TJ, MASS>;
   extern __shared__ __align__(128) double smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::total);  // [0],[1] step stages, [2] area
@@ -118,12 +120,6 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(c
       tma_load3(sh + L::n_x, &a.xfx, xx, yq, k, &bar[b]);
       tma_load3(sh + 2 * L::n_x, &a.cry, xq, yy, k, &bar[b]);
       tma_load3(sh + 2 * L::n_x + L::n_y, &a.yfx, xq, yy, k, &bar[b]);
-      if (MASS) {
-        double* m = sh + 2 * L::n_x + 2 * L::n_y;
-        tma_load3(m, &a.mfx, xx, yy, k, &bar[b]);
-        tma_load3(m + L::n_mx, &a.mfy, xx, yy, k, &bar[b]);
-        tma_load3(m + L::n_mx + L::n_my, &a.dp1, xx, yy, k, &bar[b]);
-      }
     }
   };
 
@@ -145,7 +141,6 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(c
   double* sfx2 = smem + L::o_fx2;          // XW, origin (0, 0)
   double* sfy2 = smem + L::o_fy2;          // TI, origin (0, 0)
   double* sfx = smem + L::o_fx;            // XW, origin (0, 0)
-  double* sdp2 = smem + L::o_dp2;          // TI, origin (0, 0)
   if (nsteps > 0) mbar_wait(&bar[2], 0);
 
   constexpr int NSEG = TI / SEG;
@@ -168,7 +163,7 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(c
     const int gj = gj0 + jb2 + u;
     ra[u] = (yth && gi2 < a.ni && gj < a.nj) ? a.rarea[gi2 + (int64_t)gj * a.sj] : 0.0;
   }
-  double fy[SEG + 1], qc[SEG], dpa[SEG], dpb[SEG];
+  double fy[SEG + 1], qc[SEG];
   int pend_k = -1, pend_t = 0;  // step whose output is pending
 
   auto write_pending = [&]() {
@@ -180,10 +175,7 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(c
       if (gi2 < a.ni && gj < a.nj) {
         const int64_t off = gi2 + (int64_t)gj * a.sj + (int64_t)pend_k * a.sk;
         const double div = (sfx[j * L::XW + ci2] - sfx[j * L::XW + ci2 + 1] + fy[u] - fy[u + 1]) * ra[u];
-        if (MASS)
-          qo[off] = (qc[u] * dpa[u] + div) / dpb[u];
-        else
-          qo[off] = qc[u] + div;
+        qo[off] = qc[u] + div;
       }
     }
   };
@@ -202,24 +194,12 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(c
     const double* sxfx = sh + L::n_x;                                          // XW, origin (0, -3)
     const double* scry = sh + 2 * L::n_x;                                      // YW, origin (-4, 0)
     const double* syfx = sh + 2 * L::n_x + L::n_y;                             // YW, origin (-4, 0)
-    const double* smfx = sh + 2 * L::n_x + 2 * L::n_y;                         // XW, origin (0, 0)
-    const double* smfy = smfx + L::n_mx;                                       // TI, origin (0, 0)
-    const double* sdp1 = smfy + L::n_my;                                       // TI, origin (0, 0)
     auto Q = [&](int i, int j) { return sq + (j + 3) * L::QW + (i + 4); };
     auto CX = [&](const double* p, int i, int j) { return p + (j + 3) * L::XW + i; };
     auto CY = [&](const double* p, int i, int j) { return p + j * L::YW + (i + 4); };
 
-    // ---- phase A: previous step's output; dp2; yppm(q)/xppm(q) ----------
+    // ---- phase A: previous step's output; yppm(q)/xppm(q) ---------------
     write_pending();
-    if (MASS && t == 0) {
-      // dp2 = dp1 + (mfx - mfx[1,0,0] + mfy - mfy[0,1,0]) * rarea      (tracer_dp)
-      for (int e = tid; e < TI * TJ; e += blockDim.x) {
-        const int li = e % TI, lj = e / TI;
-        const double rr = (gi0 + li < a.ni && gj0 + lj < a.nj) ? a.rarea[(gi0 + li) + (int64_t)(gj0 + lj) * a.sj] : 0.0;
-        sdp2[lj * TI + li] = sdp1[lj * TI + li] + (smfx[lj * L::XW + li] - smfx[lj * L::XW + li + 1] +
-                                                   smfy[lj * TI + li] - smfy[(lj + 1) * TI + li]) * rr;
-      }
-    }
     // Y items: consecutive threads own consecutive columns; X items:
     // consecutive threads own consecutive rows (bank-conflict-free, see QW).
     {
@@ -275,7 +255,7 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(c
       for (int u = 0; u < SEG + 1; ++u) {
         if (u < nf) {
           const int i = ib + u;
-          const double w = MASS ? smfx[rj * L::XW + i] : *CX(sxfx, i, rj);
+          const double w = *CX(sxfx, i, rj);
           sfx[rj * L::XW + i] = 0.5 * (f[u] + sfx2[rj * L::XW + i]) * w;
         }
       }
@@ -284,16 +264,12 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(c
 #pragma unroll
       for (int u = 0; u < SEG + 1; ++u) {
         const int j = jb2 + u;
-        const double w = MASS ? smfy[j * TI + ci2] : *CY(syfx, ci2, j);
+        const double w = *CY(syfx, ci2, j);
         fy[u] = 0.5 * (fy[u] + sfy2[j * TI + ci2]) * w;
       }
 #pragma unroll
       for (int u = 0; u < SEG; ++u) {
         qc[u] = *Q(ci2, jb2 + u);
-        if (MASS) {
-          dpa[u] = sdp1[(jb2 + u) * TI + ci2];
-          dpb[u] = sdp2[(jb2 + u) * TI + ci2];
-        }
       }
     }
     pend_k = k;
@@ -303,12 +279,260 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ, MASS>())) tp_kernel(c
   write_pending();
 }
 
-template <int TI, int TJ, bool MASS>
-static int launch_tp(const TpArgs& a0, cudaStream_t st) {
-  using L = TpLayout<TI, TJ, MASS>;
+// ---------------------------------------------------------------------------
+// tracer_2d, group schedule. The tracers of one level are processed TG at a
+// time; per group two barrier intervals:
+//   A: cell updates of the previous group (one cell per thread: dp2 from
+//      registers, q' written straight to HBM) + phase A of all TG tracers;
+//   B: phase B of all TG tracers (fluxes fx, fy to shared memory).
+// Twice the work per barrier of tp_kernel, every thread busy in phase B, and
+// the mass-flux divergence dp2 computed once per level in registers.
+constexpr int TG = 2;
+
+template <int TI, int TJ>
+struct Tr2Layout {
+  using B = TpLayout<TI, TJ, true>;  // tile shapes and TMA boxes as tp_kernel
+  static constexpr int NQB = 3;      // q stages (group s in stage s % 3)
+  // per-tracer intermediates: qi, qj, fx2, fy2, fx, fy
+  static constexpr int s_qi = 0, s_qj = B::n_qi, s_fx2 = s_qj + B::n_qj, s_fy2 = s_fx2 + B::n_fx,
+                       s_fx = s_fy2 + B::n_fy, s_fy = s_fx + B::n_fx, n_set = s_fy + B::n_fy;
+  static constexpr int o_q = 0;
+  static constexpr int o_sh = o_q + NQB * TG * B::n_q;  // 2 per-level stages
+  static constexpr int o_area = o_sh + 2 * B::n_shared;
+  static constexpr int o_set = o_area + B::n_q;
+  static constexpr int total = o_set + TG * n_set;
+  static constexpr size_t bytes = total * sizeof(double) + 64;
+  static_assert(2 * bytes + 2048 <= 228 * 1024, "two CTAs per SM");
+};
+
+template <int TI, int TJ>
+__global__ void __launch_bounds__(TI * TJ, 2) tracer2_kernel(const __grid_constant__ TpArgs a) {
+  using B = TpLayout<TI, TJ, true>;
+  using L = Tr2Layout<TI, TJ>;
+  constexpr int NT = TI * TJ;
+  extern __shared__ __align__(128) double smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::total);  // [0..2] q stages, [3] area
+  const int tid = threadIdx.x;
+  const int gi0 = blockIdx.x * TI, gj0 = blockIdx.y * TJ;
+  const int k0 = blockIdx.z * a.kchunk;
+  const int k1 = min(a.nk, k0 + a.kchunk);
+  const int ng = (a.nq + TG - 1) / TG;
+  const int nsteps = (k1 - k0) * ng;
+  const int xq = a.i0 + gi0 - 4, yq = a.j0 + gj0 - 3;
+  const int xx = a.i0 + gi0, yy = a.j0 + gj0;
+  const double p1 = a.p1, p2 = a.p2;
+  auto qstage = [&](int s, int c) { return smem + L::o_q + ((s % L::NQB) * TG + c) * B::n_q; };
+  auto shstage = [&](int lv) { return smem + L::o_sh + (lv & 1) * B::n_shared; };
+
+  auto issue = [&](int s) {  // single thread
+    const int lv = s / ng, g = s % ng, k = k0 + lv;
+    const int t0 = g * TG, cnt = min(TG, a.nq - t0);
+    uint64_t* mb = &bar[s % L::NQB];
+    mbar_expect_tx(mb, cnt * B::tx_q + (g == 0 ? B::tx_shared : 0));
+    for (int c = 0; c < cnt; ++c) tma_load3(qstage(s, c), &a.q[t0 + c], xq, yq, k, mb);
+    if (g == 0) {
+      double* sh = shstage(lv);
+      tma_load3(sh, &a.crx, xx, yq, k, mb);
+      tma_load3(sh + B::n_x, &a.xfx, xx, yq, k, mb);
+      tma_load3(sh + 2 * B::n_x, &a.cry, xq, yy, k, mb);
+      tma_load3(sh + 2 * B::n_x + B::n_y, &a.yfx, xq, yy, k, mb);
+      double* m = sh + 2 * B::n_x + 2 * B::n_y;
+      tma_load3(m, &a.mfx, xx, yy, k, mb);
+      tma_load3(m + B::n_mx, &a.mfy, xx, yy, k, mb);
+      tma_load3(m + B::n_mx + B::n_my, &a.dp1, xx, yy, k, mb);
+    }
+  };
+
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0 && nsteps > 0) {
+    mbar_expect_tx(&bar[3], B::tx_area);
+    tma_load3(smem + L::o_area, &a.area, xq, yq, 0, &bar[3]);
+    issue(0);
+  }
+  if (nsteps <= 0) return;
+  const double* sarea = smem + L::o_area;  // QW, origin (-4, -3)
+  mbar_wait(&bar[3], 0);
+
+  // cell owned by this thread in the update pass
+  const int li = tid % TI, lj = tid / TI;
+  const bool live = gi0 + li < a.ni && gj0 + lj < a.nj;
+  const int64_t coff = (gi0 + li) + (int64_t)(gj0 + lj) * a.sj;
+  const double rr = live ? a.rarea[coff] : 0.0;
+  double dp1c = 0.0, dp2c = 0.0;
+  int dp_lv = -1;
+
+  auto update = [&](int s) {  // q' of group s, one cell per thread
+    const int lv = s / ng, g = s % ng;
+    const int t0 = g * TG, cnt = min(TG, a.nq - t0);
+    if (lv != dp_lv) {
+      // dp2 = dp1 + (mfx - mfx[1,0,0] + mfy - mfy[0,1,0]) * rarea      (tracer_dp)
+      const double* smfx = shstage(lv) + 2 * B::n_x + 2 * B::n_y;
+      const double* smfy = smfx + B::n_mx;
+      const double* sdp1 = smfy + B::n_my;
+      dp1c = sdp1[lj * TI + li];
+      dp2c = dp1c + (smfx[lj * B::XW + li] - smfx[lj * B::XW + li + 1] + smfy[lj * TI + li] -
+                     smfy[(lj + 1) * TI + li]) * rr;
+      dp_lv = lv;
+    }
+    if (!live) return;
+    const int64_t off = coff + (int64_t)(k0 + lv) * a.sk;
+#pragma unroll
+    for (int c = 0; c < TG; ++c) {
+      if (c < cnt) {
+        const double* st = smem + L::o_set + c * L::n_set;
+        const double* fx = st + L::s_fx;  // XW, origin (0, 0)
+        const double* fy = st + L::s_fy;  // TI, origin (0, 0)
+        const double div = (fx[lj * B::XW + li] - fx[lj * B::XW + li + 1] + fy[lj * TI + li] -
+                            fy[(lj + 1) * TI + li]) * rr;
+        const double qc = qstage(s, c)[(lj + 3) * B::QW + li + 4];
+        a.qout[t0 + c][off] = (qc * dp1c + div) / dp2c;
+      }
+    }
+  };
+
+  constexpr int NCY = TI + 6, NSY = TJ / SEG;  // phase-A y columns i in [-3, TI+3)
+  constexpr int NRX = TJ + 6, NSX = TI / SEG;  // phase-A x rows j in [-3, TJ+3)
+  constexpr int NY = NCY * NSY, NX = NRX * NSX;
+  constexpr int NX2 = TJ * NSX, NY2 = TI * NSY;  // phase-B x rows / y columns
+  static_assert(TG * (NX2 + NY2) <= NT, "one phase-B item per thread");
+  // with few tracer groups per level the next level's shared stage may only
+  // be refilled once the previous group's cell updates are done (phase B)
+  const bool early = ng >= 2;
+
+  int lv = 0, g = 0;
+  for (int s = 0; s < nsteps; ++s, (++g == ng ? (g = 0, ++lv) : 0)) {
+    const int cnt = min(TG, a.nq - g * TG);
+    if (early && tid == 0 && s + 1 < nsteps) {
+      fence_async_smem();
+      issue(s + 1);
+    }
+    mbar_wait(&bar[s % L::NQB], (s / L::NQB) & 1);
+    const double* sh = shstage(lv);
+    const double* scrx = sh;                             // XW, origin (0, -3)
+    const double* sxfx = sh + B::n_x;                    // XW, origin (0, -3)
+    const double* scry = sh + 2 * B::n_x;                // YW, origin (-4, 0)
+    const double* syfx = sh + 2 * B::n_x + B::n_y;       // YW, origin (-4, 0)
+    const double* smfx = sh + 2 * B::n_x + 2 * B::n_y;   // XW, origin (0, 0)
+    const double* smfy = smfx + B::n_mx;                 // TI, origin (0, 0)
+    auto CX = [&](const double* p, int i, int j) { return p + (j + 3) * B::XW + i; };
+    auto CY = [&](const double* p, int i, int j) { return p + j * B::YW + (i + 4); };
+
+    // ---- interval A: previous group's cell updates; phase A ------------------
+    if (s > 0) update(s - 1);
+    // y items of every tracer first, then x items (warps stay on one path)
+    for (int item = tid; item < cnt * (NY + NX); item += NT) {
+      if (item < cnt * NY) {
+        const int c = item / NY, it = item % NY;
+        const double* sq = qstage(s, c);
+        double* st = smem + L::o_set + c * L::n_set;
+        const int ci = it % NCY - 3, jb = (it / NCY) * SEG;
+        double f[SEG + 1];
+        ppm_line<SEG + 1>(sq + (jb + 3) * B::QW + ci + 4, B::QW, CY(scry, ci, jb), B::YW, p1, p2, f);
+#pragma unroll
+        for (int u = 0; u < SEG; ++u) {
+          const int j = jb + u;
+          const double ar = sarea[(j + 3) * B::QW + ci + 4];
+          const double y0 = *CY(syfx, ci, j), y1 = *CY(syfx, ci, j + 1);
+          st[L::s_qi + j * B::QW + ci + 4] = (sq[(j + 3) * B::QW + ci + 4] * ar + f[u] * y0 - f[u + 1] * y1) /
+                                             (ar + y0 - y1);
+        }
+        if (ci >= 0 && ci < TI) {
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) st[L::s_fy2 + (jb + u) * TI + ci] = f[u];
+          if (jb + SEG == TJ) st[L::s_fy2 + TJ * TI + ci] = f[SEG];
+        }
+      } else {
+        const int x = item - cnt * NY;
+        const int c = x / NX, it = x % NX;
+        const double* sq = qstage(s, c);
+        double* st = smem + L::o_set + c * L::n_set;
+        const int rj = it % NRX - 3, ib = (it / NRX) * SEG;
+        double f[SEG + 1];
+        ppm_line<SEG + 1>(sq + (rj + 3) * B::QW + ib + 4, 1, CX(scrx, ib, rj), 1, p1, p2, f);
+#pragma unroll
+        for (int u = 0; u < SEG; ++u) {
+          const int i = ib + u;
+          const double ar = sarea[(rj + 3) * B::QW + i + 4];
+          const double x0 = *CX(sxfx, i, rj), x1 = *CX(sxfx, i + 1, rj);
+          st[L::s_qj + (rj + 3) * B::JW + i] = (sq[(rj + 3) * B::QW + i + 4] * ar + f[u] * x0 - f[u + 1] * x1) /
+                                               (ar + x0 - x1);
+        }
+        if (rj >= 0 && rj < TJ) {
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) st[L::s_fx2 + rj * B::XW + ib + u] = f[u];
+          if (ib + SEG == TI) st[L::s_fx2 + rj * B::XW + TI] = f[SEG];
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- interval B: xppm(qi) -> fx, yppm(qj) -> fy (mass-flux weighted) -----
+    if (!early && tid == 0 && s + 1 < nsteps) {
+      fence_async_smem();
+      issue(s + 1);
+    }
+    if (tid < cnt * NX2) {
+      const int c = tid / NX2, it = tid % NX2;
+      double* st = smem + L::o_set + c * L::n_set;
+      const int rj = it % TJ, ib = (it / TJ) * SEG;
+      double f[SEG + 1];
+      ppm_line<SEG + 1>(st + L::s_qi + rj * B::QW + ib + 4, 1, CX(scrx, ib, rj), 1, p1, p2, f);
+      const int nf = (ib + SEG == TI) ? SEG + 1 : SEG;
+#pragma unroll
+      for (int u = 0; u < SEG + 1; ++u) {
+        if (u < nf) {
+          const int i = ib + u;
+          st[L::s_fx + rj * B::XW + i] = 0.5 * (f[u] + st[L::s_fx2 + rj * B::XW + i]) * smfx[rj * B::XW + i];
+        }
+      }
+    } else if (tid < cnt * NX2 + cnt * NY2) {
+      const int y = tid - cnt * NX2;
+      const int c = y / NY2, it = y % NY2;
+      double* st = smem + L::o_set + c * L::n_set;
+      const int ci = it % TI, jb = (it / TI) * SEG;
+      double f[SEG + 1];
+      ppm_line<SEG + 1>(st + L::s_qj + (jb + 3) * B::JW + ci, B::JW, CY(scry, ci, jb), B::YW, p1, p2, f);
+      const int nf = (jb + SEG == TJ) ? SEG + 1 : SEG;
+#pragma unroll
+      for (int u = 0; u < SEG + 1; ++u) {
+        if (u < nf) {
+          const int j = jb + u;
+          st[L::s_fy + j * TI + ci] = 0.5 * (f[u] + st[L::s_fy2 + j * TI + ci]) * smfy[j * TI + ci];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  update(nsteps - 1);
+}
+
+template <int TI, int TJ>
+static int launch_tracer2(const TpArgs& a0, cudaStream_t st) {
+  using L = Tr2Layout<TI, TJ>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(tp_kernel<TI, TJ, MASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes) !=
+    if (cudaFuncSetAttribute(tracer2_kernel<TI, TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes) !=
+        cudaSuccess)
+      return check_launch("tracer_2d smem attribute");
+    attr = true;
+  }
+  TpArgs a = a0;
+  a.kchunk = level_chunk(cdiv(a.ni, TI) * cdiv(a.nj, TJ), a.nk, 2);
+  dim3 grid(cdiv(a.ni, TI), cdiv(a.nj, TJ), cdiv(a.nk, a.kchunk));
+  tracer2_kernel<TI, TJ><<<grid, TI * TJ, L::bytes, st>>>(a);
+  return check_launch("tracer_2d");
+}
+
+template <int TI, int TJ>
+static int launch_tp(const TpArgs& a0, cudaStream_t st) {
+  using L = TpLayout<TI, TJ, false>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(tp_kernel<TI, TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes) !=
         cudaSuccess)
       return check_launch("tp smem attribute");
     attr = true;
@@ -323,10 +547,10 @@ static int launch_tp(const TpArgs& a0, cudaStream_t st) {
   }
   // ~4 waves of one CTA per SM; at least 2 levels per CTA so the pipeline overlaps
   (void)sms;
-  a.kchunk = level_chunk(tiles, a.nk, cps_of<TJ, MASS>());
+  a.kchunk = level_chunk(tiles, a.nk, cps_of<TJ>());
   dim3 grid(cdiv(a.ni, TI), cdiv(a.nj, TJ), cdiv(a.nk, a.kchunk));
-  tp_kernel<TI, TJ, MASS><<<grid, nt_of<TJ>(), L::bytes, st>>>(a);
-  return check_launch(MASS ? "tracer_2d" : "fv_tp_2d");
+  tp_kernel<TI, TJ><<<grid, nt_of<TJ>(), L::bytes, st>>>(a);
+  return check_launch("fv_tp_2d");
 }
 
 // Build the tensor maps for one call; boxes match TpLayout.
@@ -400,7 +624,7 @@ extern "C" int fv3b_fv_tp_2d(const fv3b_field* f, int nf, const double* s, int n
   a.ni = d->ni; a.nj = d->nj; a.nk = d->nk;
   a.p1 = s[0];
   a.p2 = s[1];
-  return launch_tp<TP_TI, TP_TJ, false>(a, (cudaStream_t)stream);
+  return launch_tp<TP_TI, TP_TJ>(a, (cudaStream_t)stream);
 }
 
 static constexpr int TR_TI = 32, TR_TJ = 8;
@@ -446,5 +670,5 @@ extern "C" int fv3b_tracer_2d(const fv3b_field* f, int nf, const double* s, int 
   a.ni = d->ni; a.nj = d->nj; a.nk = d->nk;
   a.p1 = s[0];
   a.p2 = s[1];
-  return launch_tp<TR_TI, TR_TJ, true>(a, (cudaStream_t)stream);
+  return launch_tracer2<TR_TI, TR_TJ>(a, (cudaStream_t)stream);
 }
