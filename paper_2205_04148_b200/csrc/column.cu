@@ -64,9 +64,14 @@ struct D1 { double x; };
 struct D2 { double x, y; };
 struct D3 { double x, y, z; };
 
-constexpr int PF = 4;   // prefetch distance (levels), riem passes with long bodies (A, C)
-constexpr int PFS = 12; // riem passes with short bodies (B, D, E, F): L2-resident staging reads
-constexpr int PFR = 8;  // remap: short per-level bodies need a deeper ring
+#ifndef FV3B_PF  // (overridable for tuning sweeps, tools/build_variant.py)
+#define FV3B_PF 4
+#define FV3B_PFS 12
+#define FV3B_PFR 8
+#endif
+constexpr int PF = FV3B_PF;    // prefetch distance (levels), riem passes with long bodies (A, C)
+constexpr int PFS = FV3B_PFS;  // riem passes with short bodies (B, D, E, F): L2-resident staging reads
+constexpr int PFR = FV3B_PFR;  // remap: short per-level bodies need a deeper ring
 
 // Statement-for-statement restatement of templates.riem_stencils for one
 // column.  FAST: branch-free divisions/logs (fastdiv.cuh), returns false if
@@ -277,6 +282,12 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   return ar.ok;
 }
 
+#ifdef FV3B_EXACT_NOINLINE
+__device__ __noinline__ void riem_exact(const RiemArgs& a, int i, int j, int c, int NC, double* sm) {
+  riem_column<false>(a, i, j, c, NC, sm);
+}
+#endif
+
 __global__ void __launch_bounds__(NC_MAX) riem_kernel(const RiemArgs a) {
   extern __shared__ double sm[];
   const int c = threadIdx.x, NC = blockDim.x;
@@ -285,7 +296,11 @@ __global__ void __launch_bounds__(NC_MAX) riem_kernel(const RiemArgs a) {
   const int i = a.ilo + cidx % a.ni_ext;
   const int j = a.jlo + cidx / a.ni_ext;
   // outputs never alias inputs: a failed fast evaluation is simply redone
+#ifdef FV3B_EXACT_NOINLINE
+  if (!riem_column<true>(a, i, j, c, NC, sm)) riem_exact(a, i, j, c, NC, sm);
+#else
   if (!riem_column<true>(a, i, j, c, NC, sm)) riem_column<false>(a, i, j, c, NC, sm);
+#endif
 }
 
 // ---------------------------------------------------------------------------

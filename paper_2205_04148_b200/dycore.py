@@ -127,48 +127,69 @@ class Dycore:
             st.copy_(self._window(self.cur[n]))
             dst.copy_(st, non_blocking=True)
 
-    def _io_stages(self, names) -> tuple[dict, dict]:
-        if getattr(self, "_io", None) is None or set(self._io[0]) != set(names):
+    def _io_stages(self, names, slot: int) -> tuple[dict, dict]:
+        """Device staging for step_host, double-buffered by call parity."""
+        if getattr(self, "_io", None) is None or set(self._io[0][0]) != set(names):
             h, c = self.cfg.halo, self.cfg
             shape = (c.ni + 2 * h, c.nj + 2 * h, c.nk + 1)
             mk = lambda: {n: torch.empty(shape, dtype=torch.float64, device=self.device) for n in names}
-            self._io = (mk(), mk())
-        return self._io
+            self._io = ((mk(), mk()), (mk(), mk()))
+            self._io_free = [[None, None], [None, None]]  # [slot] -> (inputs consumed, outputs downloaded)
+        return self._io[slot]
 
-    def step_host(self, h_in: dict[str, torch.Tensor], h_out: dict[str, torch.Tensor],
-                  copy_stream: torch.cuda.Stream | None = None) -> None:
-        """One timestep from pinned host state to pinned host state, with the
-        transfers overlapped with the compute they do not feed: the tracers'
-        host->device copies run during the acoustic substeps (first needed by
-        tracer_2d), the dynamics fields' device->host copies during the tracer
-        advection and remapping (their values are final after the last
-        substep), the tracers' during remapping.  Copies run on ``copy_stream``; the current stream waits for
-        them before returning, so an event recorded afterwards covers the
-        whole step."""
+    def _io_streams(self) -> tuple[torch.cuda.Stream, torch.cuda.Stream]:
+        if getattr(self, "_up", None) is None:
+            self._up, self._down = torch.cuda.Stream(), torch.cuda.Stream()
+            self._io_slot, self._prev_out, self._prev_done = 0, set(), None
+        return self._up, self._down
+
+    def step_host(self, h_in: dict[str, torch.Tensor], h_out: dict[str, torch.Tensor]) -> torch.cuda.Event:
+        """One timestep from pinned host state ``h_in`` to pinned host state
+        ``h_out`` (reference array convention, host_buffers()).  Returns an
+        event that completes when ``h_out`` holds the result; the host buffers
+        must stay untouched until then.
+
+        Transfers run on an upload and a download stream (both PCIe
+        directions at once) and overlap the compute they do not feed: the
+        tracers' uploads run during the acoustic substeps (first needed by
+        tracer_2d), the dynamics fields' downloads during tracer advection
+        and remapping, the tracers' after tracer_2d.  Device staging is
+        double-buffered by call parity, so successive calls pipeline: the
+        next call's uploads overlap this call's compute, this call's
+        downloads the next call's compute.  A call whose inputs are the
+        previous call's outputs (a chained integration) waits for those
+        downloads before uploading."""
         comp = torch.cuda.current_stream()
-        cs = copy_stream or getattr(self, "_copy_stream", None)
-        if cs is None:
-            cs = self._copy_stream = torch.cuda.Stream()
+        up, down = self._io_streams()
         trc = [n for n in h_in if n in self.cfg.tracer_names()]
         dyn = [n for n in h_in if n not in trc]
-        sin, sout = self._io_stages(list(h_in))
-        cs.wait_stream(comp)  # staging buffers are free (previous step done)
-        with torch.cuda.stream(cs):
+        slot = self._io_slot
+        self._io_slot ^= 1
+        sin, sout = self._io_stages(list(h_in), slot)
+        free = self._io_free[slot]
+        if free[0] is not None:  # this slot's inputs were consumed two calls ago
+            up.wait_event(free[0])
+        if self._prev_done is not None and self._prev_out & {t.data_ptr() for t in h_in.values()}:
+            up.wait_event(self._prev_done)
+        with torch.cuda.stream(up):
             for n in dyn:
                 sin[n].copy_(h_in[n], non_blocking=True)
-            e_dyn = cs.record_event()
+            e_dyn = up.record_event()
             for n in trc:
                 sin[n].copy_(h_in[n], non_blocking=True)
-            e_trc = cs.record_event()
+            e_trc = up.record_event()
         comp.wait_event(e_dyn)
         for n in dyn:
             self._window(self.cur[n]).copy_(sin[n])
-        def out(names):  # device transpose on the compute stream, download on the copy stream
+        if free[1] is not None:  # this slot's outputs were downloaded two calls ago
+            comp.wait_event(free[1])
+
+        def out(names):  # device transpose on the compute stream, download on the download stream
             for n in names:
                 sout[n].copy_(self._window(self.cur[n]))
             e_out = comp.record_event()
-            with torch.cuda.stream(cs):
-                cs.wait_event(e_out)
+            down.wait_event(e_out)
+            with torch.cuda.stream(down):
                 for n in names:
                     h_out[n].copy_(sout[n], non_blocking=True)
 
@@ -177,11 +198,16 @@ class Dycore:
                 comp.wait_event(e_trc)
                 for n in trc:
                     self._window(self.cur[n]).copy_(sin[n])
+                free[0] = comp.record_event()
                 out(dyn)
             self.halo.update(names)
         if not trc:
+            free[0] = comp.record_event()
             out(dyn)
-        comp.wait_stream(cs)
+        done = down.record_event()
+        free[1] = done
+        self._prev_done, self._prev_out = done, {t.data_ptr() for t in h_out.values()}
+        return done
 
     # -- launch helpers -----------------------------------------------------
 

@@ -84,6 +84,34 @@ def test_checkpoint_restart_is_bitwise(tmp_path):
         assert np.array_equal(a.download([n])[n][h:-h, h:-h, :top], b.download([n])[n][h:-h, h:-h, :top]), n
 
 
+def test_step_host_chained_matches_step():
+    """step_host fed its own previous output (uploads wait for the downloads)
+    == load + step + store chained the same way."""
+    import torch
+
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.dycore import Dycore
+    from paper_2205_04148_b200.state import initial_state
+
+    cfg = RunConfig(ni=32, nj=24, nk=10, n_split=3, dt_atmos=45.0)
+    st = initial_state(cfg)
+    a, b = Dycore(cfg, st), Dycore(cfg, st)
+    ha, hb = [a.host_buffers(), a.host_buffers()], [b.host_buffers(), b.host_buffers()]
+    for n in ha[0]:
+        ha[0][n].copy_(torch.from_numpy(st[n]))
+        hb[0][n].copy_(torch.from_numpy(st[n]))
+    for s in range(4):
+        a.step_host(ha[s % 2], ha[(s + 1) % 2])
+        b.load_host(hb[s % 2])
+        b.step()
+        b.store_host(hb[(s + 1) % 2])
+    torch.cuda.synchronize()
+    h = cfg.halo
+    for n in ha[0]:
+        top = cfg.nk + 1 if n in INTERFACE else cfg.nk
+        assert torch.equal(ha[0][n][h:-h, h:-h, :top], hb[0][n][h:-h, h:-h, :top]), n
+
+
 def test_step_host_overlapped_io_matches_step():
     """Dycore.step_host (overlapped pinned-host transfers) == load + step + store."""
     import torch
