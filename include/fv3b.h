@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define FV3B_ABI_VERSION 2
+#define FV3B_ABI_VERSION 3
 
 enum {
   FV3B_OK = 0,
@@ -179,6 +179,15 @@ int fv3b_halo_gather(const fv3b_field* f, int nf, const double* s, int ns,
                      const fv3b_domain* d, void* stream);
 int fv3b_halo_scatter(const fv3b_field* f, int nf, const double* s, int ns,
                       const fv3b_domain* d, void* stream);
+
+/*   fv3b_transpose  state layout conversion for host I/O: copy the d->ni x
+ *                   d->nj x d->nk region at f[0].data to f[1].data where one
+ *                   field has unit K stride (the reference's numpy (I, J, K)
+ *                   C-order arrays, fieldio / run_reference) and the other
+ *                   unit I stride (the Layout).  fields: src, dst (rank 3,
+ *                   data = region origin, halo_lo ignored).  scalars: none. */
+int fv3b_transpose(const fv3b_field* f, int nf, const double* s, int ns,
+                   const fv3b_domain* d, void* stream);
 
 #ifdef __cplusplus
 }

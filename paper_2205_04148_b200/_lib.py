@@ -12,7 +12,7 @@ from pathlib import Path
 
 LIB_PATH = Path(os.environ.get("FV3B_LIB", Path(__file__).resolve().parent / "libfv3b.so"))
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class Field(ctypes.Structure):

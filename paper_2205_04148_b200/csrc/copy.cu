@@ -86,3 +86,63 @@ extern "C" int fv3b_copy(const fv3b_field* f, int nf, const double* s, int ns, c
     copy_scalar_kernel<<<grid, 256, 0, st>>>(in, out, d->ni, d->nj, d->nk);
   return check_launch("fv3b_copy");
 }
+
+// ---------------------------------------------------------------------------
+// Reference array convention (I, J, K with K unit stride: the numpy C-order
+// arrays of the reference's run_reference / fieldio) <-> the I-unit-stride
+// Layout.  Per J row a 32 x 32 (I, K) tile goes through shared memory, so
+// loads run along the source's unit axis and stores along the destination's:
+// both sides coalesced (the host<->device state path of Dycore.step_host).
+namespace fv3b {
+
+template <bool K2I>  // true: source K-unit -> destination I-unit
+__global__ void __launch_bounds__(256) transpose_ik_kernel(const double* __restrict__ src, int64_t s0, int64_t s1,
+                                                           int64_t s2, double* __restrict__ dst, int64_t d0,
+                                                           int64_t d1, int64_t d2, int ni, int nk) {
+  __shared__ double t[32][33];
+  const int64_t j = blockIdx.z;
+  const int ib = blockIdx.y * 32, kb = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int i = K2I ? ib + r : ib + tx, k = K2I ? kb + tx : kb + r;
+    if (i < ni && k < nk) t[r][tx] = __ldcs(src + i * s0 + j * s1 + k * s2);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int i = K2I ? ib + tx : ib + r, k = K2I ? kb + r : kb + tx;
+    if (i < ni && k < nk) __stcs(dst + i * d0 + j * d1 + k * d2, t[tx][r]);
+  }
+}
+
+}  // namespace fv3b
+
+extern "C" int fv3b_transpose(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                              void* stream) {
+  (void)s;
+  (void)ns;
+  if (f == nullptr || d == nullptr || nf != 2)
+    return fv3b::fail(FV3B_EINVAL, "fv3b_transpose: expects 2 fields (src, dst)");
+  const fv3b_field &a = f[0], &b = f[1];
+  if (a.data == nullptr || b.data == nullptr || a.rank != 3 || b.rank != 3)
+    return fv3b::fail(FV3B_EINVAL, "fv3b_transpose: src and dst must be 3-D fields");
+  const bool k2i = a.stride[2] == 1 && b.stride[0] == 1, i2k = a.stride[0] == 1 && b.stride[2] == 1;
+  if (!k2i && !i2k)
+    return fv3b::fail(FV3B_ELAYOUT, "fv3b_transpose: one field must be K-unit-stride, the other I-unit-stride");
+  for (int x = 0; x < 3; ++x) {
+    const int n = x == 0 ? d->ni : (x == 1 ? d->nj : d->nk);
+    if (n > a.shape[x] || n > b.shape[x])
+      return fv3b::fail(FV3B_EDOMAIN, "fv3b_transpose: region axis %d (%d) exceeds a field's shape", x, n);
+  }
+  if (d->ni <= 0 || d->nj <= 0 || d->nk <= 0) return FV3B_OK;
+  dim3 grid(fv3b::cdiv(d->nk, 32), fv3b::cdiv(d->ni, 32), d->nj), block(32, 8);
+  auto st = (cudaStream_t)stream;
+  if (k2i)
+    fv3b::transpose_ik_kernel<true><<<grid, block, 0, st>>>(a.data, a.stride[0], a.stride[1], a.stride[2], b.data,
+                                                            b.stride[0], b.stride[1], b.stride[2], d->ni, d->nk);
+  else
+    fv3b::transpose_ik_kernel<false><<<grid, block, 0, st>>>(a.data, a.stride[0], a.stride[1], a.stride[2], b.data,
+                                                             b.stride[0], b.stride[1], b.stride[2], d->ni, d->nk);
+  return fv3b::check_launch("fv3b_transpose");
+}

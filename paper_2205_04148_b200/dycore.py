@@ -112,35 +112,53 @@ class Dycore:
         a = g.i0 - self.cfg.halo
         return t[:, :, a : a + self.cfg.ni + 2 * self.cfg.halo].permute(2, 1, 0)
 
+    def _transpose(self, src: torch.Tensor, dst: torch.Tensor) -> None:
+        """Reference-convention (I, J, K) array <-> Layout window copy on the
+        device (fv3b_transpose, current stream); both are (I, J, K) views."""
+        fs = []
+        for t in (src, dst):
+            f = _lib.Field()
+            f.data = t.data_ptr()
+            f.stride[:] = list(t.stride())
+            f.shape[:] = list(t.shape)
+            f.halo_lo[:] = [0, 0, 0]
+            f.rank = 3
+            fs.append(f)
+        d = _lib.Domain()
+        d.ni, d.nj, d.nk = src.shape
+        self.launch("transpose", "fv3b_transpose", fs, [], d)
+
     def load_host(self, host: dict[str, torch.Tensor]) -> None:
         """Enqueue host -> device copies (pinned, async) of ``host`` fields
         into the current state, then the layout transpose on the device."""
         st = self._staging()
         for n, src in host.items():
             st.copy_(src, non_blocking=True)
-            self._window(self.cur[n]).copy_(st)
+            self._transpose(st, self._window(self.cur[n]))
 
     def store_host(self, host: dict[str, torch.Tensor]) -> None:
         """Enqueue device -> host copies of the current state into ``host``."""
         st = self._staging()
         for n, dst in host.items():
-            st.copy_(self._window(self.cur[n]))
+            self._transpose(self._window(self.cur[n]), st)
             dst.copy_(st, non_blocking=True)
 
-    def _io_stages(self, names, slot: int) -> tuple[dict, dict]:
-        """Device staging for step_host, double-buffered by call parity."""
+    def _io_stages(self, names) -> tuple[dict, dict, list]:
+        """Device staging for step_host of the current call: input stage i
+        (three-deep ring: a call's uploads never wait for the compute of the
+        call before last), output stage o (two-deep), and the slots' free events."""
         if getattr(self, "_io", None) is None or set(self._io[0][0]) != set(names):
             h, c = self.cfg.halo, self.cfg
             shape = (c.ni + 2 * h, c.nj + 2 * h, c.nk + 1)
             mk = lambda: {n: torch.empty(shape, dtype=torch.float64, device=self.device) for n in names}
-            self._io = ((mk(), mk()), (mk(), mk()))
-            self._io_free = [[None, None], [None, None]]  # [slot] -> (inputs consumed, outputs downloaded)
-        return self._io[slot]
+            self._io = ([mk() for _ in range(3)], [mk() for _ in range(2)])
+            self._io_free = ([None] * 3, [None] * 2)  # inputs consumed / outputs downloaded
+        return self._io
 
     def _io_streams(self) -> tuple[torch.cuda.Stream, torch.cuda.Stream]:
         if getattr(self, "_up", None) is None:
             self._up, self._down = torch.cuda.Stream(), torch.cuda.Stream()
-            self._io_slot, self._prev_out, self._prev_done = 0, set(), None
+            self._io_calls, self._prev_out, self._prev_done = 0, set(), None
         return self._up, self._down
 
     def step_host(self, h_in: dict[str, torch.Tensor], h_out: dict[str, torch.Tensor]) -> torch.cuda.Event:
@@ -153,22 +171,23 @@ class Dycore:
         directions at once) and overlap the compute they do not feed: the
         tracers' uploads run during the acoustic substeps (first needed by
         tracer_2d), the dynamics fields' downloads during tracer advection
-        and remapping, the tracers' after tracer_2d.  Device staging is
-        double-buffered by call parity, so successive calls pipeline: the
-        next call's uploads overlap this call's compute, this call's
-        downloads the next call's compute.  A call whose inputs are the
+        and remapping, the tracers' after tracer_2d.  Device staging is a ring
+        (three input stages, two output stages), so successive calls
+        pipeline: the next call's uploads overlap this call's compute, this
+        call's downloads the next call's compute.  A call whose inputs are the
         previous call's outputs (a chained integration) waits for those
         downloads before uploading."""
         comp = torch.cuda.current_stream()
         up, down = self._io_streams()
         trc = [n for n in h_in if n in self.cfg.tracer_names()]
         dyn = [n for n in h_in if n not in trc]
-        slot = self._io_slot
-        self._io_slot ^= 1
-        sin, sout = self._io_stages(list(h_in), slot)
-        free = self._io_free[slot]
-        if free[0] is not None:  # this slot's inputs were consumed two calls ago
-            up.wait_event(free[0])
+        stages = self._io_stages(list(h_in))
+        si, so = self._io_calls % 3, self._io_calls % 2
+        self._io_calls += 1
+        sin, sout = stages[0][si], stages[1][so]
+        in_free, out_free = self._io_free
+        if in_free[si] is not None:  # consumed by the compute three calls ago
+            up.wait_event(in_free[si])
         if self._prev_done is not None and self._prev_out & {t.data_ptr() for t in h_in.values()}:
             up.wait_event(self._prev_done)
         with torch.cuda.stream(up):
@@ -180,13 +199,13 @@ class Dycore:
             e_trc = up.record_event()
         comp.wait_event(e_dyn)
         for n in dyn:
-            self._window(self.cur[n]).copy_(sin[n])
-        if free[1] is not None:  # this slot's outputs were downloaded two calls ago
-            comp.wait_event(free[1])
+            self._transpose(sin[n], self._window(self.cur[n]))
+        if out_free[so] is not None:  # downloaded two calls ago
+            comp.wait_event(out_free[so])
 
         def out(names):  # device transpose on the compute stream, download on the download stream
             for n in names:
-                sout[n].copy_(self._window(self.cur[n]))
+                self._transpose(self._window(self.cur[n]), sout[n])
             e_out = comp.record_event()
             down.wait_event(e_out)
             with torch.cuda.stream(down):
@@ -197,15 +216,15 @@ class Dycore:
             if trc and trc[0] in names:
                 comp.wait_event(e_trc)
                 for n in trc:
-                    self._window(self.cur[n]).copy_(sin[n])
-                free[0] = comp.record_event()
+                    self._transpose(sin[n], self._window(self.cur[n]))
+                in_free[si] = comp.record_event()
                 out(dyn)
             self.halo.update(names)
         if not trc:
-            free[0] = comp.record_event()
+            in_free[si] = comp.record_event()
             out(dyn)
         done = down.record_event()
-        free[1] = done
+        out_free[so] = done
         self._prev_done, self._prev_out = done, {t.data_ptr() for t in h_out.values()}
         return done
 
