@@ -97,8 +97,8 @@ int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, int ns,
 
 /* K5  remap_profile.stn / remap_tracers.stn — PPM edge solve + limited
  *     sub-grid coefficients.  Program domain nk = interface levels.
- *     fields: delp, then per tracer: q, a4_2, a4_3, a4_4, then a 3-D scratch
- *     (gam, shared by the tracers).  scalars: none. */
+ *     fields: delp, then per tracer: q, a4_2, a4_3, a4_4 (outputs must not
+ *     alias the inputs).  scalars: none. */
 int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns,
                        const fv3b_domain* d, void* stream);
 

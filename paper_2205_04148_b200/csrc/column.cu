@@ -67,11 +67,9 @@ struct D3 { double x, y, z; };
 #ifndef FV3B_PF  // (overridable for tuning sweeps, tools/build_variant.py)
 #define FV3B_PF 4
 #define FV3B_PFS 12
-#define FV3B_PFR 8
 #endif
 constexpr int PF = FV3B_PF;    // prefetch distance (levels), riem passes with long bodies (A, C)
 constexpr int PFS = FV3B_PFS;  // riem passes with short bodies (B, D, E, F): L2-resident staging reads
-constexpr int PFR = FV3B_PFR;  // remap: short per-level bodies need a deeper ring
 
 // Statement-for-statement restatement of templates.riem_stencils for one
 // column.  FAST: branch-free divisions/logs (fastdiv.cuh), returns false if
@@ -314,100 +312,97 @@ struct RemapArgs {
   double* a2[16];
   double* a3[16];
   double* a4[16];
-  double* gam;  // scratch: gam per column (interior origin, strides sj / sk)
   int64_t sj, sk;
   int nq, ni, nj, nk;  // nk layers (program domain nk+1)
 };
 
+// One (column, tracer) per thread: 8x the independent recurrences of a
+// column-per-thread solver (the tracers' sweeps share nothing but delp), so
+// the latency of the division chains is hidden by occupancy.  gam (delp
+// only) is re-derived per tracer inside the forward sweep (its statement
+// shares bet and d4 with the edge recurrence: same operands, same bits).
+// The values the backward sweep consumes are staged in the tracer's own
+// output slots (gam in a4_2[k], the forward edge in a4_3[k], both read back
+// before level k's coefficients overwrite them; L2-resident).
 template <bool FAST>
-__device__ __forceinline__ bool remap_column(const RemapArgs& a, int i, int j, int c, int NC, double* sm) {
+__device__ __forceinline__ bool remap_column(const RemapArgs& a, int i, int j, int t) {
   ColArith<FAST> ar;
-  const int nk = a.nk, L = nk + 1;
-  double* E = sm + c;  // qe (shared memory)
-  (void)L;
-#define AT(S, k) (S)[(k) * NC]
+  const int nk = a.nk;
   const int64_t off = i + (int64_t)j * a.sj, sk = a.sk;
-  double* G = a.gam + off;  // gam depends on delp only: computed once, shared by all tracers (L1/L2-resident)
   const double* __restrict__ dp = a.delp.ptr(i, j, 0);
-  // gam of remap_edge_fwd, once per column
+  const double* __restrict__ q = a.q[t] + off;
+  double* o2 = a.a2[t] + off;  // gam(k), then a4_2
+  double* o3 = a.a3[t] + off;  // forward edge qe(k), then a4_3
+  double* o4 = a.a4[t] + off;
+  // forward: remap_edge_fwd (gam and qe)
   const double dp0 = __ldg(dp), dp1 = __ldg(dp + sk);
+  const double q0 = __ldg(q), q1 = __ldg(q + sk);
   const double grat0 = ar.div(dp1, dp0);
   const double bet0 = grat0 * (grat0 + 0.5);
-  G[0] = ar.div(1.0 + grat0 * (grat0 + 1.5), bet0);
-  double d4last = 0.0;
-  {
-    double dprev = dp0, gprev = G[0];
-    pipelined<PFR, D1>(
-        nk - 1, [&](int s) { return D1{__ldg(dp + (s + 1) * sk)}; },
-        [&](int s, const D1& v) {
-          const double d4 = ar.div(dprev, v.x);
-          const double bet = 2.0 + d4 + d4 - gprev;
-          gprev = ar.div(d4, bet);
-          G[(s + 1) * sk] = gprev;
-          dprev = v.x;
-          d4last = d4;
-        });
-  }
-  for (int t = 0; t < a.nq; ++t) {
-    const double* __restrict__ q = a.q[t] + off;
-    // forward: remap_edge_fwd (qe)
-    const double q0 = __ldg(q), q1 = __ldg(q + sk);
-    AT(E, 0) = ar.div((grat0 + grat0) * (grat0 + 1.0) * q0 + q1, bet0);
-    {
-      double dprev = dp0, qprev = q0, eprev = AT(E, 0);
-      pipelined<PFR, D3>(
-          nk - 1, [&](int s) { return D3{__ldg(dp + (s + 1) * sk), __ldg(q + (s + 1) * sk), G[s * sk]}; },
-          [&](int s, const D3& v) {
-            const int k = s + 1;
-            const double d4 = ar.div(dprev, v.x);
-            const double bet = 2.0 + d4 + d4 - v.z;  // gam(k-1)
-            eprev = ar.div(3.0 * (qprev + d4 * v.y) - eprev, bet);
-            AT(E, k) = eprev;
-            dprev = v.x;
-            qprev = v.y;
-          });
-      const double d4p = d4last;
-      const double abot = 1.0 + d4p * (d4p + 1.5);
-      AT(E, nk) = ar.div(2.0 * d4p * (d4p + 1.0) * qprev + __ldg(q + (nk - 2) * sk) - abot * eprev,
-                         d4p * (d4p + 0.5) - abot * G[(nk - 1) * sk]);
-    }
-    // backward: remap_edge_bwd fused with remap_a4 for layer k
-    double* o2 = a.a2[t] + off;
-    double* o3 = a.a3[t] + off;
-    double* o4 = a.a4[t] + off;
-    double qen = AT(E, nk);
-    pipelined<PFR, D2>(
-        nk, [&](int s) { return D2{__ldg(q + (nk - 1 - s) * sk), G[(nk - 1 - s) * sk]}; },
-        [&](int s, const D2& v) {
-          const int k = nk - 1 - s;
-          const double qek = AT(E, k) - v.y * qen;
-          const double qc = v.x;
-          const double al = qek, ar_ = qen;
-          const double ext = (ar_ - qc) * (qc - al);
-          const double da1 = ar_ - al;
-          const double a6 = 3.0 * (2.0 * qc - (al + ar_));
-          const double a6da = a6 * da1;
-          const double da2 = da1 * da1;
-          const double v2 = (ext <= 0.0) ? qc : ((a6da > da2) ? 3.0 * qc - 2.0 * ar_ : al);
-          const double v3 = (ext <= 0.0) ? qc : ((a6da < -da2) ? 3.0 * qc - 2.0 * al : ar_);
-          o2[k * sk] = v2;
-          o3[k * sk] = v3;
-          o4[k * sk] = 3.0 * (2.0 * qc - (v2 + v3));
-          qen = qek;
-        });
-  }
-#undef AT
+  const double rb0 = ar.rcp(bet0);
+  double gprev = ar.div_r(1.0 + grat0 * (grat0 + 1.5), bet0, rb0);
+  double eprev = ar.div_r((grat0 + grat0) * (grat0 + 1.0) * q0 + q1, bet0, rb0);
+  o2[0] = gprev;
+  o3[0] = eprev;
+  double dprev = dp0, qprev = q0, d4last = 0.0;
+#ifndef FV3B_RM_PF
+#define FV3B_RM_PF 8  // measured: 8 > 4, 12, 16 (tools/build_variant.py sweeps)
+#endif
+  pipelined<FV3B_RM_PF, D2>(
+      nk - 1, [&](int s) { return D2{__ldg(dp + (s + 1) * sk), __ldg(q + (s + 1) * sk)}; },
+      [&](int s, const D2& v) {
+        const int k = s + 1;
+        const double d4 = ar.div(dprev, v.x);
+        const double bet = 2.0 + d4 + d4 - gprev;  // gam(k-1)
+        const double rb = ar.rcp(bet);
+        eprev = ar.div_r(3.0 * (qprev + d4 * v.y) - eprev, bet, rb);
+        gprev = ar.div_r(d4, bet, rb);
+        o2[k * sk] = gprev;
+        o3[k * sk] = eprev;
+        dprev = v.x;
+        qprev = v.y;
+        d4last = d4;
+      });
+  const double d4p = d4last;
+  const double abot = 1.0 + d4p * (d4p + 1.5);
+  // gam(nk-1) = gprev
+  double qen = ar.div(2.0 * d4p * (d4p + 1.0) * qprev + __ldg(q + (nk - 2) * sk) - abot * eprev,
+                      d4p * (d4p + 0.5) - abot * gprev);
+  // backward: remap_edge_bwd fused with remap_a4 for layer k
+  pipelined<FV3B_RM_PF, D3>(
+      nk, [&](int s) { const int k = nk - 1 - s; return D3{__ldg(q + k * sk), o2[k * sk], o3[k * sk]}; },
+      [&](int s, const D3& v) {
+        const int k = nk - 1 - s;
+        const double qek = v.z - v.y * qen;
+        const double qc = v.x;
+        const double al = qek, ar_ = qen;
+        const double ext = (ar_ - qc) * (qc - al);
+        const double da1 = ar_ - al;
+        const double a6 = 3.0 * (2.0 * qc - (al + ar_));
+        const double a6da = a6 * da1;
+        const double da2 = da1 * da1;
+        const double v2 = (ext <= 0.0) ? qc : ((a6da > da2) ? 3.0 * qc - 2.0 * ar_ : al);
+        const double v3 = (ext <= 0.0) ? qc : ((a6da < -da2) ? 3.0 * qc - 2.0 * al : ar_);
+        o2[k * sk] = v2;
+        o3[k * sk] = v3;
+        o4[k * sk] = 3.0 * (2.0 * qc - (v2 + v3));
+        qen = qek;
+      });
   return ar.ok;
 }
 
-__global__ void __launch_bounds__(NC_MAX) remap_kernel(const RemapArgs a) {
-  extern __shared__ double sm[];
-  const int c = threadIdx.x, NC = blockDim.x;
-  const int cidx = blockIdx.x * NC + c;
-  if (cidx >= a.ni * a.nj) return;
+constexpr int RM_COLS = 32, RM_TQ = 4;  // CTA: 32 columns x 4 tracers
+#ifndef FV3B_RM_MINB
+#define FV3B_RM_MINB 1
+#endif
+
+__global__ void __launch_bounds__(RM_COLS * RM_TQ, FV3B_RM_MINB) remap_kernel(const RemapArgs a) {
+  const int cidx = blockIdx.x * RM_COLS + threadIdx.x;
+  const int t = blockIdx.y * RM_TQ + threadIdx.y;
+  if (cidx >= a.ni * a.nj || t >= a.nq) return;
   const int i = cidx % a.ni, j = cidx / a.ni;
-  // outputs never alias inputs: a failed fast evaluation is simply redone
-  if (!remap_column<true>(a, i, j, c, NC, sm)) remap_column<false>(a, i, j, c, NC, sm);
+  // inputs are never written: a failed fast evaluation is simply redone
+  if (!remap_column<true>(a, i, j, t)) remap_column<false>(a, i, j, t);
 }
 
 static int set_smem(const void* fn, size_t bytes) {
@@ -493,27 +488,19 @@ extern "C" int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, 
   return launch_riem(a, (cudaStream_t)stream);
 }
 
-// fields: delp, then per tracer t: q_t, a2_t, a3_t, a4_t, then a 3-D scratch
-// (gam).  Domain nk =
-// interface levels (program domain).  No scalars.
+// fields: delp, then per tracer t: q_t, a2_t, a3_t, a4_t.  Domain nk =
+// interface levels (program domain).  No scalars.  Outputs must not alias
+// the inputs (a2 / a3 stage the backward sweep's operands).
 extern "C" int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                                   void* stream) {
   (void)s;
-  if (f == nullptr || d == nullptr || nf < 6 || (nf - 2) % 4 != 0 || (nf - 2) / 4 > 16 || ns != 0)
-    return fail(FV3B_EINVAL, "fv3b_remap_profile: expects 1 + 4*nq + 1 fields (nq <= 16), 0 scalars");
+  if (f == nullptr || d == nullptr || nf < 5 || (nf - 1) % 4 != 0 || (nf - 1) / 4 > 16 || ns != 0)
+    return fail(FV3B_EINVAL, "fv3b_remap_profile: expects 1 + 4*nq fields (nq <= 16), 0 scalars");
   if (d->nk < 3) return fail(FV3B_EDOMAIN, "fv3b_remap_profile: program domain nk=%d below minimum 3", d->nk);
   RemapArgs a;
   const Halo h0 = {0, 0, 0, 0, 0, 0};
   FV3B_TRY(view_of(f[0], 3, *d, h0, "delp", &a.delp));
-  a.nq = (nf - 2) / 4;
-  {
-    View g;
-    FV3B_TRY(view_of(f[nf - 1], 3, *d, h0, "scratch", &g));
-    if (g.sj != a.delp.sj || g.sk != a.delp.sk) return fail(FV3B_ELAYOUT, "fv3b_remap_profile: scratch strides differ");
-    a.gam = g.o;
-    for (int t = 0; t < nf - 1; ++t)
-      if (f[t].data == f[nf - 1].data) return fail(FV3B_EINVAL, "fv3b_remap_profile: scratch aliases field %d", t);
-  }
+  a.nq = (nf - 1) / 4;
   for (int t = 0; t < a.nq; ++t) {
     View v[4];
     for (int u = 0; u < 4; ++u) FV3B_TRY(view_of(f[1 + 4 * t + u], 3, *d, h0, "remap field", &v[u]));
@@ -524,16 +511,20 @@ extern "C" int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, 
     a.a3[t] = v[2].o;
     a.a4[t] = v[3].o;
   }
+  for (int t = 0; t < a.nq; ++t)
+    for (int u = 1; u < 4; ++u) {
+      const void* o = f[1 + 4 * t + u].data;
+      if (o == f[0].data) return fail(FV3B_EINVAL, "fv3b_remap_profile: output aliases delp");
+      for (int r = 0; r < a.nq; ++r)
+        if (o == f[1 + 4 * r].data) return fail(FV3B_EINVAL, "fv3b_remap_profile: output aliases q%d", r);
+    }
   a.sj = a.delp.sj;
   a.sk = a.delp.sk;
   a.ni = d->ni;
   a.nj = d->nj;
   a.nk = d->nk - 1;
   if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
-  const size_t per_col = (size_t)(a.nk + 1) * sizeof(double);
-  const int nc = cols_per_cta(per_col, (int64_t)a.ni * a.nj);
-  const size_t bytes = per_col * nc;
-  FV3B_TRY(set_smem((const void*)remap_kernel, bytes));
-  remap_kernel<<<cdiv(a.ni * a.nj, nc), nc, bytes, (cudaStream_t)stream>>>(a);
+  dim3 grid(cdiv(a.ni * a.nj, RM_COLS), cdiv(a.nq, RM_TQ));
+  remap_kernel<<<grid, dim3(RM_COLS, RM_TQ), 0, (cudaStream_t)stream>>>(a);
   return check_launch("remap_profile");
 }

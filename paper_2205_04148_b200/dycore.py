@@ -57,7 +57,7 @@ class Dycore:
         self.cur: dict[str, torch.Tensor] = {n: g.new3(device) for n in names3}
         self.cur.update({n: g.new2(device) for n in METRICS_2D})
         self.alt: dict[str, torch.Tensor] = {n: g.new3(device) for n in list(PINGPONG) + ["gz"] + cfg.tracer_names()}
-        self.scratch = {n: g.new3(device) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc", "riem_scr", "remap_gam")}
+        self.scratch = {n: g.new3(device) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc", "riem_scr")}
         self.halo = halo or PeriodicHalo(self)
         self.stream = None
         self.launches = 0
@@ -293,7 +293,6 @@ class Dycore:
         fields = [self.f("delp")]
         for q in self.cfg.tracer_names():
             fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4")]
-        fields.append(self.s("remap_gam"))
         self.launch("remap_tracers", "fv3b_remap_profile", fields, [], self.dom_ifaces)
 
     def phases(self, after_tracers=None):

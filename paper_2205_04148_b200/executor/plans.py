@@ -168,7 +168,6 @@ class RemapPlan(Plan):
         else:
             for t in self._tracers(prog):
                 fields += [ctx.f(f"q{t}"), ctx.o(f"q{t}_a2"), ctx.o(f"q{t}_a3"), ctx.o(f"q{t}_a4")]
-        fields.append(ctx.scratch("remap_gam"))
         ctx.call(prog.trace[0][0] + "_0", "fv3b_remap_profile", fields, [])
 
 
