@@ -33,6 +33,15 @@ struct PgArgs {
   double dt;
 };
 
+// p_grad_d tiling (below): 32 x 8 cells and PG_KC levels per CTA.
+#ifndef FV3B_PG_KC
+#define FV3B_PG_KC 4
+#endif
+constexpr int PG_TI = 32, PG_TJ = 8, PG_KC = FV3B_PG_KC;
+constexpr int PG_CW = PG_TI + 1, PG_CH = PG_TJ + 1, PG_NP = PG_CW * PG_CH;
+
+// one thread per cell (measured faster here than the shared-memory tiling
+// used for p_grad_d: only three columns' interface values are reused)
 __global__ void p_grad_c_kernel(const PgArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
   if (i >= a.ni) return;
@@ -59,34 +68,51 @@ struct PgdArgs {
   double dt;
 };
 
-__global__ void p_grad_d_kernel(const PgdArgs a) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
-  if (i >= a.ni) return;
-  // pkd = 0.25 * (pef + pef[-1,0,0] + pef[0,-1,0] + pef[-1,-1,0])   (corner (i, j))
-  auto PK = [&](int ci, int cj, int kk) {
-    return 0.25 * (*a.pef.ptr(ci, cj, kk) + *a.pef.ptr(ci - 1, cj, kk) + *a.pef.ptr(ci, cj - 1, kk) +
-                   *a.pef.ptr(ci - 1, cj - 1, kk));
-  };
-  auto GZ = [&](int ci, int cj, int kk) {
-    return 0.25 * (*a.gz.ptr(ci, cj, kk) + *a.gz.ptr(ci - 1, cj, kk) + *a.gz.ptr(ci, cj - 1, kk) +
-                   *a.gz.ptr(ci - 1, cj - 1, kk));
-  };
-  const double p00 = PK(i, j, k), p01 = PK(i, j, k + 1);
-  const double g00 = GZ(i, j, k), g01 = GZ(i, j, k + 1);
-  const double wk = p01 - p00;
-  {  // u at (i, j-1/2): corners (i, j) and (i+1, j)
-    const double p10 = PK(i + 1, j, k), p11 = PK(i + 1, j, k + 1);
-    const double g10 = GZ(i + 1, j, k), g11 = GZ(i + 1, j, k + 1);
-    const double wkx = p11 - p10;
-    *a.uo.ptr(i, j, k) = *a.u.ptr(i, j, k) + a.dt * met(a.rdx, i, j) / (wk + wkx) *
-                                                 ((g01 - g10) * (p11 - p00) + (g00 - g11) * (p01 - p10));
+// Tile kernel: a CTA of 32 x 8 threads owns a 32 x 8 cell tile and PG_KC
+// levels.  The corner averages of the tile ((TI+1) x (TJ+1) corners x
+// (PG_KC+1) levels, all loads independent) are computed once into shared
+// memory, then every thread updates its cell's u and v on the PG_KC levels.
+__global__ void __launch_bounds__(PG_TI * PG_TJ) p_grad_d_kernel(const PgdArgs a) {
+  __shared__ double spk[PG_KC + 1][PG_NP], sgz[PG_KC + 1][PG_NP];
+  const int tid = threadIdx.x + threadIdx.y * PG_TI;
+  const int i0 = blockIdx.x * PG_TI, j0 = blockIdx.y * PG_TJ, k0 = blockIdx.z * PG_KC;
+  const int nl = min(PG_KC, a.nk - k0);
+  const int64_t pj = a.pef.sj, zj = a.gz.sj;
+  // corners (i0+ci, j0+cj), ci <= TI, cj <= TJ, levels k0 .. k0+nl
+  for (int e = tid; e < (nl + 1) * PG_NP; e += PG_TI * PG_TJ) {
+    const int l = e / PG_NP, c = e % PG_NP;
+    const int gi = i0 + c % PG_CW, gj = j0 + c / PG_CW;
+    if (gi <= a.ni && gj <= a.nj) {
+      // pkd = 0.25 * (pef + pef[-1,0,0] + pef[0,-1,0] + pef[-1,-1,0])
+      const double* p = a.pef.ptr(gi, gj, k0 + l);
+      const double* z = a.gz.ptr(gi, gj, k0 + l);
+      spk[l][c] = 0.25 * (__ldg(p) + __ldg(p - 1) + __ldg(p - pj) + __ldg(p - 1 - pj));
+      sgz[l][c] = 0.25 * (__ldg(z) + __ldg(z - 1) + __ldg(z - zj) + __ldg(z - 1 - zj));
+    }
   }
-  {  // v at (i-1/2, j): corners (i, j) and (i, j+1)
-    const double p10 = PK(i, j + 1, k), p11 = PK(i, j + 1, k + 1);
-    const double g10 = GZ(i, j + 1, k), g11 = GZ(i, j + 1, k + 1);
-    const double wky = p11 - p10;
-    *a.vo.ptr(i, j, k) = *a.v.ptr(i, j, k) + a.dt * met(a.rdy, i, j) / (wk + wky) *
-                                                 ((g01 - g10) * (p11 - p00) + (g00 - g11) * (p01 - p10));
+  __syncthreads();
+  const int li = threadIdx.x, lj = threadIdx.y, i = i0 + li, j = j0 + lj;
+  if (i >= a.ni || j >= a.nj) return;
+  const int c = lj * PG_CW + li;
+  const double rx = met(a.rdx, i, j), ry = met(a.rdy, i, j);
+  for (int l = 0; l < nl; ++l) {
+    const int k = k0 + l;
+    const double p00 = spk[l][c], p01 = spk[l + 1][c], g00 = sgz[l][c], g01 = sgz[l + 1][c];
+    const double wk = p01 - p00;
+    {  // u at (i, j-1/2): corners (i, j) and (i+1, j)
+      const double p10 = spk[l][c + 1], p11 = spk[l + 1][c + 1];
+      const double g10 = sgz[l][c + 1], g11 = sgz[l + 1][c + 1];
+      const double wkx = p11 - p10;
+      *a.uo.ptr(i, j, k) = __ldg(a.u.ptr(i, j, k)) + a.dt * rx / (wk + wkx) *
+                                                         ((g01 - g10) * (p11 - p00) + (g00 - g11) * (p01 - p10));
+    }
+    {  // v at (i-1/2, j): corners (i, j) and (i, j+1)
+      const double p10 = spk[l][c + PG_CW], p11 = spk[l + 1][c + PG_CW];
+      const double g10 = sgz[l][c + PG_CW], g11 = sgz[l + 1][c + PG_CW];
+      const double wky = p11 - p10;
+      *a.vo.ptr(i, j, k) = __ldg(a.v.ptr(i, j, k)) + a.dt * ry / (wk + wky) *
+                                                         ((g01 - g10) * (p11 - p00) + (g00 - g11) * (p01 - p10));
+    }
   }
 }
 
@@ -288,7 +314,7 @@ extern "C" int fv3b_p_grad_d(const fv3b_field* f, int nf, const double* s, int n
   if (f[6].data == f[0].data || f[7].data == f[1].data) return fail(FV3B_EINVAL, "fv3b_p_grad_d: outputs alias inputs");
   p.ni = d->ni; p.nj = d->nj; p.nk = d->nk - 1; p.dt = s[0];
   if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
-  dim3 grid(cdiv(d->ni, 64), d->nj, p.nk);
-  p_grad_d_kernel<<<grid, 64, 0, (cudaStream_t)stream>>>(p);
+  dim3 grid(cdiv(d->ni, PG_TI), cdiv(d->nj, PG_TJ), cdiv(p.nk, PG_KC));
+  p_grad_d_kernel<<<grid, dim3(PG_TI, PG_TJ), 0, (cudaStream_t)stream>>>(p);
   return check_launch("p_grad_d");
 }
