@@ -102,6 +102,15 @@ int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns,
                        const fv3b_domain* d, void* stream);
 
+/* K5b remap mapping (FV3 map1_ppm; oracle/remap_map.py): integrate each
+ *     tracer's remap_profile parabolas over the target layers of
+ *     pe2 = ak + bk * ps (ps = ptop + sum of delp), then delp <- pe2
+ *     differences in place.  Program domain nk = interface levels.
+ *     fields: delp, ak (K), bk (K), then per tracer: q, a4_2, a4_3, a4_4,
+ *     q_out (q_out must not alias any other field).  scalars: none. */
+int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int ns,
+                   const fv3b_domain* d, void* stream);
+
 /* K2  c_sw.stn — C-grid half step.  fields: u, v, delp, pt, w (3-D); dx, dy,
  *     dxc, dyc, rdxc, rdyc, rarea, rarea_c, fc (2-D); uc, vc, delpc, ptc, wc
  *     (3-D outputs).  scalars: dt2. */

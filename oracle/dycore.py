@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import interp
+from . import interp, remap_map
 
 PERIODIC = interp.PERIODIC
 
@@ -118,6 +118,8 @@ class OracleDycore:
         yield cfg.tracer_names() + ["cx", "cy", "xfa", "yfa", "mfx", "mfy"]
         self.call("tracer_2d", c)
         self.call("remap_tracers", c)
+        ak, bk = cfg.target_coordinate()
+        remap_map.remap_map(st, cfg.tracer_names(), ak, bk, cfg.nk, self._h)
 
     def step(self) -> None:
         for names in self.phases():

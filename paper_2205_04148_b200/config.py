@@ -14,6 +14,7 @@ One dycore timestep (k_split = 1):
     halo_update(q*, cx, cy, xfa, yfa, mfx, mfy)
     tracer_2d (nq tracers)                            -> q*
     remap_tracers (remap_profile of every tracer)     -> q*_a2, q*_a3, q*_a4
+    remap_map (Lagrangian -> Eulerian, map1_ppm)      -> q*, delp
 """
 
 from __future__ import annotations
@@ -48,6 +49,14 @@ class RunConfig:
 
     def tracer_names(self) -> list[str]:
         return [f"q{n}" for n in range(self.nq)]
+
+    def target_coordinate(self):
+        """ak, bk (nk+1) of the vertical remapping's target interfaces
+        pe2 = ak + bk * ps: pure sigma below ptop, bk = k / nk."""
+        import numpy as np
+
+        bk = np.arange(self.nk + 1, dtype=np.float64) / self.nk
+        return self.consts["ptop"] * (1.0 - bk), bk
 
 
 # Prognostic / diagnostic state fields.  3-D fields have nk+1 levels

@@ -58,12 +58,14 @@ class Dycore:
         self.cur.update({n: g.new2(device) for n in METRICS_2D})
         self.alt: dict[str, torch.Tensor] = {n: g.new3(device) for n in list(PINGPONG) + ["gz"] + cfg.tracer_names()}
         self.scratch = {n: g.new3(device) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc", "riem_scr")}
+        # target coordinate of the vertical remapping (pe2 = ak + bk * ps)
+        ak, bk = cfg.target_coordinate()
+        self.coord = {"ak": torch.from_numpy(ak).to(device), "bk": torch.from_numpy(bk).to(device)}
         self.halo = halo or PeriodicHalo(self)
         self.stream = None
         self.launches = 0
         self.timer = None
-        self._graphs: dict[int, torch.cuda.CUDAGraph] = {}
-        self._parity = 0
+        self._graphs: dict[tuple, tuple] = {}
         if state is not None:
             self.load(state)
 
@@ -170,17 +172,21 @@ class Dycore:
         Transfers run on an upload and a download stream (both PCIe
         directions at once) and overlap the compute they do not feed: the
         tracers' uploads run during the acoustic substeps (first needed by
-        tracer_2d), the dynamics fields' downloads during tracer advection
-        and remapping, the tracers' after tracer_2d.  Device staging is a ring
-        (three input stages, two output stages), so successive calls
-        pipeline: the next call's uploads overlap this call's compute, this
-        call's downloads the next call's compute.  A call whose inputs are the
-        previous call's outputs (a chained integration) waits for those
-        downloads before uploading."""
+        tracer_2d); the dynamics fields other than delp are final after the
+        substeps and download during tracer advection and remapping; the
+        tracers and delp (rewritten by the remap mapping) download at the end
+        of the step.  Device staging is a ring (three input stages, two output
+        stages), so successive calls pipeline: the next call's uploads
+        overlap this call's compute, this call's downloads the next call's
+        compute.  A call whose inputs are the previous call's outputs (a
+        chained integration) waits for those downloads before uploading."""
         comp = torch.cuda.current_stream()
         up, down = self._io_streams()
-        trc = [n for n in h_in if n in self.cfg.tracer_names()]
-        dyn = [n for n in h_in if n not in trc]
+        tracers = set(self.cfg.tracer_names())
+        trc = [n for n in h_in if n in tracers]           # uploaded during the substeps
+        dyn = [n for n in h_in if n not in tracers]       # uploaded before the step
+        late = [n for n in h_in if n in tracers or n == "delp"]  # downloaded after remap_map
+        early = [n for n in h_in if n not in late]
         stages = self._io_stages(list(h_in))
         si, so = self._io_calls % 3, self._io_calls % 2
         self._io_calls += 1
@@ -204,6 +210,8 @@ class Dycore:
             comp.wait_event(out_free[so])
 
         def out(names):  # device transpose on the compute stream, download on the download stream
+            if not names:
+                return
             for n in names:
                 self._transpose(self._window(self.cur[n]), sout[n])
             e_out = comp.record_event()
@@ -212,17 +220,20 @@ class Dycore:
                 for n in names:
                     h_out[n].copy_(sout[n], non_blocking=True)
 
-        for names in self.phases(after_tracers=(lambda: out(trc)) if trc else None):
-            if trc and trc[0] in names:
+        tracer_point, consumed = set(self.cfg.tracer_names()), False
+        for names in self.phases():
+            if tracer_point & set(names):  # the tracer halo point: substeps done
                 comp.wait_event(e_trc)
                 for n in trc:
                     self._transpose(sin[n], self._window(self.cur[n]))
-                in_free[si] = comp.record_event()
-                out(dyn)
+                in_free[si], consumed = comp.record_event(), True
+                out(early)
             self.halo.update(names)
-        if not trc:
+        if not consumed:  # no tracers in the run
+            comp.wait_event(e_trc)
             in_free[si] = comp.record_event()
-            out(dyn)
+            out(early)
+        out(late)
         done = down.record_event()
         out_free[so] = done
         self._prev_done, self._prev_out = done, {t.data_ptr() for t in h_out.values()}
@@ -295,7 +306,17 @@ class Dycore:
             fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4")]
         self.launch("remap_tracers", "fv3b_remap_profile", fields, [], self.dom_ifaces)
 
-    def phases(self, after_tracers=None):
+    def remap_map(self) -> None:
+        """Lagrangian -> Eulerian: every tracer's profile integrated over the
+        target layers (pe2 = ak + bk * ps), delp <- pe2 differences."""
+        qs = self.cfg.tracer_names()
+        fields = [self.f("delp")] + [self.grid.abi(self.coord[n], rank=1) for n in ("ak", "bk")]
+        for q in qs:
+            fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4"), self.a(q)]
+        self.launch("remap_map", "fv3b_remap_map", fields, [], self.dom_ifaces)
+        self.swap(*qs)
+
+    def phases(self):
         """One timestep as a generator: enqueues the programs on the current
         stream and yields, at each halo-update point, the fields to refresh
         (the caller performs the update; a decomposed run exchanges them
@@ -314,10 +335,8 @@ class Dycore:
             self.p_grad_d()
         yield cfg.tracer_names() + list(ACCUM)
         self.tracer_2d()
-        if after_tracers is not None:  # the advected tracers are final (remap only reads them)
-            after_tracers()
         self.remap()
-        self._parity ^= 1  # the tracers swap buffers once per step
+        self.remap_map()
 
     def step(self) -> None:
         """Enqueue one full timestep on the current stream."""
@@ -326,27 +345,32 @@ class Dycore:
 
     # -- CUDA graphs ---------------------------------------------------------
 
+    def _assignment(self) -> tuple:
+        return tuple(self.cur[n].data_ptr() for n in sorted(self.cur))
+
     def capture(self) -> None:
-        """Capture one timestep per buffer parity (the tracers alternate
-        buffers each step; every other ping-pong field swaps an even number of
-        times).  Capture executes nothing, so the state is unchanged; the
-        two captures leave the buffer bookkeeping where it started."""
+        """Capture one timestep per distinct buffer assignment.  A step
+        permutes the ping-pong buffers (every field swaps an even number of
+        times at present, so one graph suffices); the captures follow the
+        assignments until they cycle.  Capture executes nothing, so the
+        state is unchanged; the bookkeeping is restored afterwards."""
         torch.cuda.synchronize()
-        start = self._parity
-        for _ in range(2):
-            parity = self._parity
+        start = (dict(self.cur), dict(self.alt))
+        self._graphs = {}
+        while self._assignment() not in self._graphs:
+            key = self._assignment()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 self.step()
-            self._graphs[parity] = g
-        assert self._parity == start
+            self._graphs[key] = (g, dict(self.cur), dict(self.alt))
+        self.cur, self.alt = start
         torch.cuda.synchronize()
 
     def replay(self) -> None:
         """Run one captured timestep on the current stream."""
-        self._graphs[self._parity].replay()
-        self._parity ^= 1
-        self.swap(*self.cfg.tracer_names())
+        g, cur, alt = self._graphs[self._assignment()]
+        g.replay()
+        self.cur, self.alt = dict(cur), dict(alt)
 
 
 # libfv3b kernels launched per entry point (fused entries launch several)
@@ -355,4 +379,4 @@ KERNELS = {"fv3b_c_grid": 3, "fv3b_d_sw": 2}
 
 def kernels_per_step(cfg: RunConfig) -> int:
     per_sub = 3 + KERNELS["fv3b_c_grid"] + KERNELS["fv3b_d_sw"] + 1 + 1
-    return cfg.n_split * per_sub + 1 + 1 + 1
+    return cfg.n_split * per_sub + 1 + 1 + 1 + 1

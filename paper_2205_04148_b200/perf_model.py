@@ -29,7 +29,14 @@ _TABLE = Path(__file__).resolve().parent / "traffic_table.json"
 
 
 def unique_bytes(program: str, domain) -> tuple[int, str]:
-    """(bytes, source) of one launch of `program` on `domain`."""
+    """(bytes, source) of one launch of `program` on `domain`.  The remap
+    mapping (not a .stn program: its source-layer search is data dependent)
+    takes ``domain = (ni, nj, nk + 1, nq)``."""
+    if program == "remap_map":
+        ni, nj, nki, nq = domain
+        cells = ni * nj * (nki - 1)
+        # delp read and rewritten; per tracer q, a4_2, a4_3, a4_4 read, q_out written; ak, bk
+        return 8 * (cells * (2 + 5 * nq) + 2 * nki), "analytic (each operand level once: upper bound)"
     key = f"{program}@{domain[0]}x{domain[1]}x{domain[2]}"
     if _TABLE.exists():
         tab = json.loads(_TABLE.read_text())
