@@ -45,6 +45,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+FP64_PEAK_OPS = 18.37e12  # measured fp64 op/s of one B200 (profiles/fp64_probe.txt: DFMA 63.2 op/clk/SM)
 METRIC = "dycore step grid-cells/s (fp64 FV3 timestep, 192x192x80 per GPU)"
 UNIT = "cells/s"
 
@@ -327,6 +328,19 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     if tf.exists():
         traffic = json.loads(tf.read_text()).get(top)
     step_bytes = sum(by[n].unique_bytes * len(per_node[n]) for n in progs) / args.steps
+    # the compute-side roof of the same kernel: fp64 thread operations per
+    # launch (ncu DADD + DMUL + DFMA, profiles/fp64.json via
+    # tools/traffic_from_ncu.py) / its mean launch time, against the fp64
+    # issue peak measured on the box (tools/fp64_probe.cu, profiles/fp64_probe.txt)
+    fp64 = None
+    ff = ROOT / "profiles" / "fp64.json"
+    if ff.exists() and json.loads(ff.read_text()).get(top):
+        ops = json.loads(ff.read_text())[top]
+        fp64_peak = FP64_PEAK_OPS * torch.cuda.get_device_properties(0).multi_processor_count / 148
+        fp64 = {"kernel": top, "ops_per_launch": ops, "achieved": ops / mean_launch / 1e12,
+                "peak": fp64_peak / 1e12, "unit": "Top/s", "frac": ops / mean_launch / fp64_peak,
+                "source": "ncu op counts (profiles/fp64.json) / CUDA-event launch time; peak: "
+                          "tools/fp64_probe.cu DFMA issue (profiles/fp64_probe.txt)"}
     cpu = None
     if not args.no_cpu and world == 1:
         v, cores, sample = cpu_run(1)
@@ -348,6 +362,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                      "mean_launch_s": mean_launch, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)",
                      "algo_bytes_source": by[top].source,
                      "step_algo_bytes": step_bytes, "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak},
+        "fp64_roofline": fp64,
         "report": {e.kernel: {"invocations_per_step": e.invocations // args.steps,
                               "measured_us": round(e.measured_time * 1e6, 2),
                               "bound_us": round(e.bound_time * 1e6, 2),

@@ -90,3 +90,24 @@ def test_remap_map_rejects_aliased_output():
     fields = [g.abi(t[0]), g.abi(ak, rank=1), g.abi(ak, rank=1)] + [g.abi(x) for x in t[1:]] + [g.abi(t[1])]
     with pytest.raises(_lib.Fv3bError):
         _lib.call("fv3b_remap_map", fields, [], g.domain(nk=5), torch.cuda.current_stream().cuda_stream)
+
+
+def test_transpose_round_trip_bitwise():
+    """fv3b_transpose: reference (I, J, K) order <-> Layout window, both ways,
+    on a ragged shape (tile edges in I, J and K)."""
+    import torch
+
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.dycore import Dycore
+
+    cfg = RunConfig(ni=37, nj=21, nk=45, nq=1, n_split=1)
+    d = Dycore(cfg)
+    h = cfg.halo
+    shape = (cfg.ni + 2 * h, cfg.nj + 2 * h, cfg.nk + 1)
+    src = torch.from_numpy(np.random.default_rng(9).standard_normal(shape)).cuda()
+    d._transpose(src, d._window(d.cur["pt"]))
+    assert torch.equal(d._window(d.cur["pt"]), src)
+    back = torch.empty_like(src)
+    d._transpose(d._window(d.cur["pt"]), back)
+    torch.cuda.synchronize()
+    assert torch.equal(back, src)

@@ -1,6 +1,8 @@
-"""Per-program DRAM traffic per launch from one ncu --set full capture of a
-single eager C2 step with n_split = 1 (tools/profile_step.py 1 1), written to
-profiles/traffic.json for bench.py's roofline ``traffic`` field.
+"""Per-program DRAM traffic and fp64 thread operations per launch from one
+ncu --set full capture of a single eager C2 step with n_split = 1
+(tools/profile_step.py 1 1), written to profiles/traffic.json (bench.py's
+roofline ``traffic`` field) and profiles/fp64.json (its ``fp64`` roofline:
+DADD + DMUL + DFMA thread instructions, each one fp64 operation issue).
 
     python tools/traffic_from_ncu.py gpurun_out/prof_X.ncu-rep [more.ncu-rep ...]
 
@@ -15,14 +17,24 @@ import sys
 from pathlib import Path
 
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-def launches(rep):
+FP64 = [f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum.per_cycle_elapsed" for o in ("dadd", "dmul", "dfma")]
+
+
+def launches(rep, what="bytes"):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     hdr, units = r[0], r[1]
     u = dict(zip(hdr, units))
     nb = lambda d, key: float(d[key]) * SCALE.get(u[key], 1.0)
-    return [(d["Kernel Name"], nb(d, "dram__bytes_read.sum") + nb(d, "dram__bytes_write.sum"))
-            for d in (dict(zip(hdr, x)) for x in r[2:])]
+
+    def ops(d):  # (summed over sub-partitions) per-cycle rates x elapsed cycles
+        cyc = float(d["smsp__cycles_elapsed.avg"])
+        return sum(float(d[k]) for k in FP64 if d.get(k) not in (None, "", "n/a")) * cyc
+
+    rows = [dict(zip(hdr, x)) for x in r[2:]]
+    if what == "fp64":
+        return [(d["Kernel Name"], ops(d)) for d in rows]
+    return [(d["Kernel Name"], nb(d, "dram__bytes_read.sum") + nb(d, "dram__bytes_write.sum")) for d in rows]
 
 
 def programs(seq):
@@ -43,6 +55,8 @@ def programs(seq):
             key = "tracer_2d"
         elif "remap_kernel" in name:
             key = "remap_tracers"
+        elif "remap_map" in name:
+            key = "remap_map"
         elif "halo" in name:
             key = "halo"
         else:
@@ -51,9 +65,12 @@ def programs(seq):
     return prog
 
 
-prog = {}
-for rep in sys.argv[1:]:
-    prog.update(programs(launches(rep)))
-prog["_source"] = "ncu --set full, " + ", ".join(Path(r).name for r in sys.argv[1:]) + ": dram__bytes_read.sum + dram__bytes_write.sum per launch"
-Path("profiles/traffic.json").write_text(json.dumps(prog, indent=1, sort_keys=True) + "\n")
-print(json.dumps(prog, indent=1))
+names = ", ".join(Path(r).name for r in sys.argv[1:])
+for what, path, src in (("bytes", "profiles/traffic.json", "dram__bytes_read.sum + dram__bytes_write.sum per launch"),
+                        ("fp64", "profiles/fp64.json", "fp64 thread operations (DADD + DMUL + DFMA) per launch")):
+    prog = {}
+    for rep in sys.argv[1:]:
+        prog.update({k: v for k, v in programs(launches(rep, what)).items() if v > 0 or what == "bytes"})
+    prog["_source"] = f"ncu --set full, {names}: {src}"
+    Path(path).write_text(json.dumps(prog, indent=1, sort_keys=True) + "\n")
+    print(json.dumps(prog, indent=1))
