@@ -29,6 +29,7 @@ BINDINGS = {
     "p_grad_d": ("interfaces", {}),
     "tracer_2d": ("layers", {"xfx": "xfa", "yfx": "yfa"}),
     "remap_tracers": ("interfaces", {}),
+    "remap_profile": ("interfaces", {}),
 }
 
 
@@ -53,9 +54,9 @@ class OracleDycore:
         self.docs = {n: interp.load_manifest(n) for n in BINDINGS}
         self.written = {n: _written(d) for n, d in self.docs.items()}
         h, nk = cfg.halo, cfg.nk
-        for t in range(cfg.nq):
+        for q in cfg.remapped():
             for a in ("a2", "a3", "a4"):
-                state.setdefault(f"q{t}_{a}", np.zeros_like(state["delp"]))
+                state.setdefault(f"{q}_{a}", np.zeros_like(state["delp"]))
         self._h = h
 
     def _slices(self, doc, name, nk_dom):
@@ -74,9 +75,10 @@ class OracleDycore:
                 sl.append(slice(0 + lo, nk_dom + hi))
         return tuple(sl)
 
-    def call(self, prog: str, consts: dict) -> None:
+    def call(self, prog: str, consts: dict, bind: dict | None = None) -> None:
         doc = self.docs[prog]
-        vert, bind = BINDINGS[prog]
+        vert, bind0 = BINDINGS[prog]
+        bind = {**bind0, **(bind or {})}
         nk_dom = self.cfg.nk if vert == "layers" else self.cfg.nk + 1
         inputs, slices = {}, {}
         for f in doc["program"]["fields"]:
@@ -118,8 +120,10 @@ class OracleDycore:
         yield cfg.tracer_names() + ["cx", "cy", "xfa", "yfa", "mfx", "mfy"]
         self.call("tracer_2d", c)
         self.call("remap_tracers", c)
+        for n in ("pt", "w"):  # the remap_profile program on each thermodynamic field
+            self.call("remap_profile", c, bind={"q": n, "a4_2": f"{n}_a2", "a4_3": f"{n}_a3", "a4_4": f"{n}_a4"})
         ak, bk = cfg.target_coordinate()
-        remap_map.remap_map(st, cfg.tracer_names(), ak, bk, cfg.nk, self._h)
+        remap_map.remap_map(st, cfg.remapped(), ak, bk, cfg.nk, self._h)
 
     def step(self) -> None:
         for names in self.phases():

@@ -13,8 +13,8 @@ One dycore timestep (k_split = 1):
         p_grad_d                                      -> u, v
     halo_update(q*, cx, cy, xfa, yfa, mfx, mfy)
     tracer_2d (nq tracers)                            -> q*
-    remap_tracers (remap_profile of every tracer)     -> q*_a2, q*_a3, q*_a4
-    remap_map (Lagrangian -> Eulerian, map1_ppm)      -> q*, delp
+    remap_tracers (remap_profile of q*, pt, w)        -> *_a2, *_a3, *_a4
+    remap_map (Lagrangian -> Eulerian, map1_ppm)      -> q*, pt, w, delp
 """
 
 from __future__ import annotations
@@ -49,6 +49,12 @@ class RunConfig:
 
     def tracer_names(self) -> list[str]:
         return [f"q{n}" for n in range(self.nq)]
+
+    def remapped(self) -> list[str]:
+        """Fields the vertical remapping maps onto the target layers: the
+        tracers, then pt and w (u and v, at staggered pressures, are not
+        remapped; DESIGN.md)."""
+        return self.tracer_names() + ["pt", "w"]
 
     def target_coordinate(self):
         """ak, bk (nk+1) of the vertical remapping's target interfaces

@@ -556,7 +556,7 @@ struct RemapMapArgs {
   int nq, ni, nj, nk;  // nk layers
 };
 
-constexpr int MP_COLS = 32, MP_TY = 8;
+constexpr int MP_COLS = 32, MP_TY = 16;  // blockDim.y = min(nq, MP_TY): one thread per (column, field)
 constexpr double MP_R3 = 1.0 / 3.0, MP_R23 = 2.0 / 3.0;  // the oracle's R3, R23 (same roundings)
 
 __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapMapArgs a) {
@@ -574,9 +574,10 @@ __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapM
   const int i = live ? cidx % a.ni : 0, j = live ? cidx / a.ni : 0;
   const int64_t off = i + (int64_t)j * a.sj, sk = a.sk;
   // stage delp (in pe1's slots 1..nk) and ak / bk with every warp: coalesced level rows
-  for (int k = ty; k < nk; k += MP_TY)
+  const int ny = blockDim.y;
+  for (int k = ty; k < nk; k += ny)
     if (live) P1[(k + 1) * MP_COLS + c] = __ldg(a.delp.o + off + k * sk);
-  for (int e = c + ty * MP_COLS; e <= nk; e += MP_COLS * MP_TY) {
+  for (int e = c + ty * MP_COLS; e <= nk; e += MP_COLS * ny) {
     AK[e] = __ldg(a.ak.o + e * a.ak.sk);
     BK[e] = __ldg(a.bk.o + e * a.bk.sk);
   }
@@ -592,12 +593,12 @@ __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapM
   __syncthreads();
   if (live) {
     const double ps = p1(nk);
-    for (int k = ty; k <= nk; k += MP_TY)
+    for (int k = ty; k <= nk; k += ny)
       P2[k * MP_COLS + c] = k == 0 ? p1(0) : (k == nk ? ps : AK[k] + BK[k] * ps);
   }
   __syncthreads();
   if (!live) return;
-  for (int t = ty; t < a.nq; t += MP_TY) {
+  for (int t = ty; t < a.nq; t += ny) {
     const double* Q = a.q[t] + off;
     const double* A2 = a.a2[t] + off;
     const double* A3 = a.a3[t] + off;
@@ -688,6 +689,7 @@ extern "C" int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int 
   if (bytes > 48 * 1024 &&
       cudaFuncSetAttribute(remap_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
     return check_launch("remap_map smem attribute");
-  remap_map_kernel<<<cdiv(a.ni * a.nj, MP_COLS), dim3(MP_COLS, MP_TY), bytes, (cudaStream_t)stream>>>(a);
+  remap_map_kernel<<<cdiv(a.ni * a.nj, MP_COLS), dim3(MP_COLS, a.nq < MP_TY ? a.nq : MP_TY), bytes,
+                     (cudaStream_t)stream>>>(a);
   return check_launch("remap_map");
 }

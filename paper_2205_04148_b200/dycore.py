@@ -53,7 +53,7 @@ class Dycore:
         self.dom_layers = self.grid.domain(placement, nk=cfg.nk)
         self.dom_ifaces = self.grid.domain(placement, nk=cfg.nk + 1)
         g = self.grid
-        names3 = STATE_3D + cfg.tracer_names() + [f"q{t}_{a}" for t in range(cfg.nq) for a in ("a2", "a3", "a4")]
+        names3 = STATE_3D + cfg.tracer_names() + [f"{q}_{a}" for q in cfg.remapped() for a in ("a2", "a3", "a4")]
         self.cur: dict[str, torch.Tensor] = {n: g.new3(device) for n in names3}
         self.cur.update({n: g.new2(device) for n in METRICS_2D})
         self.alt: dict[str, torch.Tensor] = {n: g.new3(device) for n in list(PINGPONG) + ["gz"] + cfg.tracer_names()}
@@ -172,10 +172,9 @@ class Dycore:
         Transfers run on an upload and a download stream (both PCIe
         directions at once) and overlap the compute they do not feed: the
         tracers' uploads run during the acoustic substeps (first needed by
-        tracer_2d); the dynamics fields other than delp are final after the
-        substeps and download during tracer advection and remapping; the
-        tracers and delp (rewritten by the remap mapping) download at the end
-        of the step.  Device staging is a ring (three input stages, two output
+        tracer_2d); u, v and gz are final after the substeps and download
+        during tracer advection and remapping; the tracers, delp, pt and w
+        (rewritten by the remap mapping) download at the end of the step.  Device staging is a ring (three input stages, two output
         stages), so successive calls pipeline: the next call's uploads
         overlap this call's compute, this call's downloads the next call's
         compute.  A call whose inputs are the previous call's outputs (a
@@ -185,7 +184,7 @@ class Dycore:
         tracers = set(self.cfg.tracer_names())
         trc = [n for n in h_in if n in tracers]           # uploaded during the substeps
         dyn = [n for n in h_in if n not in tracers]       # uploaded before the step
-        late = [n for n in h_in if n in tracers or n == "delp"]  # downloaded after remap_map
+        late = [n for n in h_in if n in tracers or n in ("delp", "pt", "w")]  # rewritten by remap_map
         early = [n for n in h_in if n not in late]
         stages = self._io_stages(list(h_in))
         si, so = self._io_calls % 3, self._io_calls % 2
@@ -301,15 +300,18 @@ class Dycore:
         self.swap(*qs)
 
     def remap(self) -> None:
+        """remap_profile of every remapped field (the tracers, then pt and w):
+        the remap_tracers program plus the remap_profile program per
+        thermodynamic field, in one launch."""
         fields = [self.f("delp")]
-        for q in self.cfg.tracer_names():
+        for q in self.cfg.remapped():
             fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4")]
         self.launch("remap_tracers", "fv3b_remap_profile", fields, [], self.dom_ifaces)
 
     def remap_map(self) -> None:
-        """Lagrangian -> Eulerian: every tracer's profile integrated over the
-        target layers (pe2 = ak + bk * ps), delp <- pe2 differences."""
-        qs = self.cfg.tracer_names()
+        """Lagrangian -> Eulerian: every remapped field's profile integrated
+        over the target layers (pe2 = ak + bk * ps), delp <- pe2 differences."""
+        qs = self.cfg.remapped()
         fields = [self.f("delp")] + [self.grid.abi(self.coord[n], rank=1) for n in ("ak", "bk")]
         for q in qs:
             fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4"), self.a(q)]
