@@ -13,6 +13,7 @@ struct DswTpArgs {
   double* pto;
   double* wo;
   const double* acci[6];  // interior origins of cx, cy, xfa, yfa, mfx, mfy
+  bool acc_reset;         // read the accumulator inputs as 0.0
   double* acco[6];        // and of their outputs (may alias the inputs)
   const double* rarea;  // interior origin (2-D)
   int64_t sj, sk;

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
     // accumulator inputs of this thread's cell (consumed in S4)
     double acc[6];
 #pragma unroll
-    for (int f = 0; f < 6; ++f) acc[f] = own ? a.acci[f][coff + (int64_t)k * sk] : 0.0;
+    for (int f = 0; f < 6; ++f) acc[f] = (own && !a.acc_reset) ? a.acci[f][coff + (int64_t)k * sk] : 0.0;
     // ---- S0: courant -------------------------------------------------------
     mbar_wait(&bar[0], (k - k0) & 1);
     for (int e = tid; e < L::XW * L::XH; e += NT) {

@@ -271,12 +271,15 @@ class Dycore:
         self.launch("c_grid", "fv3b_c_grid", fields,
                     [0.5 * dt, c["ptop"], c["rdgas"], c["grav"], c["gama"], c["p_fac"]], self.dom_ifaces)
 
-    def d_sw(self) -> None:
+    def d_sw(self, first: bool = False) -> None:
+        """``first``: the timestep's first substep, whose accumulator inputs
+        are the step's zeros (fv3b_d_sw's acc_reset)."""
         c, dt = self.cfg.consts, self.cfg.dt_acoustic
         fields = [self.f(n) for n in PINGPONG + ("uc", "vc") + ACCUM] + [self.f(m) for m in D_METRICS]
         fields += [self.a(n) for n in PINGPONG] + [self.f(n) for n in ACCUM]
         self.launch("d_sw", "fv3b_d_sw", fields,
-                    [c["ppm_p1"], c["ppm_p2"], dt, c["dddmp"], c["d2_bg"], c["da_min"], c["damp_w"]], self.dom_layers)
+                    [c["ppm_p1"], c["ppm_p2"], dt, c["dddmp"], c["d2_bg"], c["da_min"], c["damp_w"],
+                     1.0 if first else 0.0], self.dom_layers)
         self.swap(*PINGPONG)
 
     def nh_d(self) -> None:
@@ -324,14 +327,14 @@ class Dycore:
         (the caller performs the update; a decomposed run exchanges them
         between ranks, parallel.py)."""
         cfg = self.cfg
-        for n in ACCUM:
-            self.cur[n].zero_()
+        # the accumulators start the step at zero: the first d_sw reads them
+        # as 0.0 (acc_reset) instead of a zero fill
         self.cur["dp1"].copy_(self.cur["delp"])
-        for _ in range(cfg.n_split):
+        for it in range(cfg.n_split):
             yield ["u", "v", "w", "delp", "pt", "gz"]
             self.c_grid()
             yield ["uc", "vc"]
-            self.d_sw()
+            self.d_sw(first=it == 0)
             self.nh_d()
             yield ["pef", "gz"]
             self.p_grad_d()
