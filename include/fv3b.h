@@ -129,8 +129,9 @@ int fv3b_c_grid(const fv3b_field* f, int nf, const double* s, int ns,
  *     w, delp, pt, uc, vc, cx, cy, xfa, yfa, mfx, mfy (3-D); dx, dy, dxc, dyc,
  *     rdx, rdy, rdxa, rdya, area, rarea, rarea_c, f0 (2-D); u, v, w, delp, pt,
  *     cx, cy, xfa, yfa, mfx, mfy outputs (3-D; accumulators may alias).
- *     scalars: ppm_p1, ppm_p2, dt, dddmp, d2_bg, da_min, damp_w [, acc_reset:
- *     nonzero reads the accumulator inputs as 0.0]. */
+ *     [optional 37th: dp1_out, receives the input delp].  scalars: ppm_p1,
+ *     ppm_p2, dt, dddmp, d2_bg, da_min, damp_w [, acc_reset: nonzero reads
+ *     the accumulator inputs as 0.0]. */
 int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns,
               const fv3b_domain* d, void* stream);
 

@@ -35,10 +35,12 @@ using namespace fv3b;
 // (pointwise update); the others must not.  scalars: ppm_p1, ppm_p2, dt,
 // dddmp, d2_bg, da_min, damp_w, and optionally acc_reset: nonzero reads the
 // accumulator inputs as 0.0 (the first substep of a timestep, where the step
-// zeroes them: 0.0 + x is the same sum, so the zero fill is skipped).
+// zeroes them: 0.0 + x is the same sum, so the zero fill is skipped).  An
+// optional 37th field receives a copy of the input delp (the timestep's dp1,
+// saved by the first substep instead of a separate copy).
 extern "C" int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d, void* stream) {
-  if (f == nullptr || d == nullptr || s == nullptr || nf != 36 || (ns != 7 && ns != 8))
-    return fail(FV3B_EINVAL, "fv3b_d_sw: expects 36 fields, 7 or 8 scalars (got %d, %d)", nf, ns);
+  if (f == nullptr || d == nullptr || s == nullptr || (nf != 36 && nf != 37) || (ns != 7 && ns != 8))
+    return fail(FV3B_EINVAL, "fv3b_d_sw: expects 36 or 37 fields, 7 or 8 scalars (got %d, %d)", nf, ns);
   DswArgs a;
   const Halo h0 = {0, 0, 0, 0, 0, 0}, h3 = {3, 3, 3, 3, 0, 0};
   const Halo hu = {3, 3, 3, 4, 0, 0}, hv = {3, 4, 3, 3, 0, 0}, huc = {0, 1, 3, 3, 0, 0}, hvc = {3, 3, 0, 1, 0, 0};
@@ -105,6 +107,14 @@ extern "C" int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns, c
     t.ni = d->ni; t.nj = d->nj; t.nk = d->nk;
     t.p1 = a.p1; t.p2 = a.p2; t.dt = a.dt; t.damp_w = a.damp_w;
     t.acc_reset = ns == 8 && s[7] != 0.0;
+    t.dp1o = nullptr;
+    if (nf == 37) {
+      View v;
+      FV3B_TRY(view_of(f[36], 3, *d, h0, "dp1_out", &v));
+      if (v.sj != a.u.sj || v.sk != a.u.sk) return fail(FV3B_ELAYOUT, "fv3b_d_sw: dp1_out strides differ");
+      if (f[36].data == f[3].data) return fail(FV3B_EINVAL, "fv3b_d_sw: dp1_out aliases delp");
+      t.dp1o = v.o;
+    }
     FV3B_TRY(launch_dsw_transport(t, st));
   }
   // momentum group (u, v): TMA-pipelined level march

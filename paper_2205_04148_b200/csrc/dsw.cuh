@@ -14,6 +14,7 @@ struct DswTpArgs {
   double* wo;
   const double* acci[6];  // interior origins of cx, cy, xfa, yfa, mfx, mfy
   bool acc_reset;         // read the accumulator inputs as 0.0
+  double* dp1o;           // optional: copy of the input delp (interior origin)
   double* acco[6];        // and of their outputs (may alias the inputs)
   const double* rarea;  // interior origin (2-D)
   int64_t sj, sk;

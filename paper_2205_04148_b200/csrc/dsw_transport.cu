@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
       if (own) {
         const int64_t off = coff + (int64_t)k * sk;
         a.delpo[off] = dn;
+        if (a.dp1o) a.dp1o[off] = dp;
         a.pto[off] = (ptc * dp + divp) / dn;
         a.wo[off] = (wc * dp + divw) / dn + a.damp_w * (wl + wr + wsth + wnth - 4.0 * wc);
         // cx += crx, cy += cry, xfa += xfx, yfa += yfx, mfx += fxm, mfy += fym

@@ -273,10 +273,13 @@ class Dycore:
 
     def d_sw(self, first: bool = False) -> None:
         """``first``: the timestep's first substep, whose accumulator inputs
-        are the step's zeros (fv3b_d_sw's acc_reset)."""
+        are the step's zeros (fv3b_d_sw's acc_reset) and which saves the
+        step's dp1 (the delp it reads)."""
         c, dt = self.cfg.consts, self.cfg.dt_acoustic
         fields = [self.f(n) for n in PINGPONG + ("uc", "vc") + ACCUM] + [self.f(m) for m in D_METRICS]
         fields += [self.a(n) for n in PINGPONG] + [self.f(n) for n in ACCUM]
+        if first:
+            fields.append(self.f("dp1"))  # the step's dp1 = delp at the step start
         self.launch("d_sw", "fv3b_d_sw", fields,
                     [c["ppm_p1"], c["ppm_p2"], dt, c["dddmp"], c["d2_bg"], c["da_min"], c["damp_w"],
                      1.0 if first else 0.0], self.dom_layers)
@@ -327,9 +330,9 @@ class Dycore:
         (the caller performs the update; a decomposed run exchanges them
         between ranks, parallel.py)."""
         cfg = self.cfg
-        # the accumulators start the step at zero: the first d_sw reads them
-        # as 0.0 (acc_reset) instead of a zero fill
-        self.cur["dp1"].copy_(self.cur["delp"])
+        # the accumulators start the step at zero and dp1 is the delp of the
+        # step start: the first d_sw reads the former as 0.0 (acc_reset) and
+        # writes the latter (its delp input) instead of a fill and a copy
         for it in range(cfg.n_split):
             yield ["u", "v", "w", "delp", "pt", "gz"]
             self.c_grid()
