@@ -22,6 +22,7 @@
 // phase B of delp | phase B of pt, w; then each thread updates its own cell.
 #include "common.cuh"
 #include "dsw.cuh"
+#include "fastdiv.cuh"
 #include "ppm.cuh"
 #include "tma.cuh"
 
@@ -184,6 +185,84 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
       }
     }
   };
+  // phase A of all three quantities for item `it`: the inner-update
+  // denominators (area + yfx - yfx[j+1], area + xfx - xfx[i+1]) are the
+  // same for delp, pt and w, so each cell's reciprocal is refined once and
+  // the three quotients take nvcc's fast-path residual step (fastdiv.cuh:
+  // bitwise a / b); an item whose range test fails is redone with `/`.
+  auto phase_a3 = [&](int it) {
+    if (it < NY) {
+      const int c = it % NCY - 3, jb = (it / NCY) * SEG;
+      double den[SEG], rd[SEG], ar[SEG], y0[SEG], y1[SEG];
+#pragma unroll
+      for (int u = 0; u < SEG; ++u) {
+        const int j = jb + u;
+        ar[u] = *QB(sarea, c, j);
+        y0[u] = *CY(syfx, c, j);
+        y1[u] = *CY(syfx, c, j + 1);
+        den[u] = ar[u] + y0[u] - y1[u];
+        rd[u] = rcp_fast(den[u]);
+      }
+      bool ok = true;
+#pragma unroll 1
+      for (int q = 0; q < 3; ++q) {
+        const double* Q = sdp + q * L::n_q;
+        double* sqi = SQI(q);
+        double* sfy2 = SFY2(q);
+        double f[SEG + 1];
+        ppm_line<SEG + 1>(QB(Q, c, jb), L::QW, CY(scry, c, jb), L::YW, p1, p2, f);
+#pragma unroll
+        for (int u = 0; u < SEG; ++u) {
+          const int j = jb + u;
+          const double num = *QB(Q, c, j) * ar[u] + f[u] * y0[u] - f[u + 1] * y1[u];
+          double v = div_fast_r(num, den[u], rd[u], ok);
+          sqi[j * L::QW + c + 4] = v;
+        }
+        if (c >= 0 && c < TI) {
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) sfy2[(jb + u) * TI + c] = f[u];
+          if (jb + SEG == TJ) sfy2[TJ * TI + c] = f[SEG];
+        }
+      }
+      if (!ok)
+        for (int q = 0; q < 3; ++q) phase_a(q, it);
+    } else {
+      const int r = it - NY;
+      const int rj = r % NRX - 3, ib = (r / NRX) * SEG;
+      double den[SEG], rd[SEG], ar[SEG], x0[SEG], x1[SEG];
+#pragma unroll
+      for (int u = 0; u < SEG; ++u) {
+        const int i = ib + u;
+        ar[u] = *QB(sarea, i, rj);
+        x0[u] = *CX(sxfx, i, rj);
+        x1[u] = *CX(sxfx, i + 1, rj);
+        den[u] = ar[u] + x0[u] - x1[u];
+        rd[u] = rcp_fast(den[u]);
+      }
+      bool ok = true;
+#pragma unroll 1
+      for (int q = 0; q < 3; ++q) {
+        const double* Q = sdp + q * L::n_q;
+        double* sqj = SQJ(q);
+        double* sfx2 = SFX2(q);
+        double f[SEG + 1];
+        ppm_line<SEG + 1>(QB(Q, ib, rj), 1, CX(scrx, ib, rj), 1, p1, p2, f);
+#pragma unroll
+        for (int u = 0; u < SEG; ++u) {
+          const int i = ib + u;
+          const double num = *QB(Q, i, rj) * ar[u] + f[u] * x0[u] - f[u + 1] * x1[u];
+          sqj[(rj + 3) * L::JW + i] = div_fast_r(num, den[u], rd[u], ok);
+        }
+        if (rj >= 0 && rj < TJ) {
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) sfx2[rj * L::XW + ib + u] = f[u];
+          if (ib + SEG == TI) sfx2[rj * L::XW + TI] = f[SEG];
+        }
+      }
+      if (!ok)
+        for (int q = 0; q < 3; ++q) phase_a(q, it);
+    }
+  };
   // phase B of quantity q, item `it` (0 <= it < NB): weighted fluxes into FLX/FLY(q)
   auto phase_b = [&](int q, int it) {
     if (it < NX2) {
@@ -241,7 +320,7 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
     }
     __syncthreads();
     // ---- S1: phase A of delp, pt, w ------------------------------------------
-    for (int e = tid; e < 3 * NA; e += NT) phase_a(e / NA, e % NA);
+    for (int e = tid; e < NA; e += NT) phase_a3(e);
     __syncthreads();
     // ---- S2: phase B of delp (mass fluxes); stage values of the update cell ---
     if (tid < NB) phase_b(0, tid);
@@ -281,8 +360,17 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
         const int64_t off = coff + (int64_t)k * sk;
         a.delpo[off] = dn;
         if (a.dp1o) a.dp1o[off] = dp;
-        a.pto[off] = (ptc * dp + divp) / dn;
-        a.wo[off] = (wc * dp + divw) / dn + a.damp_w * (wl + wr + wsth + wnth - 4.0 * wc);
+        // pt' and w' share the divisor delpn: one refined reciprocal (fastdiv.cuh)
+        bool ok = true;
+        const double rdn = rcp_fast(dn);
+        double ptn = div_fast_r(ptc * dp + divp, dn, rdn, ok);
+        double wq = div_fast_r(wc * dp + divw, dn, rdn, ok);
+        if (!ok) {
+          ptn = (ptc * dp + divp) / dn;
+          wq = (wc * dp + divw) / dn;
+        }
+        a.pto[off] = ptn;
+        a.wo[off] = wq + a.damp_w * (wl + wr + wsth + wnth - 4.0 * wc);
         // cx += crx, cy += cry, xfa += xfx, yfa += yfx, mfx += fxm, mfy += fym
         a.acco[0][off] = acc[0] + crx;
         a.acco[1][off] = acc[1] + cry;
