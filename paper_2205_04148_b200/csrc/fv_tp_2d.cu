@@ -26,6 +26,7 @@
 // shared Courant numbers / fluxes / dp1 are fetched once per level for all
 // tracers and every barrier interval carries TG tracers' work.
 #include "common.cuh"
+#include "fastdiv.cuh"
 #include "ppm.cuh"
 #include "tma.cuh"
 
@@ -283,7 +284,9 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ>())) tp_kernel(const _
 // tracer_2d, group schedule. The tracers of one level are processed TG at a
 // time; per group two barrier intervals:
 //   A: cell updates of the previous group (one cell per thread: dp2 from
-//      registers, q' written straight to HBM) + phase A of all TG tracers;
+//      registers, q' written straight to HBM) + phase A of all TG tracers
+//      (one item per thread covers the group: the tracers share the inner
+//      update's denominators, whose reciprocals are refined once);
 //   B: phase B of all TG tracers (fluxes fx, fy to shared memory).
 // Twice the work per barrier of tp_kernel, every thread busy in phase B, and
 // the mass-flux divergence dp2 computed once per level in registers.
@@ -423,48 +426,83 @@ __global__ void __launch_bounds__(TI * TJ, 2) tracer2_kernel(const __grid_consta
 
     // ---- interval A: previous group's cell updates; phase A ------------------
     if (s > 0) update(s - 1);
-    // y items of every tracer first, then x items (warps stay on one path)
-    for (int item = tid; item < cnt * (NY + NX); item += NT) {
-      if (item < cnt * NY) {
-        const int c = item / NY, it = item % NY;
-        const double* sq = qstage(s, c);
-        double* st = smem + L::o_set + c * L::n_set;
-        const int ci = it % NCY - 3, jb = (it / NCY) * SEG;
-        double f[SEG + 1];
-        ppm_line<SEG + 1>(sq + (jb + 3) * B::QW + ci + 4, B::QW, CY(scry, ci, jb), B::YW, p1, p2, f);
+    // one item for every tracer of the group: the inner-update denominators
+    // are the tracers' common ones, so each cell's reciprocal is refined once
+    // (fastdiv.cuh: bitwise a / b; an item outside the fast-path range is
+    // redone with `/`)
+    for (int item = tid; item < NY + NX; item += NT) {
+      if (item < NY) {
+        const int ci = item % NCY - 3, jb = (item / NCY) * SEG;
+        double ar[SEG], y0[SEG], y1[SEG], den[SEG], rd[SEG];
 #pragma unroll
         for (int u = 0; u < SEG; ++u) {
           const int j = jb + u;
-          const double ar = sarea[(j + 3) * B::QW + ci + 4];
-          const double y0 = *CY(syfx, ci, j), y1 = *CY(syfx, ci, j + 1);
-          st[L::s_qi + j * B::QW + ci + 4] = (sq[(j + 3) * B::QW + ci + 4] * ar + f[u] * y0 - f[u + 1] * y1) /
-                                             (ar + y0 - y1);
+          ar[u] = sarea[(j + 3) * B::QW + ci + 4];
+          y0[u] = *CY(syfx, ci, j);
+          y1[u] = *CY(syfx, ci, j + 1);
+          den[u] = ar[u] + y0[u] - y1[u];
+          rd[u] = rcp_fast(den[u]);
         }
-        if (ci >= 0 && ci < TI) {
+#pragma unroll 1
+        for (int c = 0; c < cnt; ++c) {
+          const double* sq = qstage(s, c);
+          double* st = smem + L::o_set + c * L::n_set;
+          double f[SEG + 1];
+          ppm_line<SEG + 1>(sq + (jb + 3) * B::QW + ci + 4, B::QW, CY(scry, ci, jb), B::YW, p1, p2, f);
+          bool ok = true;
+          double v[SEG];
 #pragma unroll
-          for (int u = 0; u < SEG; ++u) st[L::s_fy2 + (jb + u) * TI + ci] = f[u];
-          if (jb + SEG == TJ) st[L::s_fy2 + TJ * TI + ci] = f[SEG];
+          for (int u = 0; u < SEG; ++u)
+            v[u] = div_fast_r(sq[(jb + u + 3) * B::QW + ci + 4] * ar[u] + f[u] * y0[u] - f[u + 1] * y1[u], den[u],
+                              rd[u], ok);
+          if (!ok)
+#pragma unroll
+            for (int u = 0; u < SEG; ++u)
+              v[u] = (sq[(jb + u + 3) * B::QW + ci + 4] * ar[u] + f[u] * y0[u] - f[u + 1] * y1[u]) / den[u];
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) st[L::s_qi + (jb + u) * B::QW + ci + 4] = v[u];
+          if (ci >= 0 && ci < TI) {
+#pragma unroll
+            for (int u = 0; u < SEG; ++u) st[L::s_fy2 + (jb + u) * TI + ci] = f[u];
+            if (jb + SEG == TJ) st[L::s_fy2 + TJ * TI + ci] = f[SEG];
+          }
         }
       } else {
-        const int x = item - cnt * NY;
-        const int c = x / NX, it = x % NX;
-        const double* sq = qstage(s, c);
-        double* st = smem + L::o_set + c * L::n_set;
+        const int it = item - NY;
         const int rj = it % NRX - 3, ib = (it / NRX) * SEG;
-        double f[SEG + 1];
-        ppm_line<SEG + 1>(sq + (rj + 3) * B::QW + ib + 4, 1, CX(scrx, ib, rj), 1, p1, p2, f);
+        double ar[SEG], x0[SEG], x1[SEG], den[SEG], rd[SEG];
 #pragma unroll
         for (int u = 0; u < SEG; ++u) {
           const int i = ib + u;
-          const double ar = sarea[(rj + 3) * B::QW + i + 4];
-          const double x0 = *CX(sxfx, i, rj), x1 = *CX(sxfx, i + 1, rj);
-          st[L::s_qj + (rj + 3) * B::JW + i] = (sq[(rj + 3) * B::QW + i + 4] * ar + f[u] * x0 - f[u + 1] * x1) /
-                                               (ar + x0 - x1);
+          ar[u] = sarea[(rj + 3) * B::QW + i + 4];
+          x0[u] = *CX(sxfx, i, rj);
+          x1[u] = *CX(sxfx, i + 1, rj);
+          den[u] = ar[u] + x0[u] - x1[u];
+          rd[u] = rcp_fast(den[u]);
         }
-        if (rj >= 0 && rj < TJ) {
+#pragma unroll 1
+        for (int c = 0; c < cnt; ++c) {
+          const double* sq = qstage(s, c);
+          double* st = smem + L::o_set + c * L::n_set;
+          double f[SEG + 1];
+          ppm_line<SEG + 1>(sq + (rj + 3) * B::QW + ib + 4, 1, CX(scrx, ib, rj), 1, p1, p2, f);
+          bool ok = true;
+          double v[SEG];
 #pragma unroll
-          for (int u = 0; u < SEG; ++u) st[L::s_fx2 + rj * B::XW + ib + u] = f[u];
-          if (ib + SEG == TI) st[L::s_fx2 + rj * B::XW + TI] = f[SEG];
+          for (int u = 0; u < SEG; ++u)
+            v[u] = div_fast_r(sq[(rj + 3) * B::QW + ib + u + 4] * ar[u] + f[u] * x0[u] - f[u + 1] * x1[u], den[u],
+                              rd[u], ok);
+          if (!ok)
+#pragma unroll
+            for (int u = 0; u < SEG; ++u)
+              v[u] = (sq[(rj + 3) * B::QW + ib + u + 4] * ar[u] + f[u] * x0[u] - f[u + 1] * x1[u]) / den[u];
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) st[L::s_qj + (rj + 3) * B::JW + ib + u] = v[u];
+          if (rj >= 0 && rj < TJ) {
+#pragma unroll
+            for (int u = 0; u < SEG; ++u) st[L::s_fx2 + rj * B::XW + ib + u] = f[u];
+            if (ib + SEG == TI) st[L::s_fx2 + rj * B::XW + TI] = f[SEG];
+          }
         }
       }
     }
