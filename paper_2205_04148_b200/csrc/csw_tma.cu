@@ -15,6 +15,7 @@
 // results are bitwise the interpreter's.
 #include "common.cuh"
 #include "csw.cuh"
+#include "fastdiv.cuh"
 #include "tma.cuh"
 
 namespace fv3b {
@@ -195,8 +196,18 @@ __global__ void __launch_bounds__(CS_NT, 2) csw_kernel(const __grid_constant__ C
         const double dpc = dp + (fx0 - fx1 + fy0 - fy1) * ra;
         const int64_t off = gi + gj * sj + (int64_t)k * sk;
         a.delpc[off] = dpc;
-        a.ptc[off] = (B(PT, i, j) * dp + (fxp0 - fxp1 + fyp0 - fyp1) * ra) / dpc;
-        a.wc[off] = (B(WW, i, j) * dp + (fxw0 - fxw1 + fyw0 - fyw1) * ra) / dpc;
+        // ptc and wc share the divisor delpc: one refined reciprocal (fastdiv.cuh)
+        const double np = B(PT, i, j) * dp + (fxp0 - fxp1 + fyp0 - fyp1) * ra;
+        const double nw = B(WW, i, j) * dp + (fxw0 - fxw1 + fyw0 - fyw1) * ra;
+        bool ok = true;
+        const double r = rcp_fast(dpc);
+        double vp = div_fast_r(np, dpc, r, ok), vw = div_fast_r(nw, dpc, r, ok);
+        if (!ok) {
+          vp = np / dpc;
+          vw = nw / dpc;
+        }
+        a.ptc[off] = vp;
+        a.wc[off] = vw;
       }
     }
     pend_k = k;
