@@ -19,6 +19,7 @@
 // so results are bitwise the reference's.
 #include "common.cuh"
 #include "dsw.cuh"
+#include "fastdiv.cuh"
 #include "ppm.cuh"
 #include "tma.cuh"
 
@@ -224,13 +225,23 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
           const int ci = item % NCY - 3, jb = (item / NCY) * SEG;
           double f[SEG + 1];
           ppm_line<SEG + 1>(QB(swk, ci, jb), L::QW, CY(scry, ci, jb), L::YW, p1, p2, f);
+          // branch-free fast-path quotients, one exact fallback per item (fastdiv.cuh)
+          double num[SEG], den[SEG], v[SEG];
+          bool ok = true;
 #pragma unroll
           for (int u = 0; u < SEG; ++u) {
             const int j = jb + u;
             const double ar = *QB(sarea, ci, j);
             const double y0 = *CY(syfx, ci, j), y1 = *CY(syfx, ci, j + 1);
-            sqi[j * L::QW + ci + 4] = (*QB(swk, ci, j) * ar + f[u] * y0 - f[u + 1] * y1) / (ar + y0 - y1);
+            num[u] = *QB(swk, ci, j) * ar + f[u] * y0 - f[u + 1] * y1;
+            den[u] = ar + y0 - y1;
+            v[u] = div_fast(num[u], den[u], ok);
           }
+          if (!ok)
+#pragma unroll
+            for (int u = 0; u < SEG; ++u) v[u] = num[u] / den[u];
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) sqi[(jb + u) * L::QW + ci + 4] = v[u];
           if (ci >= 0 && ci < TI) {
 #pragma unroll
             for (int u = 0; u < SEG; ++u) sfy2[(jb + u) * TI + ci] = f[u];
@@ -241,13 +252,22 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
           const int rj = it % NRX - 3, ib = (it / NRX) * SEG;
           double f[SEG + 1];
           ppm_line<SEG + 1>(QB(swk, ib, rj), 1, CX(scrx, ib, rj), 1, p1, p2, f);
+          double num[SEG], den[SEG], v[SEG];
+          bool ok = true;
 #pragma unroll
           for (int u = 0; u < SEG; ++u) {
             const int i = ib + u;
             const double ar = *QB(sarea, i, rj);
             const double x0 = *CX(sxfx, i, rj), x1 = *CX(sxfx, i + 1, rj);
-            sqj[(rj + 3) * L::JW + i] = (*QB(swk, i, rj) * ar + f[u] * x0 - f[u + 1] * x1) / (ar + x0 - x1);
+            num[u] = *QB(swk, i, rj) * ar + f[u] * x0 - f[u + 1] * x1;
+            den[u] = ar + x0 - x1;
+            v[u] = div_fast(num[u], den[u], ok);
           }
+          if (!ok)
+#pragma unroll
+            for (int u = 0; u < SEG; ++u) v[u] = num[u] / den[u];
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) sqj[(rj + 3) * L::JW + ib + u] = v[u];
           if (rj >= 0 && rj < TJ) {
 #pragma unroll
             for (int u = 0; u < SEG; ++u) sfx2[rj * L::XW + ib + u] = f[u];
