@@ -212,13 +212,23 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ>())) tp_kernel(const _
           const int ci = item % NCY - 3, jb = (item / NCY) * SEG;
           double f[SEG + 1];
           ppm_line<SEG + 1>(Q(ci, jb), L::QW, CY(scry, ci, jb), L::YW, p1, p2, f);
+          // branch-free fast-path quotients, one exact fallback per item (fastdiv.cuh)
+          double num[SEG], den[SEG], v[SEG];
+          bool ok = true;
 #pragma unroll
           for (int u = 0; u < SEG; ++u) {
             const int j = jb + u;
             const double ar = sarea[(j + 3) * L::QW + ci + 4];
             const double y0 = *CY(syfx, ci, j), y1 = *CY(syfx, ci, j + 1);
-            sqi[j * L::QW + ci + 4] = (*Q(ci, j) * ar + f[u] * y0 - f[u + 1] * y1) / (ar + y0 - y1);
+            num[u] = *Q(ci, j) * ar + f[u] * y0 - f[u + 1] * y1;
+            den[u] = ar + y0 - y1;
+            v[u] = div_fast(num[u], den[u], ok);
           }
+          if (!ok)
+#pragma unroll
+            for (int u = 0; u < SEG; ++u) v[u] = num[u] / den[u];
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) sqi[(jb + u) * L::QW + ci + 4] = v[u];
           if (ci >= 0 && ci < TI) {
 #pragma unroll
             for (int u = 0; u < SEG; ++u) sfy2[(jb + u) * TI + ci] = f[u];
@@ -229,13 +239,22 @@ __global__ void __launch_bounds__(nt_of<TJ>(), (cps_of<TJ>())) tp_kernel(const _
           const int rj = it % NRX - 3, ib = (it / NRX) * SEG;
           double f[SEG + 1];
           ppm_line<SEG + 1>(Q(ib, rj), 1, CX(scrx, ib, rj), 1, p1, p2, f);
+          double num[SEG], den[SEG], v[SEG];
+          bool ok = true;
 #pragma unroll
           for (int u = 0; u < SEG; ++u) {
             const int i = ib + u;
             const double ar = sarea[(rj + 3) * L::QW + i + 4];
             const double x0 = *CX(sxfx, i, rj), x1 = *CX(sxfx, i + 1, rj);
-            sqj[(rj + 3) * L::JW + i] = (*Q(i, rj) * ar + f[u] * x0 - f[u + 1] * x1) / (ar + x0 - x1);
+            num[u] = *Q(i, rj) * ar + f[u] * x0 - f[u + 1] * x1;
+            den[u] = ar + x0 - x1;
+            v[u] = div_fast(num[u], den[u], ok);
           }
+          if (!ok)
+#pragma unroll
+            for (int u = 0; u < SEG; ++u) v[u] = num[u] / den[u];
+#pragma unroll
+          for (int u = 0; u < SEG; ++u) sqj[(rj + 3) * L::JW + ib + u] = v[u];
           if (rj >= 0 && rj < TJ) {
 #pragma unroll
             for (int u = 0; u < SEG; ++u) sfx2[rj * L::XW + ib + u] = f[u];
