@@ -316,7 +316,9 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     progs = [n for n in per_node if n != "halo"]
     doms = {n: (cfg.ni, cfg.nj, nk_prog.get(n, cfg.nk)) for n in progs}
     if "remap_map" in doms:
-        doms["remap_map"] = (cfg.ni, cfg.nj, cfg.nk + 1, cfg.nq)
+        doms["remap_map"] = (cfg.ni, cfg.nj, cfg.nk + 1, len(cfg.remapped()))
+    if "remap_tracers" in doms:
+        doms["remap_tracers"] = (cfg.ni, cfg.nj, cfg.nk + 1, len(cfg.remapped()))
     report = perf_model.build_report({n: per_node[n] for n in progs}, doms, peak * 1e9)
     by = {e.kernel: e for e in report.entries}
     top = max(progs, key=lambda n: node_total[n])

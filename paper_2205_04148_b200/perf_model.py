@@ -37,6 +37,13 @@ def unique_bytes(program: str, domain) -> tuple[int, str]:
         cells = ni * nj * (nki - 1)
         # delp read and rewritten; per tracer q, a4_2, a4_3, a4_4 read, q_out written; ak, bk
         return 8 * (cells * (2 + 5 * nq) + 2 * nki), "analytic (each operand level once: upper bound)"
+    if program == "remap_tracers" and len(domain) == 4:
+        # the program profiles 8 tracers; the timestep's launch profiles `nfields`
+        # fields of the same shape (bytes scale per field, delp aside)
+        b8, src = unique_bytes(program, domain[:3])
+        cells = domain[0] * domain[1] * domain[2]
+        per = (b8 - 8 * cells) / 8
+        return int(8 * cells + per * domain[3]), src + f", scaled to {domain[3]} fields"
     key = f"{program}@{domain[0]}x{domain[1]}x{domain[2]}"
     if _TABLE.exists():
         tab = json.loads(_TABLE.read_text())
