@@ -200,6 +200,14 @@ int fv3b_halo_scatter(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_transpose(const fv3b_field* f, int nf, const double* s, int ns,
                    const fv3b_domain* d, void* stream);
 
+/*   fv3b_selftest_fastmath  diagnostic: over n device operand pairs, adds to
+ *                   counts[0..3] (device, zeroed by the caller) the fast-path
+ *                   quotients x/y that differ from IEEE division although
+ *                   valid, the rejected ones, and the same two counts for
+ *                   det_log(|x|).  counts[0] and counts[2] must stay 0. */
+int fv3b_selftest_fastmath(const double* x, const double* y, int n,
+                           unsigned long long* counts, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

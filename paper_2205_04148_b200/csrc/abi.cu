@@ -135,3 +135,37 @@ int geo_of(const fv3b_field& f, Geo* g) {
 }
 
 }  // namespace fv3b
+
+// ---------------------------------------------------------------------------
+// Self-test of the branch-free fast paths (fastdiv.cuh) against the exact
+// operators (IEEE division, det_log): counts, over n operand pairs, the
+// results that differ although the fast path reported them valid (must be
+// 0), and the fast-path rejections (operands the kernels re-evaluate with
+// the exact operators).
+#include "fastdiv.cuh"
+
+namespace fv3b {
+__global__ void selftest_fastmath_kernel(const double* x, const double* y, int n, unsigned long long* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool ok = true;
+  const double q = div_fast(x[i], y[i], ok);
+  const double e = x[i] / y[i];
+  if (ok && __double_as_longlong(q) != __double_as_longlong(e)) atomicAdd(&out[0], 1ull);
+  if (!ok) atomicAdd(&out[1], 1ull);
+  bool ok2 = true;
+  const double lg = det_log_fast(fabs(x[i]), ok2);
+  const double el = det_log(fabs(x[i]));
+  if (ok2 && __double_as_longlong(lg) != __double_as_longlong(el)) atomicAdd(&out[2], 1ull);
+  if (!ok2) atomicAdd(&out[3], 1ull);
+}
+}  // namespace fv3b
+
+extern "C" int fv3b_selftest_fastmath(const double* x, const double* y, int n, unsigned long long* counts,
+                                      void* stream) {
+  if (x == nullptr || y == nullptr || counts == nullptr || n < 0)
+    return fv3b::fail(FV3B_EINVAL, "fv3b_selftest_fastmath: bad arguments");
+  if (n == 0) return FV3B_OK;
+  fv3b::selftest_fastmath_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(x, y, n, counts);
+  return fv3b::check_launch("fv3b_selftest_fastmath");
+}
