@@ -556,7 +556,11 @@ struct RemapMapArgs {
   int nq, ni, nj, nk;  // nk layers
 };
 
-constexpr int MP_COLS = 32, MP_TY = 16;  // blockDim.y = min(nq, MP_TY): one thread per (column, field)
+#ifndef FV3B_MP_F
+#define FV3B_MP_F 2
+#endif
+constexpr int MP_F = FV3B_MP_F;           // fields per thread
+constexpr int MP_COLS = 32, MP_TY = 16;  // blockDim.y = min(ceil(nq / MP_F), MP_TY)
 constexpr double MP_R3 = 1.0 / 3.0, MP_R23 = 2.0 / 3.0;  // the oracle's R3, R23 (same roundings)
 
 __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapMapArgs a) {
@@ -598,12 +602,27 @@ __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapM
   }
   __syncthreads();
   if (!live) return;
-  for (int t = ty; t < a.nq; t += ny) {
-    const double* Q = a.q[t] + off;
-    const double* A2 = a.a2[t] + off;
-    const double* A3 = a.a3[t] + off;
-    const double* A4 = a.a4[t] + off;
-    double* QO = a.qo[t] + off;
+  // MP_F fields per thread: map1_ppm's source-layer search depends on pe1 /
+  // pe2 only, so it is done once for the thread's fields, whose loads are
+  // independent (MP_F-fold memory-level parallelism in the level loop).
+  for (int t0 = ty; t0 < a.nq; t0 += ny * MP_F) {
+    const double* Q[MP_F];
+    const double* A2[MP_F];
+    const double* A3[MP_F];
+    const double* A4[MP_F];
+    double* QO[MP_F];
+    bool on[MP_F];
+#pragma unroll
+    for (int f = 0; f < MP_F; ++f) {
+      const int t = t0 + f * ny;
+      on[f] = t < a.nq;
+      const int tt = on[f] ? t : t0;
+      Q[f] = a.q[tt] + off;
+      A2[f] = a.a2[tt] + off;
+      A3[f] = a.a3[tt] + off;
+      A4[f] = a.a4[tt] + off;
+      QO[f] = a.qo[tt] + off;
+    }
     int k0 = 0;
     for (int k2 = 0; k2 < nk; ++k2) {
       const double top = p2(k2), bot = p2(k2 + 1);
@@ -612,29 +631,50 @@ __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapM
       const double pk = p1(k1), pn = p1(k1 + 1);
       const double d = pn - pk;
       const double pl = (top - pk) / d;
-      const double b2 = __ldg(A2 + k1 * sk), b3 = __ldg(A3 + k1 * sk), b4 = __ldg(A4 + k1 * sk);
+      double b2[MP_F], b3[MP_F], b4[MP_F];
+#pragma unroll
+      for (int f = 0; f < MP_F; ++f) {
+        b2[f] = __ldg(A2[f] + k1 * sk);
+        b3[f] = __ldg(A3[f] + k1 * sk);
+        b4[f] = __ldg(A4[f] + k1 * sk);
+      }
       if (bot <= pn) {  // the whole target layer lies in source layer k1
         const double pr = (bot - pk) / d;
-        QO[k2 * sk] = b2 + 0.5 * (b4 + b3 - b2) * (pr + pl) - b4 * MP_R3 * (pr * (pr + pl) + pl * pl);
+#pragma unroll
+        for (int f = 0; f < MP_F; ++f)
+          if (on[f])
+            QO[f][k2 * sk] = b2[f] + 0.5 * (b4[f] + b3[f] - b2[f]) * (pr + pl) -
+                             b4[f] * MP_R3 * (pr * (pr + pl) + pl * pl);
         k0 = k1;
       } else {  // the rest of k1, whole source layers, then part of the last one
-        double qsum = (pn - top) * (b2 + 0.5 * (b4 + b3 - b2) * (1.0 + pl) - b4 * (MP_R3 * (1.0 + pl * (1.0 + pl))));
+        double qsum[MP_F];
+#pragma unroll
+        for (int f = 0; f < MP_F; ++f)
+          qsum[f] = (pn - top) * (b2[f] + 0.5 * (b4[f] + b3[f] - b2[f]) * (1.0 + pl) -
+                                  b4[f] * (MP_R3 * (1.0 + pl * (1.0 + pl))));
         int kend = k1;
         for (int m = k1 + 1; m < nk; ++m) {
           const double pm = p1(m), pm1 = p1(m + 1);
           const double dm = pm1 - pm;
           if (bot > pm1) {
-            qsum = qsum + dm * __ldg(Q + m * sk);
+#pragma unroll
+            for (int f = 0; f < MP_F; ++f) qsum[f] = qsum[f] + dm * __ldg(Q[f] + m * sk);
           } else {
             const double dp = bot - pm;
             const double esl = dp / dm;
-            const double c2 = __ldg(A2 + m * sk);
-            qsum = qsum + dp * (c2 + 0.5 * esl * (__ldg(A3 + m * sk) - c2 + __ldg(A4 + m * sk) * (1.0 - MP_R23 * esl)));
+#pragma unroll
+            for (int f = 0; f < MP_F; ++f) {
+              const double c2 = __ldg(A2[f] + m * sk);
+              qsum[f] = qsum[f] + dp * (c2 + 0.5 * esl * (__ldg(A3[f] + m * sk) - c2 +
+                                                         __ldg(A4[f] + m * sk) * (1.0 - MP_R23 * esl)));
+            }
             kend = m;
             break;
           }
         }
-        QO[k2 * sk] = qsum / (bot - top);
+#pragma unroll
+        for (int f = 0; f < MP_F; ++f)
+          if (on[f]) QO[f][k2 * sk] = qsum[f] / (bot - top);
         k0 = kend;
       }
     }
@@ -689,7 +729,7 @@ extern "C" int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int 
   if (bytes > 48 * 1024 &&
       cudaFuncSetAttribute(remap_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
     return check_launch("remap_map smem attribute");
-  remap_map_kernel<<<cdiv(a.ni * a.nj, MP_COLS), dim3(MP_COLS, a.nq < MP_TY ? a.nq : MP_TY), bytes,
-                     (cudaStream_t)stream>>>(a);
+  const int ty = cdiv(a.nq, MP_F) < MP_TY ? cdiv(a.nq, MP_F) : MP_TY;
+  remap_map_kernel<<<cdiv(a.ni * a.nj, MP_COLS), dim3(MP_COLS, ty), bytes, (cudaStream_t)stream>>>(a);
   return check_launch("remap_map");
 }
