@@ -325,68 +325,108 @@ struct RemapArgs {
 // output slots (gam in a4_2[k], the forward edge in a4_3[k], both read back
 // before level k's coefficients overwrite them; L2-resident).
 template <bool FAST>
-__device__ __forceinline__ bool remap_column(const RemapArgs& a, int i, int j, int t) {
+__device__ __forceinline__ bool remap_column(const RemapArgs& a, int i, int j, int t0) {
+  // fields t0 and t0 + 1 (if any): gam depends on delp only, so it is
+  // computed and staged once (in t0's a4_2 slots) for both
+  constexpr int F = 2;
   ColArith<FAST> ar;
   const int nk = a.nk;
+  const int nf = a.nq - t0 < F ? a.nq - t0 : F;
   const int64_t off = i + (int64_t)j * a.sj, sk = a.sk;
   const double* __restrict__ dp = a.delp.ptr(i, j, 0);
-  const double* __restrict__ q = a.q[t] + off;
-  double* o2 = a.a2[t] + off;  // gam(k), then a4_2
-  double* o3 = a.a3[t] + off;  // forward edge qe(k), then a4_3
-  double* o4 = a.a4[t] + off;
+  const double* __restrict__ q[F];
+  double* o2[F];
+  double* o3[F];
+  double* o4[F];
+#pragma unroll
+  for (int f = 0; f < F; ++f) {
+    const int t = f < nf ? t0 + f : t0;
+    q[f] = a.q[t] + off;
+    o2[f] = a.a2[t] + off;  // t0's: gam(k), then a4_2; others: a4_2
+    o3[f] = a.a3[t] + off;  // forward edge qe(k), then a4_3
+    o4[f] = a.a4[t] + off;
+  }
+  double* G = o2[0];
   // forward: remap_edge_fwd (gam and qe)
   const double dp0 = __ldg(dp), dp1 = __ldg(dp + sk);
-  const double q0 = __ldg(q), q1 = __ldg(q + sk);
   const double grat0 = ar.div(dp1, dp0);
   const double bet0 = grat0 * (grat0 + 0.5);
   const double rb0 = ar.rcp(bet0);
   double gprev = ar.div_r(1.0 + grat0 * (grat0 + 1.5), bet0, rb0);
-  double eprev = ar.div_r((grat0 + grat0) * (grat0 + 1.0) * q0 + q1, bet0, rb0);
-  o2[0] = gprev;
-  o3[0] = eprev;
-  double dprev = dp0, qprev = q0, d4last = 0.0;
+  double eprev[F], qprev[F];
+#pragma unroll
+  for (int f = 0; f < F; ++f) {
+    const double q0 = __ldg(q[f]), q1 = __ldg(q[f] + sk);
+    eprev[f] = ar.div_r((grat0 + grat0) * (grat0 + 1.0) * q0 + q1, bet0, rb0);
+    qprev[f] = q0;
+  }
+  G[0] = gprev;
+#pragma unroll
+  for (int f = 0; f < F; ++f)
+    if (f < nf) o3[f][0] = eprev[f];
+  double dprev = dp0, d4last = 0.0;
 #ifndef FV3B_RM_PF
-#define FV3B_RM_PF 8  // measured: 8 > 4, 12, 16 (tools/build_variant.py sweeps)
+#define FV3B_RM_PF 4  // measured with two fields per thread: 4 > 8
 #endif
-  pipelined<FV3B_RM_PF, D2>(
-      nk - 1, [&](int s) { return D2{__ldg(dp + (s + 1) * sk), __ldg(q + (s + 1) * sk)}; },
-      [&](int s, const D2& v) {
+  pipelined<FV3B_RM_PF, D3>(
+      nk - 1, [&](int s) { return D3{__ldg(dp + (s + 1) * sk), __ldg(q[0] + (s + 1) * sk), __ldg(q[1] + (s + 1) * sk)}; },
+      [&](int s, const D3& v) {
         const int k = s + 1;
         const double d4 = ar.div(dprev, v.x);
         const double bet = 2.0 + d4 + d4 - gprev;  // gam(k-1)
         const double rb = ar.rcp(bet);
-        eprev = ar.div_r(3.0 * (qprev + d4 * v.y) - eprev, bet, rb);
+        const double qv[F] = {v.y, v.z};
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          eprev[f] = ar.div_r(3.0 * (qprev[f] + d4 * qv[f]) - eprev[f], bet, rb);
+          qprev[f] = qv[f];
+        }
         gprev = ar.div_r(d4, bet, rb);
-        o2[k * sk] = gprev;
-        o3[k * sk] = eprev;
+        G[k * sk] = gprev;
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+          if (f < nf) o3[f][k * sk] = eprev[f];
         dprev = v.x;
-        qprev = v.y;
         d4last = d4;
       });
   const double d4p = d4last;
   const double abot = 1.0 + d4p * (d4p + 1.5);
   // gam(nk-1) = gprev
-  double qen = ar.div(2.0 * d4p * (d4p + 1.0) * qprev + __ldg(q + (nk - 2) * sk) - abot * eprev,
-                      d4p * (d4p + 0.5) - abot * gprev);
+  double qen[F];
+#pragma unroll
+  for (int f = 0; f < F; ++f)
+    qen[f] = ar.div(2.0 * d4p * (d4p + 1.0) * qprev[f] + __ldg(q[f] + (nk - 2) * sk) - abot * eprev[f],
+                    d4p * (d4p + 0.5) - abot * gprev);
   // backward: remap_edge_bwd fused with remap_a4 for layer k
-  pipelined<FV3B_RM_PF, D3>(
-      nk, [&](int s) { const int k = nk - 1 - s; return D3{__ldg(q + k * sk), o2[k * sk], o3[k * sk]}; },
-      [&](int s, const D3& v) {
+  struct D5 { double g, q0, q1, e0, e1; };
+  pipelined<FV3B_RM_PF, D5>(
+      nk,
+      [&](int s) {
         const int k = nk - 1 - s;
-        const double qek = v.z - v.y * qen;
-        const double qc = v.x;
-        const double al = qek, ar_ = qen;
-        const double ext = (ar_ - qc) * (qc - al);
-        const double da1 = ar_ - al;
-        const double a6 = 3.0 * (2.0 * qc - (al + ar_));
-        const double a6da = a6 * da1;
-        const double da2 = da1 * da1;
-        const double v2 = (ext <= 0.0) ? qc : ((a6da > da2) ? 3.0 * qc - 2.0 * ar_ : al);
-        const double v3 = (ext <= 0.0) ? qc : ((a6da < -da2) ? 3.0 * qc - 2.0 * al : ar_);
-        o2[k * sk] = v2;
-        o3[k * sk] = v3;
-        o4[k * sk] = 3.0 * (2.0 * qc - (v2 + v3));
-        qen = qek;
+        return D5{G[k * sk], __ldg(q[0] + k * sk), __ldg(q[1] + k * sk), o3[0][k * sk], o3[1][k * sk]};
+      },
+      [&](int s, const D5& v) {
+        const int k = nk - 1 - s;
+        const double qv[F] = {v.q0, v.q1}, ev[F] = {v.e0, v.e1};
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          const double qek = ev[f] - v.g * qen[f];
+          const double qc = qv[f];
+          const double al = qek, ar_ = qen[f];
+          const double ext = (ar_ - qc) * (qc - al);
+          const double da1 = ar_ - al;
+          const double a6 = 3.0 * (2.0 * qc - (al + ar_));
+          const double a6da = a6 * da1;
+          const double da2 = da1 * da1;
+          const double v2 = (ext <= 0.0) ? qc : ((a6da > da2) ? 3.0 * qc - 2.0 * ar_ : al);
+          const double v3 = (ext <= 0.0) ? qc : ((a6da < -da2) ? 3.0 * qc - 2.0 * al : ar_);
+          if (f < nf) {
+            o2[f][k * sk] = v2;
+            o3[f][k * sk] = v3;
+            o4[f][k * sk] = 3.0 * (2.0 * qc - (v2 + v3));
+          }
+          qen[f] = qek;
+        }
       });
   return ar.ok;
 }
@@ -398,7 +438,7 @@ constexpr int RM_COLS = 32, RM_TQ = 4;  // CTA: 32 columns x 4 tracers
 
 __global__ void __launch_bounds__(RM_COLS * RM_TQ, FV3B_RM_MINB) remap_kernel(const RemapArgs a) {
   const int cidx = blockIdx.x * RM_COLS + threadIdx.x;
-  const int t = blockIdx.y * RM_TQ + threadIdx.y;
+  const int t = 2 * (blockIdx.y * RM_TQ + threadIdx.y);  // fields t, t + 1
   if (cidx >= a.ni * a.nj || t >= a.nq) return;
   const int i = cidx % a.ni, j = cidx / a.ni;
   // inputs are never written: a failed fast evaluation is simply redone
@@ -524,7 +564,7 @@ extern "C" int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, 
   a.nj = d->nj;
   a.nk = d->nk - 1;
   if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
-  dim3 grid(cdiv(a.ni * a.nj, RM_COLS), cdiv(a.nq, RM_TQ));
+  dim3 grid(cdiv(a.ni * a.nj, RM_COLS), cdiv(cdiv(a.nq, 2), RM_TQ));
   remap_kernel<<<grid, dim3(RM_COLS, RM_TQ), 0, (cudaStream_t)stream>>>(a);
   return check_launch("remap_profile");
 }
