@@ -280,6 +280,36 @@ class LoopbackCluster:
         for h, ch in zip(self.halos, chunks):
             h.finish(ch)
 
+    def _assignment(self) -> tuple:
+        return tuple(d._assignment() for d in self.d)
+
+    def capture(self) -> None:
+        """Capture one lockstep step of every rank (programs and device-copy
+        halo exchanges) as a CUDA graph per distinct buffer assignment, as
+        Dycore.capture does for one rank.  Captures execute nothing; the
+        bookkeeping is restored afterwards."""
+        import torch
+
+        torch.cuda.synchronize()
+        start = [(dict(d.cur), dict(d.alt)) for d in self.d]
+        self._graphs = {}
+        while self._assignment() not in self._graphs:
+            key = self._assignment()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.step()
+            self._graphs[key] = (g, [(dict(d.cur), dict(d.alt)) for d in self.d])
+        for d, (cur, alt) in zip(self.d, start):
+            d.cur, d.alt = cur, alt
+        torch.cuda.synchronize()
+
+    def replay(self) -> None:
+        """Run one captured lockstep step on the current stream."""
+        g, post = self._graphs[self._assignment()]
+        g.replay()
+        for d, (cur, alt) in zip(self.d, post):
+            d.cur, d.alt = dict(cur), dict(alt)
+
     def step(self) -> None:
         gens = [d.phases() for d in self.d]
         while True:
