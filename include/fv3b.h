@@ -98,7 +98,9 @@ int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, int ns,
 /* K5  remap_profile.stn / remap_tracers.stn — PPM edge solve + limited
  *     sub-grid coefficients.  Program domain nk = interface levels.
  *     fields: delp, then per tracer: q, a4_2, a4_3, a4_4 (outputs must not
- *     alias the inputs).  scalars: none. */
+ *     alias the inputs).  scalars: none.  Grouped form (fields at several
+ *     layer thicknesses, one launch): scalars s[g] = fields in group g, and
+ *     the field list is, per group, its thickness then 4 per member. */
 int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns,
                        const fv3b_domain* d, void* stream);
 
@@ -107,7 +109,10 @@ int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns,
  *     pe2 = ak + bk * ps (ps = ptop + sum of delp), then delp <- pe2
  *     differences in place.  Program domain nk = interface levels.
  *     fields: delp, ak (K), bk (K), then per tracer: q, a4_2, a4_3, a4_4,
- *     q_out (q_out must not alias any other field).  scalars: none. */
+ *     q_out (q_out must not alias any other field).  scalars: none.
+ *     Grouped form: scalars s[g] = fields in group g; fields ak, bk, then
+ *     per group its thickness (rewritten with its pe2 differences) and 5
+ *     per member. */
 int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int ns,
                    const fv3b_domain* d, void* stream);
 
@@ -199,6 +204,13 @@ int fv3b_halo_scatter(const fv3b_field* f, int nf, const double* s, int ns,
  *                   data = region origin, halo_lo ignored).  scalars: none. */
 int fv3b_transpose(const fv3b_field* f, int nf, const double* s, int ns,
                    const fv3b_domain* d, void* stream);
+
+/*   fv3b_face_thickness  layer thickness at the D-grid wind points for the
+ *                   remapping of u and v: du = 0.5 * (delp[0,-1,0] + delp),
+ *                   dv = 0.5 * (delp[-1,0,0] + delp) over the interior.
+ *                   fields: delp (I / J halo >= 1), du, dv.  scalars: none. */
+int fv3b_face_thickness(const fv3b_field* f, int nf, const double* s, int ns,
+                        const fv3b_domain* d, void* stream);
 
 /*   fv3b_selftest_fastmath  diagnostic: over n device operand pairs, adds to
  *                   counts[0..3] (device, zeroed by the caller) the fast-path

@@ -54,7 +54,7 @@ class OracleDycore:
         self.docs = {n: interp.load_manifest(n) for n in BINDINGS}
         self.written = {n: _written(d) for n, d in self.docs.items()}
         h, nk = cfg.halo, cfg.nk
-        for q in cfg.remapped():
+        for q in cfg.remapped() + ["u", "v"]:
             for a in ("a2", "a3", "a4"):
                 state.setdefault(f"{q}_{a}", np.zeros_like(state["delp"]))
         self._h = h
@@ -117,13 +117,20 @@ class OracleDycore:
             self.call("nh_d", {**c, "dt": dt})
             yield ["pef", "gz"]
             self.call("p_grad_d", {**c, "dt": dt})
-        yield cfg.tracer_names() + ["cx", "cy", "xfa", "yfa", "mfx", "mfy"]
+        yield cfg.tracer_names() + ["cx", "cy", "xfa", "yfa", "mfx", "mfy", "delp"]
         self.call("tracer_2d", c)
         self.call("remap_tracers", c)
         for n in ("pt", "w"):  # the remap_profile program on each thermodynamic field
             self.call("remap_profile", c, bind={"q": n, "a4_2": f"{n}_a2", "a4_3": f"{n}_a3", "a4_4": f"{n}_a4"})
+        # the D-grid winds at their own thickness (remap_profile program, map1_ppm)
+        st["du"], st["dv"] = remap_map.face_thickness(st["delp"], cfg.nk, self._h)
+        for w, dw in (("u", "du"), ("v", "dv")):
+            self.call("remap_profile", c,
+                      bind={"q": w, "delp": dw, "a4_2": f"{w}_a2", "a4_3": f"{w}_a3", "a4_4": f"{w}_a4"})
         ak, bk = cfg.target_coordinate()
         remap_map.remap_map(st, cfg.remapped(), ak, bk, cfg.nk, self._h)
+        for w, dw in (("u", "du"), ("v", "dv")):
+            remap_map.remap_map(st, [w], ak, bk, cfg.nk, self._h, delp_key=dw)
 
     def step(self) -> None:
         for names in self.phases():

@@ -129,12 +129,26 @@ def map_column(pe1, pe2, q, a2, a3, a4, nk: int) -> np.ndarray:
     return q2
 
 
-def remap_map(state: dict, names: list[str], ak, bk, nk: int, h: int) -> None:
+def face_thickness(delp: np.ndarray, nk: int, h: int) -> tuple[np.ndarray, np.ndarray]:
+    """Layer thickness at the D-grid wind points (u(i, j) between cells
+    (i, j-1) and (i, j), v(i, j) between (i-1, j) and (i, j)), interior
+    columns, as fv3b_face_thickness: du = 0.5 * (delp[0,-1,0] + delp)."""
+    du = np.zeros_like(delp)
+    dv = np.zeros_like(delp)
+    I, J = delp.shape[0] - 2 * h, delp.shape[1] - 2 * h
+    c = delp[h:h + I, h:h + J, :nk]
+    du[h:h + I, h:h + J, :nk] = 0.5 * (delp[h:h + I, h - 1:h - 1 + J, :nk] + c)
+    dv[h:h + I, h:h + J, :nk] = 0.5 * (delp[h - 1:h - 1 + I, h:h + J, :nk] + c)
+    return du, dv
+
+
+def remap_map(state: dict, names: list[str], ak, bk, nk: int, h: int, delp_key: str = "delp") -> None:
     """In place on the interior columns of reference-convention arrays:
-    every tracer q in ``names`` <- its profile (q_a2, q_a3, q_a4) mapped onto
-    the target layers; then delp <- pe2 differences."""
+    every field q in ``names`` <- its profile (q_a2, q_a3, q_a4) mapped onto
+    the target layers of the thickness ``state[delp_key]``; then that
+    thickness <- pe2 differences."""
     sl = (slice(h, -h or None), slice(h, -h or None))
-    delp = state["delp"][sl]
+    delp = state[delp_key][sl]
     pe1, pe2 = pe_edges(delp, ak, bk, nk)
     for n in names:
         q = state[n][sl]

@@ -307,13 +307,16 @@ __global__ void __launch_bounds__(NC_MAX) riem_kernel(const RiemArgs a) {
 // backward sweep (layer k needs final edges k and k+1).
 // ---------------------------------------------------------------------------
 struct RemapArgs {
-  View delp;
+  View delp;                // thickness of the first group (strides shared by every field)
+  const double* dp[16];     // per field: the interior origin of its group's thickness
   double* q[16];
   double* a2[16];
   double* a3[16];
   double* a4[16];
+  int pair0[16];       // first field of each pair (a pair never spans two groups)
+  int pairn[16];       // fields in the pair (1 or 2)
   int64_t sj, sk;
-  int nq, ni, nj, nk;  // nk layers (program domain nk+1)
+  int nq, npair, ni, nj, nk;  // nk layers (program domain nk+1)
 };
 
 // One (column, tracer) per thread: 8x the independent recurrences of a
@@ -325,15 +328,15 @@ struct RemapArgs {
 // output slots (gam in a4_2[k], the forward edge in a4_3[k], both read back
 // before level k's coefficients overwrite them; L2-resident).
 template <bool FAST>
-__device__ __forceinline__ bool remap_column(const RemapArgs& a, int i, int j, int t0) {
+__device__ __forceinline__ bool remap_column(const RemapArgs& a, int i, int j, int t0, int nf) {
   // fields t0 and t0 + 1 (if any): gam depends on delp only, so it is
   // computed and staged once (in t0's a4_2 slots) for both
   constexpr int F = 2;
   ColArith<FAST> ar;
   const int nk = a.nk;
-  const int nf = a.nq - t0 < F ? a.nq - t0 : F;
+
   const int64_t off = i + (int64_t)j * a.sj, sk = a.sk;
-  const double* __restrict__ dp = a.delp.ptr(i, j, 0);
+  const double* __restrict__ dp = a.dp[t0] + off;  // (t0 and t0 + 1 share a group: same thickness)
   const double* __restrict__ q[F];
   double* o2[F];
   double* o3[F];
@@ -438,11 +441,12 @@ constexpr int RM_COLS = 32, RM_TQ = 4;  // CTA: 32 columns x 4 tracers
 
 __global__ void __launch_bounds__(RM_COLS * RM_TQ, FV3B_RM_MINB) remap_kernel(const RemapArgs a) {
   const int cidx = blockIdx.x * RM_COLS + threadIdx.x;
-  const int t = 2 * (blockIdx.y * RM_TQ + threadIdx.y);  // fields t, t + 1
-  if (cidx >= a.ni * a.nj || t >= a.nq) return;
+  const int p = blockIdx.y * RM_TQ + threadIdx.y;  // field pair p: fields pair0[p] and pair0[p] + 1
+  if (cidx >= a.ni * a.nj || p >= a.npair) return;
+  const int t = a.pair0[p], n = a.pairn[p];
   const int i = cidx % a.ni, j = cidx / a.ni;
   // inputs are never written: a failed fast evaluation is simply redone
-  if (!remap_column<true>(a, i, j, t)) remap_column<false>(a, i, j, t);
+  if (!remap_column<true>(a, i, j, t, n)) remap_column<false>(a, i, j, t, n);
 }
 
 static int set_smem(const void* fn, size_t bytes) {
@@ -533,38 +537,70 @@ extern "C" int fv3b_riem_solver_c(const fv3b_field* f, int nf, const double* s, 
 // the inputs (a2 / a3 stage the backward sweep's operands).
 extern "C" int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                                   void* stream) {
-  (void)s;
-  if (f == nullptr || d == nullptr || nf < 5 || (nf - 1) % 4 != 0 || (nf - 1) / 4 > 16 || ns != 0)
-    return fail(FV3B_EINVAL, "fv3b_remap_profile: expects 1 + 4*nq fields (nq <= 16), 0 scalars");
+  // groups of fields sharing a layer thickness: ns == 0 -> one group
+  // (delp, 4 fields per tracer); else s[g] = fields in group g and the field
+  // list is, per group, its thickness then 4 fields per member
+  int ng = ns == 0 ? 1 : ns, cnt[16], total = 0;
+  if (f == nullptr || d == nullptr || ns < 0 || ns > 16 || (ns > 0 && s == nullptr))
+    return fail(FV3B_EINVAL, "fv3b_remap_profile: bad arguments");
+  if (ns == 0) {
+    if (nf < 5 || (nf - 1) % 4 != 0) return fail(FV3B_EINVAL, "fv3b_remap_profile: expects 1 + 4*nq fields");
+    cnt[0] = (nf - 1) / 4;
+  } else {
+    for (int g = 0; g < ng; ++g) {
+      cnt[g] = (int)s[g];
+      if (cnt[g] < 1 || (double)cnt[g] != s[g]) return fail(FV3B_EINVAL, "fv3b_remap_profile: bad group size %g", s[g]);
+    }
+  }
+  for (int g = 0; g < ng; ++g) total += cnt[g];
+  if (total > 16 || nf != ng + 4 * total)
+    return fail(FV3B_EINVAL, "fv3b_remap_profile: expects per group its thickness + 4 per field (<= 16 fields)");
   if (d->nk < 3) return fail(FV3B_EDOMAIN, "fv3b_remap_profile: program domain nk=%d below minimum 3", d->nk);
+  // outputs never alias an input (any thickness or any q)
+  bool input[4 * 16 + 16] = {};
+  for (int g = 0, x = 0; g < ng; ++g) {
+    input[x++] = true;
+    for (int m = 0; m < cnt[g]; ++m, x += 4) input[x] = true;
+  }
+  for (int x = 0; x < nf; ++x)
+    if (!input[x])
+      for (int y = 0; y < nf; ++y)
+        if (y != x && f[y].data == f[x].data)
+          return fail(FV3B_EINVAL, "fv3b_remap_profile: output %d aliases field %d", x, y);
   RemapArgs a;
   const Halo h0 = {0, 0, 0, 0, 0, 0};
-  FV3B_TRY(view_of(f[0], 3, *d, h0, "delp", &a.delp));
-  a.nq = (nf - 1) / 4;
-  for (int t = 0; t < a.nq; ++t) {
-    View v[4];
-    for (int u = 0; u < 4; ++u) FV3B_TRY(view_of(f[1 + 4 * t + u], 3, *d, h0, "remap field", &v[u]));
-    for (int u = 0; u < 4; ++u)
-      if (v[u].sj != a.delp.sj || v[u].sk != a.delp.sk) return fail(FV3B_ELAYOUT, "fv3b_remap_profile: strides differ");
-    a.q[t] = v[0].o;
-    a.a2[t] = v[1].o;
-    a.a3[t] = v[2].o;
-    a.a4[t] = v[3].o;
-  }
-  for (int t = 0; t < a.nq; ++t)
-    for (int u = 1; u < 4; ++u) {
-      const void* o = f[1 + 4 * t + u].data;
-      if (o == f[0].data) return fail(FV3B_EINVAL, "fv3b_remap_profile: output aliases delp");
-      for (int r = 0; r < a.nq; ++r)
-        if (o == f[1 + 4 * r].data) return fail(FV3B_EINVAL, "fv3b_remap_profile: output aliases q%d", r);
+  a.nq = total;
+  a.npair = 0;
+  for (int g = 0, x = 0, t = 0; g < ng; ++g) {
+    View dp;
+    const int xd = x++;
+    FV3B_TRY(view_of(f[xd], 3, *d, h0, "thickness", &dp));
+    if (g == 0) a.delp = dp;
+    if (dp.sj != a.delp.sj || dp.sk != a.delp.sk) return fail(FV3B_ELAYOUT, "fv3b_remap_profile: strides differ");
+    for (int m = 0; m < cnt[g]; ++m, ++t) {
+      View v[4];
+      for (int u = 0; u < 4; ++u) FV3B_TRY(view_of(f[x + u], 3, *d, h0, "remap field", &v[u]));
+      for (int u = 0; u < 4; ++u)
+        if (v[u].sj != a.delp.sj || v[u].sk != a.delp.sk) return fail(FV3B_ELAYOUT, "fv3b_remap_profile: strides differ");
+      a.dp[t] = dp.o;
+      a.q[t] = v[0].o;
+      a.a2[t] = v[1].o;
+      a.a3[t] = v[2].o;
+      a.a4[t] = v[3].o;
+      if (m % 2 == 0) {
+        a.pair0[a.npair] = t;
+        a.pairn[a.npair++] = m + 1 < cnt[g] ? 2 : 1;
+      }
+      x += 4;
     }
+  }
   a.sj = a.delp.sj;
   a.sk = a.delp.sk;
   a.ni = d->ni;
   a.nj = d->nj;
   a.nk = d->nk - 1;
   if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
-  dim3 grid(cdiv(a.ni * a.nj, RM_COLS), cdiv(cdiv(a.nq, 2), RM_TQ));
+  dim3 grid(cdiv(a.ni * a.nj, RM_COLS), cdiv(a.npair, RM_TQ));
   remap_kernel<<<grid, dim3(RM_COLS, RM_TQ), 0, (cudaStream_t)stream>>>(a);
   return check_launch("remap_profile");
 }
@@ -586,7 +622,11 @@ extern "C" int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, 
 namespace fv3b {
 
 struct RemapMapArgs {
-  View delp, ak, bk;
+  View delp, ak, bk;           // delp: the first group's thickness (strides shared)
+  double* thick[16];           // per group: its thickness (rewritten with the pe2 differences)
+  int gfirst[17];              // group g maps fields gfirst[g] .. gfirst[g+1]-1
+  int ngroup;
+  int ncb;                     // blocks of 32 columns per CTA
   const double* q[16];
   const double* a2[16];
   const double* a3[16];
@@ -604,125 +644,119 @@ constexpr int MP_COLS = 32, MP_TY = 16;  // blockDim.y = min(ceil(nq / MP_F), MP
 constexpr double MP_R3 = 1.0 / 3.0, MP_R23 = 2.0 / 3.0;  // the oracle's R3, R23 (same roundings)
 
 __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapMapArgs a) {
-  extern __shared__ double sm[];  // pe1, pe2 [(nk+1) x 32]; ak, bk [nk+1]
-  const int c = threadIdx.x, ty = threadIdx.y;
-  const int cidx = blockIdx.x * MP_COLS + c;
+  // map1_ppm's walk over the source layers only moves downwards, so the
+  // Lagrangian interfaces pe1 are produced by a running sum as it advances
+  // (the same additions in the same order as pe1[k+1] = pe1[k] + delp[k]):
+  // no per-column level arrays in shared memory, occupancy bounded by
+  // registers only.  ps = pe1[nk] comes from a first pass over the column.
+  extern __shared__ double sm[];  // ak, bk [nk + 1]
+  // threadIdx.y = (column block, field thread): a.ncb blocks of 32 columns,
+  // blockDim.y / a.ncb field threads per column
+  const int c = threadIdx.x, ny = blockDim.y / a.ncb, ty = threadIdx.y % ny, cb = threadIdx.y / ny;
+  const int cidx = (blockIdx.x * a.ncb + cb) * MP_COLS + c;
   const bool live = cidx < a.ni * a.nj;
   const int nk = a.nk;
-  double* P1 = sm;
-  double* P2 = sm + (nk + 1) * MP_COLS;
-  double* AK = sm + 2 * (nk + 1) * MP_COLS;
-  double* BK = AK + (nk + 1);
-  auto p1 = [&](int k) { return P1[k * MP_COLS + c]; };
-  auto p2 = [&](int k) { return P2[k * MP_COLS + c]; };
   const int i = live ? cidx % a.ni : 0, j = live ? cidx / a.ni : 0;
   const int64_t off = i + (int64_t)j * a.sj, sk = a.sk;
-  // stage delp (in pe1's slots 1..nk) and ak / bk with every warp: coalesced level rows
-  const int ny = blockDim.y;
-  for (int k = ty; k < nk; k += ny)
-    if (live) P1[(k + 1) * MP_COLS + c] = __ldg(a.delp.o + off + k * sk);
-  for (int e = c + ty * MP_COLS; e <= nk; e += MP_COLS * ny) {
+  const int grp = blockIdx.y;
+  double* thick = a.thick[grp] + off;
+  double* AK = sm;
+  double* BK = sm + (nk + 1);
+  for (int e = c + threadIdx.y * MP_COLS; e <= nk; e += MP_COLS * blockDim.y) {
     AK[e] = __ldg(a.ak.o + e * a.ak.sk);
     BK[e] = __ldg(a.bk.o + e * a.bk.sk);
   }
   __syncthreads();
-  if (ty == 0 && live) {
-    double p = AK[0];
-    P1[c] = p;
-    for (int k = 0; k < nk; ++k) {
-      p = p + P1[(k + 1) * MP_COLS + c];  // + delp[k]
-      P1[(k + 1) * MP_COLS + c] = p;
-    }
-  }
-  __syncthreads();
-  if (live) {
-    const double ps = p1(nk);
-    for (int k = ty; k <= nk; k += ny)
-      P2[k * MP_COLS + c] = k == 0 ? p1(0) : (k == nk ? ps : AK[k] + BK[k] * ps);
-  }
-  __syncthreads();
-  if (!live) return;
-  // MP_F fields per thread: map1_ppm's source-layer search depends on pe1 /
-  // pe2 only, so it is done once for the thread's fields, whose loads are
-  // independent (MP_F-fold memory-level parallelism in the level loop).
-  for (int t0 = ty; t0 < a.nq; t0 += ny * MP_F) {
-    const double* Q[MP_F];
-    const double* A2[MP_F];
-    const double* A3[MP_F];
-    const double* A4[MP_F];
-    double* QO[MP_F];
-    bool on[MP_F];
-#pragma unroll
-    for (int f = 0; f < MP_F; ++f) {
-      const int t = t0 + f * ny;
-      on[f] = t < a.nq;
-      const int tt = on[f] ? t : t0;
-      Q[f] = a.q[tt] + off;
-      A2[f] = a.a2[tt] + off;
-      A3[f] = a.a3[tt] + off;
-      A4[f] = a.a4[tt] + off;
-      QO[f] = a.qo[tt] + off;
-    }
-    int k0 = 0;
-    for (int k2 = 0; k2 < nk; ++k2) {
-      const double top = p2(k2), bot = p2(k2 + 1);
-      int k1 = k0;
-      while (top > p1(k1 + 1) && k1 < nk - 1) ++k1;
-      const double pk = p1(k1), pn = p1(k1 + 1);
-      const double d = pn - pk;
-      const double pl = (top - pk) / d;
-      double b2[MP_F], b3[MP_F], b4[MP_F];
+  auto th = [&](int k) { return thick[k * sk]; };  // (rewritten at the end: plain loads)
+  double ps = AK[0];
+  if (live)
+    for (int k = 0; k < nk; ++k) ps = ps + th(k);
+  // pe2 = ak + bk * ps, the end interfaces from pe1 (pe1[0] = ak[0])
+  auto p2 = [&](int k) { return k == 0 ? AK[0] : (k == nk ? ps : AK[k] + BK[k] * ps); };
+  const int tb = a.gfirst[grp], te = a.gfirst[grp + 1];
+  if (live)
+    for (int t0 = tb + ty; t0 < te; t0 += ny * MP_F) {
+      const double* Q[MP_F];
+      const double* A2[MP_F];
+      const double* A3[MP_F];
+      const double* A4[MP_F];
+      double* QO[MP_F];
+      bool on[MP_F];
 #pragma unroll
       for (int f = 0; f < MP_F; ++f) {
-        b2[f] = __ldg(A2[f] + k1 * sk);
-        b3[f] = __ldg(A3[f] + k1 * sk);
-        b4[f] = __ldg(A4[f] + k1 * sk);
+        const int t = t0 + f * ny;
+        on[f] = t < te;
+        const int tt = on[f] ? t : t0;
+        Q[f] = a.q[tt] + off;
+        A2[f] = a.a2[tt] + off;
+        A3[f] = a.a3[tt] + off;
+        A4[f] = a.a4[tt] + off;
+        QO[f] = a.qo[tt] + off;
       }
-      if (bot <= pn) {  // the whole target layer lies in source layer k1
-        const double pr = (bot - pk) / d;
-#pragma unroll
-        for (int f = 0; f < MP_F; ++f)
-          if (on[f])
-            QO[f][k2 * sk] = b2[f] + 0.5 * (b4[f] + b3[f] - b2[f]) * (pr + pl) -
-                             b4[f] * MP_R3 * (pr * (pr + pl) + pl * pl);
-        k0 = k1;
-      } else {  // the rest of k1, whole source layers, then part of the last one
-        double qsum[MP_F];
-#pragma unroll
-        for (int f = 0; f < MP_F; ++f)
-          qsum[f] = (pn - top) * (b2[f] + 0.5 * (b4[f] + b3[f] - b2[f]) * (1.0 + pl) -
-                                  b4[f] * (MP_R3 * (1.0 + pl * (1.0 + pl))));
-        int kend = k1;
-        for (int m = k1 + 1; m < nk; ++m) {
-          const double pm = p1(m), pm1 = p1(m + 1);
-          const double dm = pm1 - pm;
-          if (bot > pm1) {
-#pragma unroll
-            for (int f = 0; f < MP_F; ++f) qsum[f] = qsum[f] + dm * __ldg(Q[f] + m * sk);
-          } else {
-            const double dp = bot - pm;
-            const double esl = dp / dm;
-#pragma unroll
-            for (int f = 0; f < MP_F; ++f) {
-              const double c2 = __ldg(A2[f] + m * sk);
-              qsum[f] = qsum[f] + dp * (c2 + 0.5 * esl * (__ldg(A3[f] + m * sk) - c2 +
-                                                         __ldg(A4[f] + m * sk) * (1.0 - MP_R23 * esl)));
-            }
-            kend = m;
-            break;
-          }
+      // cursor: source layer k1 with pk = pe1[k1], pn = pe1[k1 + 1]
+      int k1 = 0;
+      double pk = AK[0], pn = pk + th(0);
+      for (int k2 = 0; k2 < nk; ++k2) {
+        const double top = p2(k2), bot = p2(k2 + 1);
+        while (top > pn && k1 < nk - 1) {
+          ++k1;
+          pk = pn;
+          pn = pk + th(k1);
         }
+        const double d = pn - pk;
+        const double pl = (top - pk) / d;
+        double b2[MP_F], b3[MP_F], b4[MP_F];
 #pragma unroll
-        for (int f = 0; f < MP_F; ++f)
-          if (on[f]) QO[f][k2 * sk] = qsum[f] / (bot - top);
-        k0 = kend;
+        for (int f = 0; f < MP_F; ++f) {
+          b2[f] = __ldg(A2[f] + k1 * sk);
+          b3[f] = __ldg(A3[f] + k1 * sk);
+          b4[f] = __ldg(A4[f] + k1 * sk);
+        }
+        if (bot <= pn) {  // the whole target layer lies in source layer k1
+          const double pr = (bot - pk) / d;
+#pragma unroll
+          for (int f = 0; f < MP_F; ++f)
+            if (on[f])
+              QO[f][k2 * sk] = b2[f] + 0.5 * (b4[f] + b3[f] - b2[f]) * (pr + pl) -
+                               b4[f] * MP_R3 * (pr * (pr + pl) + pl * pl);
+        } else {  // the rest of k1, whole source layers, then part of the last one
+          double qsum[MP_F];
+#pragma unroll
+          for (int f = 0; f < MP_F; ++f)
+            qsum[f] = (pn - top) * (b2[f] + 0.5 * (b4[f] + b3[f] - b2[f]) * (1.0 + pl) -
+                                    b4[f] * (MP_R3 * (1.0 + pl * (1.0 + pl))));
+          double pm = pn;  // pe1[m]
+          for (int m = k1 + 1; m < nk; ++m) {
+            const double pm1 = pm + th(m);  // pe1[m + 1]
+            const double dm = pm1 - pm;
+            if (bot > pm1) {
+#pragma unroll
+              for (int f = 0; f < MP_F; ++f) qsum[f] = qsum[f] + dm * __ldg(Q[f] + m * sk);
+              pm = pm1;
+            } else {
+              const double dp = bot - pm;
+              const double esl = dp / dm;
+#pragma unroll
+              for (int f = 0; f < MP_F; ++f) {
+                const double c2 = __ldg(A2[f] + m * sk);
+                qsum[f] = qsum[f] + dp * (c2 + 0.5 * esl * (__ldg(A3[f] + m * sk) - c2 +
+                                                           __ldg(A4[f] + m * sk) * (1.0 - MP_R23 * esl)));
+              }
+              k1 = m;  // the next target layer starts in this one
+              pk = pm;
+              pn = pm1;
+              break;
+            }
+          }
+#pragma unroll
+          for (int f = 0; f < MP_F; ++f)
+            if (on[f]) QO[f][k2 * sk] = qsum[f] / (bot - top);
+        }
       }
     }
-  }
-  if (ty == 0) {
-    double* dp = a.delp.o + off;
-    for (int k = 0; k < nk; ++k) dp[k * sk] = p2(k + 1) - p2(k);
-  }
+  __syncthreads();  // every walk of the CTA has read the thickness
+  if (live && ty == 0)
+    for (int k = 0; k < nk; ++k) thick[k * sk] = p2(k + 1) - p2(k);
 }
 
 }  // namespace fv3b
@@ -732,20 +766,61 @@ __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapM
 // outputs), q_out_t.  Domain nk = interface levels.  No scalars.
 extern "C" int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                               void* stream) {
-  (void)s;
-  if (f == nullptr || d == nullptr || nf < 8 || (nf - 3) % 5 != 0 || (nf - 3) / 5 > 16 || ns != 0)
-    return fail(FV3B_EINVAL, "fv3b_remap_map: expects 3 + 5*nq fields (nq <= 16), 0 scalars");
+  // ns == 0: delp, ak, bk, then 5 fields per tracer (one group).  ns >= 1:
+  // groups of fields sharing a thickness, s[g] = fields in group g; the field
+  // list is ak, bk, then per group its thickness and 5 per member.
+  int ng = ns == 0 ? 1 : ns, cnt[16], total = 0;
+  if (f == nullptr || d == nullptr || ns < 0 || ns > 16 || (ns > 0 && s == nullptr))
+    return fail(FV3B_EINVAL, "fv3b_remap_map: bad arguments");
+  if (ns == 0) {
+    if (nf < 8 || (nf - 3) % 5 != 0) return fail(FV3B_EINVAL, "fv3b_remap_map: expects 3 + 5*nq fields");
+    cnt[0] = (nf - 3) / 5;
+  } else {
+    for (int g = 0; g < ng; ++g) {
+      cnt[g] = (int)s[g];
+      if (cnt[g] < 1 || (double)cnt[g] != s[g]) return fail(FV3B_EINVAL, "fv3b_remap_map: bad group size %g", s[g]);
+    }
+  }
+  for (int g = 0; g < ng; ++g) total += cnt[g];
+  if (total > 16 || nf != 2 + ng + 5 * total)
+    return fail(FV3B_EINVAL, "fv3b_remap_map: expects the thickness(es), ak, bk and 5 per field (<= 16 fields)");
   if (d->nk < 2 || d->nk > 4096)
     return fail(FV3B_EDOMAIN, "fv3b_remap_map: program domain nk=%d outside [2, 4096]", d->nk);
+  // field-list positions: thickness of group g, ak, bk, field t's five
+  int xthick[16], xfield[16];
+  int xak, xbk;
+  if (ns == 0) {
+    xthick[0] = 0;
+    xak = 1;
+    xbk = 2;
+    for (int t = 0; t < total; ++t) xfield[t] = 3 + 5 * t;
+  } else {
+    xak = 0;
+    xbk = 1;
+    for (int g = 0, x = 2, t = 0; g < ng; ++g) {
+      xthick[g] = x++;
+      for (int m = 0; m < cnt[g]; ++m, ++t, x += 5) xfield[t] = x;
+    }
+  }
   RemapMapArgs a;
   const Halo h0 = {0, 0, 0, 0, 0, 0};
-  FV3B_TRY(view_of(f[0], 3, *d, h0, "delp", &a.delp));
-  FV3B_TRY(view_of(f[1], 1, *d, h0, "ak", &a.ak));
-  FV3B_TRY(view_of(f[2], 1, *d, h0, "bk", &a.bk));
-  a.nq = (nf - 3) / 5;
-  for (int t = 0; t < a.nq; ++t) {
+  FV3B_TRY(view_of(f[xthick[0]], 3, *d, h0, "delp", &a.delp));
+  FV3B_TRY(view_of(f[xak], 1, *d, h0, "ak", &a.ak));
+  FV3B_TRY(view_of(f[xbk], 1, *d, h0, "bk", &a.bk));
+  a.nq = total;
+  a.ngroup = ng;
+  for (int g = 0, t = 0; g < ng; ++g) {
+    View v;
+    FV3B_TRY(view_of(f[xthick[g]], 3, *d, h0, "thickness", &v));
+    if (v.sj != a.delp.sj || v.sk != a.delp.sk) return fail(FV3B_ELAYOUT, "fv3b_remap_map: strides differ");
+    a.thick[g] = v.o;
+    a.gfirst[g] = t;
+    t += cnt[g];
+    a.gfirst[g + 1] = t;
+  }
+  for (int t = 0; t < total; ++t) {
     View v[5];
-    for (int u = 0; u < 5; ++u) FV3B_TRY(view_of(f[3 + 5 * t + u], 3, *d, h0, "remap_map field", &v[u]));
+    for (int u = 0; u < 5; ++u) FV3B_TRY(view_of(f[xfield[t] + u], 3, *d, h0, "remap_map field", &v[u]));
     for (int u = 0; u < 5; ++u)
       if (v[u].sj != a.delp.sj || v[u].sk != a.delp.sk) return fail(FV3B_ELAYOUT, "fv3b_remap_map: strides differ");
     a.q[t] = v[0].o;
@@ -754,10 +829,10 @@ extern "C" int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int 
     a.a4[t] = v[3].o;
     a.qo[t] = v[4].o;
   }
-  for (int t = 0; t < a.nq; ++t) {
-    const void* o = f[3 + 5 * t + 4].data;
+  for (int t = 0; t < total; ++t) {  // q_out never aliases another field
+    const int x = xfield[t] + 4;
     for (int g = 0; g < nf; ++g)
-      if (g != 3 + 5 * t + 4 && f[g].data == o) return fail(FV3B_EINVAL, "fv3b_remap_map: q_out%d aliases field %d", t, g);
+      if (g != x && f[g].data == f[x].data) return fail(FV3B_EINVAL, "fv3b_remap_map: q_out%d aliases field %d", t, g);
   }
   a.sj = a.delp.sj;
   a.sk = a.delp.sk;
@@ -765,11 +840,15 @@ extern "C" int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int 
   a.nj = d->nj;
   a.nk = d->nk - 1;
   if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
-  const size_t bytes = ((size_t)2 * (a.nk + 1) * MP_COLS + 2 * (a.nk + 1)) * sizeof(double);
+  int maxc = 1;
+  for (int g = 0; g < ng; ++g) maxc = cnt[g] > maxc ? cnt[g] : maxc;
+  const int ty = cdiv(maxc, MP_F) < MP_TY ? cdiv(maxc, MP_F) : MP_TY;
+  a.ncb = ty >= 4 ? 1 : 4 / ty;  // at least 4 warps per CTA
+  const size_t bytes = (size_t)2 * (a.nk + 1) * sizeof(double);
   if (bytes > 48 * 1024 &&
       cudaFuncSetAttribute(remap_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
     return check_launch("remap_map smem attribute");
-  const int ty = cdiv(a.nq, MP_F) < MP_TY ? cdiv(a.nq, MP_F) : MP_TY;
-  remap_map_kernel<<<cdiv(a.ni * a.nj, MP_COLS), dim3(MP_COLS, ty), bytes, (cudaStream_t)stream>>>(a);
+  dim3 grid(cdiv(a.ni * a.nj, MP_COLS * a.ncb), ng);
+  remap_map_kernel<<<grid, dim3(MP_COLS, ty * a.ncb), bytes, (cudaStream_t)stream>>>(a);
   return check_launch("remap_map");
 }

@@ -146,3 +146,37 @@ extern "C" int fv3b_transpose(const fv3b_field* f, int nf, const double* s, int 
                                                              b.stride[0], b.stride[1], b.stride[2], d->ni, d->nk);
   return fv3b::check_launch("fv3b_transpose");
 }
+
+// ---------------------------------------------------------------------------
+// Layer thickness at the D-grid wind points for the vertical remapping of u
+// and v: u(i, j) sits between cells (i, j-1) and (i, j), v(i, j) between
+// (i-1, j) and (i, j) (p_grad_d.stn), so
+//   du = 0.5 * (delp[0,-1,0] + delp),  dv = 0.5 * (delp[-1,0,0] + delp)
+// over the interior (oracle/remap_map.py face_thickness).
+namespace fv3b {
+__global__ void __launch_bounds__(256) face_thickness_kernel(View dp, View du, View dv, int ni, int nj) {
+  const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y, k = blockIdx.z;
+  if (i >= ni || j >= nj) return;
+  const double c = __ldg(dp.ptr(i, j, k));
+  *du.ptr(i, j, k) = 0.5 * (__ldg(dp.ptr(i, j - 1, k)) + c);
+  *dv.ptr(i, j, k) = 0.5 * (__ldg(dp.ptr(i - 1, j, k)) + c);
+}
+}  // namespace fv3b
+
+extern "C" int fv3b_face_thickness(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                   void* stream) {
+  (void)s;
+  if (f == nullptr || d == nullptr || nf != 3 || ns != 0)
+    return fv3b::fail(FV3B_EINVAL, "fv3b_face_thickness: expects 3 fields (delp, du, dv), 0 scalars");
+  fv3b::View dp, du, dv;
+  const fv3b::Halo h1 = {1, 0, 1, 0, 0, 0}, h0 = {0, 0, 0, 0, 0, 0};
+  FV3B_TRY(fv3b::view_of(f[0], 3, *d, h1, "delp", &dp));
+  FV3B_TRY(fv3b::view_of(f[1], 3, *d, h0, "du", &du));
+  FV3B_TRY(fv3b::view_of(f[2], 3, *d, h0, "dv", &dv));
+  if (f[1].data == f[0].data || f[2].data == f[0].data || f[1].data == f[2].data)
+    return fv3b::fail(FV3B_EINVAL, "fv3b_face_thickness: outputs alias");
+  if (d->ni <= 0 || d->nj <= 0 || d->nk <= 0) return FV3B_OK;
+  dim3 grid(fv3b::cdiv(d->ni, 32), fv3b::cdiv(d->nj, 8), d->nk);
+  fv3b::face_thickness_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(dp, du, dv, d->ni, d->nj);
+  return fv3b::check_launch("fv3b_face_thickness");
+}

@@ -53,11 +53,12 @@ class Dycore:
         self.dom_layers = self.grid.domain(placement, nk=cfg.nk)
         self.dom_ifaces = self.grid.domain(placement, nk=cfg.nk + 1)
         g = self.grid
-        names3 = STATE_3D + cfg.tracer_names() + [f"{q}_{a}" for q in cfg.remapped() for a in ("a2", "a3", "a4")]
+        names3 = STATE_3D + cfg.tracer_names() + [f"{q}_{a}" for q in cfg.remapped() + ["u", "v"]
+                                                  for a in ("a2", "a3", "a4")]
         self.cur: dict[str, torch.Tensor] = {n: g.new3(device) for n in names3}
         self.cur.update({n: g.new2(device) for n in METRICS_2D})
         self.alt: dict[str, torch.Tensor] = {n: g.new3(device) for n in list(PINGPONG) + ["gz"] + cfg.tracer_names()}
-        self.scratch = {n: g.new3(device) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc", "riem_scr")}
+        self.scratch = {n: g.new3(device) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc", "riem_scr", "du", "dv")}
         # target coordinate of the vertical remapping (pe2 = ak + bk * ps)
         ak, bk = cfg.target_coordinate()
         self.coord = {"ak": torch.from_numpy(ak).to(device), "bk": torch.from_numpy(bk).to(device)}
@@ -172,9 +173,9 @@ class Dycore:
         Transfers run on an upload and a download stream (both PCIe
         directions at once) and overlap the compute they do not feed: the
         tracers' uploads run during the acoustic substeps (first needed by
-        tracer_2d); u, v and gz are final after the substeps and download
-        during tracer advection and remapping; the tracers, delp, pt and w
-        (rewritten by the remap mapping) download at the end of the step.  Device staging is a ring (three input stages, two output
+        tracer_2d); gz is final after the substeps and downloads during
+        tracer advection and remapping; everything the remapping rewrites
+        (tracers, delp, pt, w, u, v) downloads at the end of the step.  Device staging is a ring (three input stages, two output
         stages), so successive calls pipeline: the next call's uploads
         overlap this call's compute, this call's downloads the next call's
         compute.  A call whose inputs are the previous call's outputs (a
@@ -184,7 +185,7 @@ class Dycore:
         tracers = set(self.cfg.tracer_names())
         trc = [n for n in h_in if n in tracers]           # uploaded during the substeps
         dyn = [n for n in h_in if n not in tracers]       # uploaded before the step
-        late = [n for n in h_in if n in tracers or n in ("delp", "pt", "w")]  # rewritten by remap_map
+        late = [n for n in h_in if n in tracers or n in ("delp", "pt", "w", "u", "v")]  # rewritten by the remap
         early = [n for n in h_in if n not in late]
         stages = self._io_stages(list(h_in))
         si, so = self._io_calls % 3, self._io_calls % 2
@@ -306,23 +307,43 @@ class Dycore:
         self.swap(*qs)
 
     def remap(self) -> None:
-        """remap_profile of every remapped field (the tracers, then pt and w):
-        the remap_tracers program plus the remap_profile program per
-        thermodynamic field, in one launch."""
-        fields = [self.f("delp")]
-        for q in self.cfg.remapped():
-            fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4")]
-        self.launch("remap_tracers", "fv3b_remap_profile", fields, [], self.dom_ifaces)
+        """remap_profile of every remapped field: the tracers, pt and w at
+        delp (the remap_tracers program, and the remap_profile program per
+        field), and the D-grid winds at the layer thickness of their points
+        (fv3b_face_thickness; delp's halo is refreshed at the tracer halo
+        point).  One launch per kernel, the field groups sharing it."""
+        self.launch("remap_tracers", "fv3b_face_thickness", [self.f("delp"), self.s("du"), self.s("dv")], [],
+                    self.dom_layers)
+        fields, counts = [], []
+        for thick, names in self._remap_groups():
+            counts.append(float(len(names)))
+            fields.append(thick)
+            for q in names:
+                fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4")]
+        self.launch("remap_tracers", "fv3b_remap_profile", fields, counts, self.dom_ifaces)
+
+    def _remap_groups(self):
+        return [(self.f("delp"), self.cfg.remapped()), (self.s("du"), ["u"]), (self.s("dv"), ["v"])]
 
     def remap_map(self) -> None:
         """Lagrangian -> Eulerian: every remapped field's profile integrated
-        over the target layers (pe2 = ak + bk * ps), delp <- pe2 differences."""
-        qs = self.cfg.remapped()
-        fields = [self.f("delp")] + [self.grid.abi(self.coord[n], rank=1) for n in ("ak", "bk")]
-        for q in qs:
-            fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4"), self.a(q)]
-        self.launch("remap_map", "fv3b_remap_map", fields, [], self.dom_ifaces)
-        self.swap(*qs)
+        over the target layers (pe2 = ak + bk * ps of its thickness), each
+        thickness <- its pe2 differences (delp; the winds' are scratch)."""
+        coord = [self.grid.abi(self.coord[n], rank=1) for n in ("ak", "bk")]
+        groups = self._remap_groups()
+        swapped = []
+        # the scalars' group (10 fields) and the winds' single-field groups in
+        # separate launches (measured: one launch of all three is slower)
+        for launch in (groups[:1], groups[1:]):
+            fields, counts = list(coord), []
+            for thick, names in launch:
+                counts.append(float(len(names)))
+                fields.append(thick)
+                for q in names:
+                    fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4"), self.a(q)]
+                    swapped.append(q)
+            self.launch("remap_map", "fv3b_remap_map", fields, counts, self.dom_ifaces)
+        self.swap(*swapped)
 
     def phases(self):
         """One timestep as a generator: enqueues the programs on the current
@@ -341,7 +362,7 @@ class Dycore:
             self.nh_d()
             yield ["pef", "gz"]
             self.p_grad_d()
-        yield cfg.tracer_names() + list(ACCUM)
+        yield cfg.tracer_names() + list(ACCUM) + ["delp"]  # (delp: the winds' remapping thickness)
         self.tracer_2d()
         self.remap()
         self.remap_map()
@@ -387,4 +408,4 @@ KERNELS = {"fv3b_c_grid": 3, "fv3b_d_sw": 2}
 
 def kernels_per_step(cfg: RunConfig) -> int:
     per_sub = 3 + KERNELS["fv3b_c_grid"] + KERNELS["fv3b_d_sw"] + 1 + 1
-    return cfg.n_split * per_sub + 1 + 1 + 1 + 1
+    return cfg.n_split * per_sub + 1 + 1 + 2 + 2  # tracer halo, tracer_2d, face thickness + profiles, maps
