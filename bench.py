@@ -315,10 +315,14 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     nk_prog = {"c_grid": cfg.nk + 1, "nh_d": cfg.nk + 1, "p_grad_d": cfg.nk + 1, "remap_tracers": cfg.nk + 1}
     progs = [n for n in per_node if n != "halo"]
     doms = {n: (cfg.ni, cfg.nj, nk_prog.get(n, cfg.nk)) for n in progs}
+    # the remapping: the profile launch covers the scalars and the winds, the
+    # mapping runs as the scalars' and the winds' launches
     if "remap_map" in doms:
         doms["remap_map"] = (cfg.ni, cfg.nj, cfg.nk + 1, len(cfg.remapped()))
+    if "remap_map_winds" in doms:
+        doms["remap_map_winds"] = (cfg.ni, cfg.nj, cfg.nk + 1, 2)
     if "remap_tracers" in doms:
-        doms["remap_tracers"] = (cfg.ni, cfg.nj, cfg.nk + 1, len(cfg.remapped()))
+        doms["remap_tracers"] = (cfg.ni, cfg.nj, cfg.nk + 1, len(cfg.remapped()) + 2)
     report = perf_model.build_report({n: per_node[n] for n in progs}, doms, peak * 1e9)
     by = {e.kernel: e for e in report.entries}
     top = max(progs, key=lambda n: node_total[n])

@@ -312,7 +312,7 @@ class Dycore:
         field), and the D-grid winds at the layer thickness of their points
         (fv3b_face_thickness; delp's halo is refreshed at the tracer halo
         point).  One launch per kernel, the field groups sharing it."""
-        self.launch("remap_tracers", "fv3b_face_thickness", [self.f("delp"), self.s("du"), self.s("dv")], [],
+        self.launch("remap_faces", "fv3b_face_thickness", [self.f("delp"), self.s("du"), self.s("dv")], [],
                     self.dom_layers)
         fields, counts = [], []
         for thick, names in self._remap_groups():
@@ -334,7 +334,7 @@ class Dycore:
         swapped = []
         # the scalars' group (10 fields) and the winds' single-field groups in
         # separate launches (measured: one launch of all three is slower)
-        for launch in (groups[:1], groups[1:]):
+        for node, launch in (("remap_map", groups[:1]), ("remap_map_winds", groups[1:])):
             fields, counts = list(coord), []
             for thick, names in launch:
                 counts.append(float(len(names)))
@@ -342,7 +342,7 @@ class Dycore:
                 for q in names:
                     fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4"), self.a(q)]
                     swapped.append(q)
-            self.launch("remap_map", "fv3b_remap_map", fields, counts, self.dom_ifaces)
+            self.launch(node, "fv3b_remap_map", fields, counts, self.dom_ifaces)
         self.swap(*swapped)
 
     def phases(self):

@@ -32,7 +32,10 @@ def unique_bytes(program: str, domain) -> tuple[int, str]:
     """(bytes, source) of one launch of `program` on `domain`.  The remap
     mapping (not a .stn program: its source-layer search is data dependent)
     takes ``domain = (ni, nj, nk + 1, nq)``."""
-    if program == "remap_map":
+    if program == "remap_faces":  # fv3b_face_thickness: delp read, du / dv written
+        ni, nj, nk = domain[:3]
+        return 8 * 3 * ni * nj * nk, "analytic (each operand level once)"
+    if program in ("remap_map", "remap_map_winds"):
         ni, nj, nki, nq = domain
         cells = ni * nj * (nki - 1)
         # delp read and rewritten; per tracer q, a4_2, a4_3, a4_4 read, q_out written; ak, bk

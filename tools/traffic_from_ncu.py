@@ -56,7 +56,9 @@ def programs(seq):
         elif "remap_kernel" in name:
             key = "remap_tracers"
         elif "remap_map" in name:
-            key = "remap_map"
+            key = "remap_map_winds" if "remap_map" in prog else "remap_map"
+        elif "face_thickness" in name:
+            key = "remap_faces"
         elif "halo" in name:
             key = "halo"
         else:
