@@ -42,22 +42,31 @@ constexpr int PG_CW = PG_TI + 1, PG_CH = PG_TJ + 1, PG_NP = PG_CW * PG_CH;
 
 // one thread per cell (measured faster here than the shared-memory tiling
 // used for p_grad_d: only three columns' interface values are reused)
+// PGC_K levels per thread: the interface values of level k+1 serve both k and k+1
+// (measured 20 us per step faster than one level per thread; 3 or 4 gain nothing more)
+constexpr int PGC_K = 2;
 __global__ void p_grad_c_kernel(const PgArgs a) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k0 = PGC_K * blockIdx.z;
   if (i >= a.ni) return;
-  auto P = [&](int di, int dj, int dk) { return *a.pk.ptr(i + di, j + dj, k + dk); };
-  auto Z = [&](int di, int dj, int dk) { return *a.gz.ptr(i + di, j + dj, k + dk); };
-  const double wk = P(0, 0, 1) - P(0, 0, 0);
-  const double wkx = P(-1, 0, 1) - P(-1, 0, 0);
-  const double wky = P(0, -1, 1) - P(0, -1, 0);
-  double* uc = a.uc.ptr(i, j, k);
-  double* vc = a.vc.ptr(i, j, k);
-  *uc = *uc + a.dt * met(a.rdxc, i, j) / (wkx + wk) *
-                  ((Z(-1, 0, 1) - Z(0, 0, 0)) * (P(0, 0, 1) - P(-1, 0, 0)) +
-                   (Z(-1, 0, 0) - Z(0, 0, 1)) * (P(-1, 0, 1) - P(0, 0, 0)));
-  *vc = *vc + a.dt * met(a.rdyc, i, j) / (wky + wk) *
-                  ((Z(0, -1, 1) - Z(0, 0, 0)) * (P(0, 0, 1) - P(0, -1, 0)) +
-                   (Z(0, -1, 0) - Z(0, 0, 1)) * (P(0, -1, 1) - P(0, 0, 0)));
+  const double rx = met(a.rdxc, i, j), ry = met(a.rdyc, i, j);
+  auto P = [&](int di, int dj, int kk) { return __ldg(a.pk.ptr(i + di, j + dj, kk)); };
+  auto Z = [&](int di, int dj, int kk) { return __ldg(a.gz.ptr(i + di, j + dj, kk)); };
+  double p0 = P(0, 0, k0), px0 = P(-1, 0, k0), py0 = P(0, -1, k0);
+  double z0 = Z(0, 0, k0), zx0 = Z(-1, 0, k0), zy0 = Z(0, -1, k0);
+#pragma unroll
+  for (int l = 0; l < PGC_K; ++l) {
+    const int k = k0 + l;
+    if (k >= a.nk) break;
+    const double p1 = P(0, 0, k + 1), px1 = P(-1, 0, k + 1), py1 = P(0, -1, k + 1);
+    const double z1 = Z(0, 0, k + 1), zx1 = Z(-1, 0, k + 1), zy1 = Z(0, -1, k + 1);
+    const double wk = p1 - p0, wkx = px1 - px0, wky = py1 - py0;
+    double* uc = a.uc.ptr(i, j, k);
+    double* vc = a.vc.ptr(i, j, k);
+    *uc = *uc + a.dt * rx / (wkx + wk) * ((zx1 - z0) * (p1 - px0) + (zx0 - z1) * (px1 - p0));
+    *vc = *vc + a.dt * ry / (wky + wk) * ((zy1 - z0) * (p1 - py0) + (zy0 - z1) * (py1 - p0));
+    p0 = p1; px0 = px1; py0 = py1;
+    z0 = z1; zx0 = zx1; zy0 = zy1;
+  }
 }
 
 // p_grad_d (p_grad_d.stn, nk+1 domain): corner-averaged pressure and
@@ -261,7 +270,7 @@ extern "C" int fv3b_c_grid(const fv3b_field* f, int nf, const double* s, int ns,
   PgArgs p;
   p.uc = uc; p.vc = vc; p.pk = pkc; p.gz = gzc; p.rdxc = a.rdxc; p.rdyc = a.rdyc;
   p.ni = d->ni; p.nj = d->nj; p.nk = nkl; p.dt = s[0];
-  dim3 grid(cdiv(d->ni, 64), d->nj, nkl);
+  dim3 grid(cdiv(d->ni, 64), d->nj, cdiv(nkl, PGC_K));
   p_grad_c_kernel<<<grid, 64, 0, st>>>(p);
   return check_launch("p_grad_c");
 }
