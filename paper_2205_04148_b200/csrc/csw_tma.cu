@@ -22,7 +22,7 @@ namespace fv3b {
 
 namespace {
 
-// 32x8 tiles: two CTAs of 8 warps per SM (112 KB of shared memory each)
+// 32x8 tiles: two CTAs of 10 warps per SM (112 KB of shared memory each)
 #ifndef FV3B_CS_NT
 #define FV3B_CS_NT 320  // 10 warps: measured 1% faster than 8, 12 no better
 #endif
