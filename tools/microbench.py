@@ -9,7 +9,7 @@ from paper_2205_04148_b200.inputs import synthetic_inputs
 from paper_2205_04148_b200.traffic import compulsory_bytes
 
 CASES = [("copy", (192, 192, 80)), ("fv_tp_2d", (192, 192, 80)), ("fv_tp_2d", (384, 384, 80)),
-         ("tracer_2d", (384, 384, 80))]
+         ("tracer_2d", (384, 384, 80)), ("nh_d", (192, 192, 81)), ("riem_solver_c", (192, 192, 81))]
 if len(sys.argv) > 1:
     CASES = [c for c in CASES if c[0] in sys.argv[1:]]
 peak = 6541.8
