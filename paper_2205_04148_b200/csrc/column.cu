@@ -636,13 +636,13 @@ struct RemapMapArgs {
   int nq, ni, nj, nk;  // nk layers
 };
 
-#ifndef FV3B_MP_F
-#define FV3B_MP_F 2
-#endif
-constexpr int MP_F = FV3B_MP_F;           // fields per thread
+// fields per thread (kernel template): 4 for wide groups, 2 for narrow ones
+// (measured: 4-5 best for the 10 scalar fields, 2 for the single-field wind
+// groups, whose threads then carry no second field)
 constexpr int MP_COLS = 32, MP_TY = 16;  // blockDim.y = min(ceil(nq / MP_F), MP_TY)
 constexpr double MP_R3 = 1.0 / 3.0, MP_R23 = 2.0 / 3.0;  // the oracle's R3, R23 (same roundings)
 
+template <int MP_F>
 __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapMapArgs a) {
   // map1_ppm's walk over the source layers only moves downwards, so the
   // Lagrangian interfaces pe1 are produced by a running sum as it advances
@@ -842,13 +842,17 @@ extern "C" int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int 
   if (d->ni <= 0 || d->nj <= 0) return FV3B_OK;
   int maxc = 1;
   for (int g = 0; g < ng; ++g) maxc = cnt[g] > maxc ? cnt[g] : maxc;
-  const int ty = cdiv(maxc, MP_F) < MP_TY ? cdiv(maxc, MP_F) : MP_TY;
+  const int F = maxc >= 4 ? 4 : 2;
+  const int ty = cdiv(maxc, F) < MP_TY ? cdiv(maxc, F) : MP_TY;
   a.ncb = ty >= 4 ? 1 : 4 / ty;  // at least 4 warps per CTA
   const size_t bytes = (size_t)2 * (a.nk + 1) * sizeof(double);
-  if (bytes > 48 * 1024 &&
-      cudaFuncSetAttribute(remap_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+  const void* kern = F == 4 ? (const void*)remap_map_kernel<4> : (const void*)remap_map_kernel<2>;
+  if (bytes > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
     return check_launch("remap_map smem attribute");
-  dim3 grid(cdiv(a.ni * a.nj, MP_COLS * a.ncb), ng);
-  remap_map_kernel<<<grid, dim3(MP_COLS, ty * a.ncb), bytes, (cudaStream_t)stream>>>(a);
+  dim3 grid(cdiv(a.ni * a.nj, MP_COLS * a.ncb), ng), block(MP_COLS, ty * a.ncb);
+  if (F == 4)
+    remap_map_kernel<4><<<grid, block, bytes, (cudaStream_t)stream>>>(a);
+  else
+    remap_map_kernel<2><<<grid, block, bytes, (cudaStream_t)stream>>>(a);
   return check_launch("remap_map");
 }
