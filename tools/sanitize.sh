@@ -1,0 +1,7 @@
+# compute-sanitizer over one small eager timestep: memory errors, shared-memory
+# races, barrier misuse (summaries into gpurun_out/sanitize_*.txt)
+for tool in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_step.py > gpurun_out/sanitize_$tool.txt 2>&1
+  echo "exit $?" >> gpurun_out/sanitize_$tool.txt
+done
+tail -n 4 gpurun_out/sanitize_*.txt
