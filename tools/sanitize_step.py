@@ -15,3 +15,14 @@ d = Dycore(cfg, initial_state(cfg))
 d.step()
 torch.cuda.synchronize()
 print("step done")
+# the program-level kernels the step does not launch (run_b200, ragged domains,
+# full-tile placement: edge regions fire)
+from paper_2205_04148_b200.executor import run_b200
+from paper_2205_04148_b200.inputs import synthetic_inputs
+
+for name, dom, place in (("fv_tp_2d", (37, 21, 4), (False,) * 4), ("c_sw", (37, 21, 3), (True,) * 4),
+                         ("riem_solver_c", (33, 7, 9), (False,) * 4), ("remap_profile", (33, 7, 9), (False,) * 4),
+                         ("copy", (33, 17, 5), (False,) * 4)):
+    run_b200(name, synthetic_inputs(name, dom, 1), dom, placement=place)
+torch.cuda.synchronize()
+print("programs done")
