@@ -182,6 +182,21 @@ int fv3b_halo_pack_rects(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_halo_unpack_rects(const fv3b_field* f, int nf, const double* s, int ns,
                            const fv3b_domain* d, void* stream);
 
+/*   fv3b_halo_peer_rects  the same strips without a message buffer: each
+ *                       rectangle goes from a source field straight into a
+ *                       destination field that may be another rank's
+ *                       allocation (CUDA IPC / peer-mapped over NVLink, or
+ *                       another block on the same device).  fields: nf
+ *                       sources, then rectangle r's destination of field t
+ *                       at index nf + r*nf + t (all with the sources'
+ *                       strides and level count).  scalars: [nf, nrect,
+ *                       then (src i0, src j0, dst i0, dst j0, w, h) per
+ *                       rectangle, interior-relative].  Up to 32 fields, 8
+ *                       rectangles.  Replaces pack + send/recv + unpack of
+ *                       the paper's halo updater. */
+int fv3b_halo_peer_rects(const fv3b_field* f, int nf, const double* s, int ns,
+                         const fv3b_domain* d, void* stream);
+
 /*   fv3b_halo_gather / fv3b_halo_scatter  index-list halo movement for the
  *                       cubed-sphere update (edge strips arrive rotated and,
  *                       for vector pairs, component-swapped with a sign;

@@ -178,6 +178,76 @@ static int rects_call(const fv3b_field* f, int nf, const double* s, int ns, cons
 }
 
 // ---------------------------------------------------------------------------
+// Peer-memory strip copies: the decomposed-domain halo update without
+// message buffers (parallel.PeerHalo).  Each rectangle of each field goes
+// straight from the source field to a destination field that may live in
+// another rank's allocation (a CUDA-IPC / peer mapping over NVLink, or
+// another block on the same device): the sender's edge strip is stored
+// into the neighbour's halo (posted stores over NVLink), replacing pack +
+// ncclSend/ncclRecv + unpack with one launch per rank.
+// ---------------------------------------------------------------------------
+constexpr int PEER_MAXF = HALO_MAXF;
+
+struct PeerArgs {
+  const double* src[PEER_MAXF];
+  double* dst[RECT_MAX][PEER_MAXF];
+  int64_t sj, sk;
+  int si0[RECT_MAX], sj0[RECT_MAX], di0[RECT_MAX], dj0[RECT_MAX], w[RECT_MAX], h[RECT_MAX];
+  int nrect, nf;
+};
+
+__global__ void peer_kernel(const PeerArgs a) {
+  const int r = blockIdx.z % a.nrect, t = blockIdx.z / a.nrect, k = blockIdx.y;
+  const int w = a.w[r], n = w * a.h[r];
+  const double* s = a.src[t] + (int64_t)k * a.sk + a.si0[r] + (int64_t)a.sj0[r] * a.sj;
+  double* o = a.dst[r][t] + (int64_t)k * a.sk + a.di0[r] + (int64_t)a.dj0[r] * a.sj;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int64_t off = e % w + (int64_t)(e / w) * a.sj;
+    o[off] = s[off];
+  }
+}
+
+static int peer_call(const fv3b_field* f, int ntot, const double* s, int ns, const fv3b_domain* d, void* stream) {
+  // scalars: [nf, nrect, (src i0, src j0, dst i0, dst j0, w, h) x nrect]
+  // fields: nf sources, then rectangle r's destination of field t at nf + r*nf + t
+  if (f == nullptr || d == nullptr || s == nullptr || ns < 2) return fail(FV3B_EINVAL, "halo peer: bad arguments");
+  PeerArgs a;
+  a.nf = (int)s[0];
+  a.nrect = (int)s[1];
+  if (a.nf < 1 || a.nf > PEER_MAXF || a.nrect < 1 || a.nrect > RECT_MAX || ns != 2 + 6 * a.nrect ||
+      ntot != a.nf * (1 + a.nrect))
+    return fail(FV3B_EINVAL, "halo peer: 1..%d fields, 1..%d rectangles, 2 + 6*nrect scalars, nf*(1+nrect) fields",
+                PEER_MAXF, RECT_MAX);
+  int levels[PEER_MAXF], lv[PEER_MAXF];
+  double* o[PEER_MAXF];
+  FV3B_TRY(collect(f, a.nf, d, 0, o, levels, &a.sj, &a.sk));
+  for (int t = 0; t < a.nf; ++t) a.src[t] = o[t];
+  for (int r = 0; r < a.nrect; ++r) {
+    int64_t sj, sk;
+    FV3B_TRY(collect(f + a.nf * (1 + r), a.nf, d, 0, a.dst[r], lv, &sj, &sk));
+    if (sj != a.sj || sk != a.sk) return fail(FV3B_ELAYOUT, "halo peer: destinations must share the sources' strides");
+    for (int t = 0; t < a.nf; ++t)
+      if (lv[t] != levels[t] || levels[t] != levels[0])
+        return fail(FV3B_EINVAL, "halo peer: fields must share their level count");
+  }
+  int maxn = 1;
+  for (int r = 0; r < a.nrect; ++r) {
+    const double* q = s + 2 + 6 * r;
+    a.si0[r] = (int)q[0];
+    a.sj0[r] = (int)q[1];
+    a.di0[r] = (int)q[2];
+    a.dj0[r] = (int)q[3];
+    a.w[r] = (int)q[4];
+    a.h[r] = (int)q[5];
+    if (a.w[r] <= 0 || a.h[r] <= 0) return fail(FV3B_EINVAL, "halo peer: empty rectangle %d", r);
+    maxn = a.w[r] * a.h[r] > maxn ? a.w[r] * a.h[r] : maxn;
+  }
+  dim3 grid(cdiv(maxn, 256) < 16 ? cdiv(maxn, 256) : 16, levels[0], a.nrect * a.nf);
+  peer_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch("fv3b_halo_peer_rects");
+}
+
+// ---------------------------------------------------------------------------
 // Index-list gather / scatter: the cubed-sphere halo update (cubesphere.py),
 // whose strips arrive rotated and component-swapped.  Entry s of a gather
 // list is (field slot, interior-relative cell offset); of a scatter list
@@ -304,6 +374,11 @@ extern "C" int fv3b_halo_pack_rects(const fv3b_field* f, int nf, const double* s
 extern "C" int fv3b_halo_unpack_rects(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                                       void* stream) {
   return rects_call(f, nf, s, ns, d, stream, true);
+}
+
+extern "C" int fv3b_halo_peer_rects(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                    void* stream) {
+  return peer_call(f, nf, s, ns, d, stream);
 }
 
 extern "C" int fv3b_halo_gather(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,

@@ -22,6 +22,10 @@ SURVEY 8e).  Here:
   the B200 box, gloo on CPU); messages to the rank itself (a periodic wrap
   along an undecomposed axis) are device copies.
 * :class:`DecomposedHalo` — the halo object a :class:`~.dycore.Dycore` calls.
+* :class:`PeerHalo` — the same update without messages: one
+  ``fv3b_halo_peer_rects`` launch stores this rank's strips straight into
+  the neighbours' halos (CUDA-IPC mappings over NVLink, :class:`IpcPeers`,
+  or blocks on the same device, :class:`LoopbackPeers`).
 * :class:`LoopbackCluster` — several ranks' dycores in one process on one
   GPU, advanced in lockstep with device copies as the transport; it checks
   the decomposed step against the single-domain step without a multi-GPU box.
@@ -252,18 +256,175 @@ class DecomposedHalo:
             timer.stop("halo")
 
 
+NEG = [DIRS.index((-di, -dj)) for di, dj in DIRS]
+
+
+class PeerHalo:
+    """Halo update by peer-memory stores (``fv3b_halo_peer_rects``): this
+    rank's eight edge / corner strips go straight into its neighbours' halos,
+    one launch per update for up to 32 fields -- no message buffers, no
+    pack / unpack, no NCCL on the data path.  On a multi-GPU node the
+    neighbours' state buffers are CUDA-IPC mappings (:class:`IpcPeers`) and
+    the stores travel over NVLink; in one process (:class:`LoopbackCluster`
+    with ``direct=True``) they are other blocks on the same device.
+
+    ``peers.tensor(direction, name)`` is the tensor the neighbour in that
+    direction currently holds under ``name`` (lockstep ranks share the
+    buffer assignment).  ``sync`` runs before and after the stores when the
+    ranks do not share one stream (cross-process ordering: the neighbours'
+    consumers of the old halo are done, and every store has landed before
+    anyone reads its halo)."""
+
+    def __init__(self, dycore, px: int, py: int, rank: int, peers, sync=None, copier=None):
+        self.d = dycore
+        g = dycore.grid
+        self.plan = HaloPlan(g.ni, g.nj, g.halo, px, py, rank)
+        self.peers = peers
+        self.sync = sync
+        self.copier = copier or (DevicePeerCopier(g) if dycore.device != "cpu" else TorchPeerCopier(g))
+        # direction d: my send strip -> the recv strip of direction -d of the neighbour peer[d]
+        self.rects = []
+        for d in range(8):
+            s, r = self.plan.send[d], self.plan.recv[NEG[d]]
+            self.rects.append((s.i0, s.j0, r.i0, r.j0, s.w, s.h))
+
+    def update(self, names) -> None:
+        timer = getattr(self.d, "timer", None)
+        if timer is not None:
+            timer.start("halo")
+        if self.sync is not None:
+            self.sync()
+        names = list(names)
+        for c in range(0, len(names), MAX_FIELDS):
+            chunk = names[c : c + MAX_FIELDS]
+            self.copier([self.d.cur[n] for n in chunk],
+                        [[self.peers.tensor(d, n) for n in chunk] for d in range(8)], self.rects)
+        if self.sync is not None:
+            self.sync()
+        if timer is not None:
+            timer.stop("halo")
+
+
+class DevicePeerCopier:
+    """``fv3b_halo_peer_rects``: every strip of every field, one launch."""
+
+    def __init__(self, grid):
+        from . import _lib
+
+        self._lib = _lib
+        self.grid = grid
+        self.dom = grid.domain()
+
+    def __call__(self, src, dst, rects) -> None:
+        g = self.grid
+        fields = [g.abi(t) for t in src] + [g.abi(t) for row in dst for t in row]
+        s = [float(len(src)), float(len(rects))] + [float(x) for r in rects for x in r]
+        self._lib.call("fv3b_halo_peer_rects", fields, s, self.dom, torch.cuda.current_stream().cuda_stream)
+
+
+class TorchPeerCopier:
+    """The same strip copies by tensor slicing (CPU tests)."""
+
+    def __init__(self, grid):
+        self.grid = grid
+
+    def _view(self, t, i0, j0, w, h):
+        g = self.grid
+        return t[:, g.halo + j0 : g.halo + j0 + h, g.i0 + i0 : g.i0 + i0 + w]
+
+    def __call__(self, src, dst, rects) -> None:
+        for (si, sj, di, dj, w, h), row in zip(rects, dst):
+            for s, o in zip(src, row):
+                self._view(o, di, dj, w, h).copy_(self._view(s, si, sj, w, h))
+
+
+class LoopbackPeers:
+    """The neighbours of one rank among dycores held in this process."""
+
+    def __init__(self, dycores, plan: HaloPlan):
+        self.d = dycores
+        self.plan = plan
+
+    def tensor(self, direction: int, name: str) -> torch.Tensor:
+        return self.d[self.plan.peer[direction]].cur[name]
+
+
+class IpcPeers:
+    """The neighbours' state buffers mapped into this process with CUDA IPC
+    (one process per GPU on an NVLink node; peer access is enabled by the
+    IPC open).  Every rank enumerates its state buffers in the same order
+    (sorted names, current then alternate), so buffer b of rank p is the one
+    rank p holds wherever this rank holds its own buffer b.  The handles
+    travel once, at construction, through ``all_gather_object`` on
+    ``group`` (any backend)."""
+
+    def __init__(self, dycore, plan: HaloPlan, group=None):
+        import pickle
+        from multiprocessing.reduction import ForkingPickler
+
+        import torch.distributed as dist
+        import torch.multiprocessing  # noqa: F401  (registers the tensor reducers)
+
+        self.d = dycore
+        self.plan = plan
+        mine = self._buffers(dycore)
+        # CUDA tensors pickle as IPC handles (CPU tensors move to shared memory)
+        shared = [bytes(ForkingPickler.dumps(t)) for t in mine]
+        self._index = {t.data_ptr(): b for b, t in enumerate(mine)}
+        gathered: list = [None] * dist.get_world_size(group)
+        dist.all_gather_object(gathered, shared, group=group)
+        self._peer = {}
+        for p in set(plan.peer):
+            self._peer[p] = mine if p == plan.rank else [pickle.loads(b) for b in gathered[p]]
+
+    @staticmethod
+    def _buffers(dycore) -> list:
+        out, seen = [], set()
+        for table in (dycore.cur, dycore.alt):
+            for n in sorted(table):
+                t = table[n]
+                if t.data_ptr() not in seen:
+                    seen.add(t.data_ptr())
+                    out.append(t)
+        return out
+
+    def tensor(self, direction: int, name: str) -> torch.Tensor:
+        return self._peer[self.plan.peer[direction]][self._index[self.d.cur[name].data_ptr()]]
+
+
+def ipc_sync(group=None, device: bool = True):
+    """Cross-process ordering for :class:`PeerHalo`: drain this rank's
+    stream (``device``), then a barrier on ``group``."""
+    import torch.distributed as dist
+
+    def sync():
+        if device:
+            torch.cuda.current_stream().synchronize()
+        dist.barrier(group=group)
+
+    return sync
+
+
 class LoopbackCluster:
     """px x py ranks' dycores in one process, stepped in lockstep; messages
     are device copies between the ranks' buffers (tests / single-GPU
     validation of the decomposed path)."""
 
-    def __init__(self, dycores, px: int = 1, py: int = 1, halos=None):
+    def __init__(self, dycores, px: int = 1, py: int = 1, halos=None, direct: bool = False):
         """``halos``: per-rank halo objects exposing pack / finish (default:
         a px x py doubly periodic decomposition; cubesphere.CubeHalo for
-        the six tiles of a cube)."""
+        the six tiles of a cube).  ``direct``: the decomposition's halo
+        updates as peer-memory stores (:class:`PeerHalo`) instead of
+        pack / copy / unpack."""
         self.d = dycores
-        self.halos = halos or [DecomposedHalo(d, px, py, r, transport=self, packer=None)
-                               for r, d in enumerate(dycores)]
+        if direct:
+            self.halos = []
+            for r, d in enumerate(dycores):
+                plan = HaloPlan(d.grid.ni, d.grid.nj, d.grid.halo, px, py, r)
+                self.halos.append(PeerHalo(d, px, py, r, LoopbackPeers(dycores, plan)))
+        else:
+            self.halos = halos or [DecomposedHalo(d, px, py, r, transport=self, packer=None)
+                                   for r, d in enumerate(dycores)]
         for d, h in zip(dycores, self.halos):
             d.halo = h
 
@@ -272,6 +433,10 @@ class LoopbackCluster:
 
     def exchange_all(self, reqs) -> None:
         """One halo update on every rank (``reqs[r]``: rank r's field list)."""
+        if isinstance(self.halos[0], PeerHalo):  # every rank's producers are queued: store the strips
+            for h, names in zip(self.halos, reqs):
+                h.update(names)
+            return
         chunks = [h.pack(names) for h, names in zip(self.halos, reqs)]
         for r, ch in enumerate(chunks):
             for c, (_, _, _, _, recv) in enumerate(ch):

@@ -49,8 +49,12 @@ def test_device_packer_single_rank_equals_periodic_kernel():
         assert torch.equal(a.cur[n], b.cur[n]), n
 
 
+@pytest.mark.parametrize("direct,graph", [(False, False), (True, False), (True, True)])
 @pytest.mark.parametrize("px,py", [(2, 2), (1, 2)])
-def test_loopback_decomposed_dycore_bitwise(px, py):
+def test_loopback_decomposed_dycore_bitwise(px, py, direct, graph):
+    """direct: PeerHalo (fv3b_halo_peer_rects stores into the neighbours'
+    halos) instead of pack / copy / unpack; graph: the lockstep step
+    captured as CUDA graphs and replayed."""
     import torch
 
     from paper_2205_04148_b200.config import RunConfig
@@ -68,10 +72,12 @@ def test_loopback_decomposed_dycore_bitwise(px, py):
     for r in range(px * py):
         ri, rj = r % px, r // px
         blocks.append(Dycore(blk_cfg, {n: _block(a, ri, rj, ni, nj, h) for n, a in st.items()}))
-    cluster = LoopbackCluster(blocks, px, py)
+    cluster = LoopbackCluster(blocks, px, py, direct=direct)
+    if graph:
+        cluster.capture()
     for _ in range(2):
         ref.step()
-        cluster.step()
+        cluster.replay() if graph else cluster.step()
     torch.cuda.synchronize()
     names = ["u", "v", "w", "delp", "pt", "gz", "pef", "q0", "q1", "q1_a4", "mfx", "cy"]
     full = ref.download(names)
@@ -81,3 +87,76 @@ def test_loopback_decomposed_dycore_bitwise(px, py):
         for n in names:
             want = _block(full[n], ri, rj, ni, nj, h)[h:-h, h:-h]
             assert np.array_equal(got[n][h:-h, h:-h], want), (r, n)
+
+
+def _ipc_worker(rank, port, q):
+    """One rank of a 1 x 2 decomposition in its own process on cuda:0; the
+    neighbour's state buffers are CUDA-IPC mappings (parallel.IpcPeers)."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.dycore import Dycore
+    from paper_2205_04148_b200.parallel import HaloPlan, IpcPeers, PeerHalo, ipc_sync
+    from paper_2205_04148_b200.state import initial_state
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        torch.cuda.set_device(0)
+        ni, nj, nk, px, py = 32, 24, 8, 1, 2
+        glob_cfg = RunConfig(ni=px * ni, nj=py * nj, nk=nk, n_split=2, nq=2, dt_atmos=30.0)
+        blk_cfg = RunConfig(ni=ni, nj=nj, nk=nk, n_split=2, nq=2, dt_atmos=30.0)
+        st = initial_state(glob_cfg)
+        h = glob_cfg.halo
+        ri, rj = rank % px, rank // px
+        d = Dycore(blk_cfg, {n: _block(a, ri, rj, ni, nj, h) for n, a in st.items()})
+        peers = IpcPeers(d, HaloPlan(ni, nj, h, px, py, rank))
+        d.halo = PeerHalo(d, px, py, rank, peers, sync=ipc_sync())
+        for _ in range(2):
+            d.step()
+        torch.cuda.synchronize()
+        names = ["u", "v", "w", "delp", "pt", "gz", "q0", "q1"]
+        got = d.download(names)
+        q.put((rank, {n: got[n][h:-h, h:-h] for n in names}))
+        dist.barrier()  # the neighbour's mappings stay valid until both are done
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ipc_peer_halo_two_processes_bitwise():
+    """Two processes (one per rank, as on an NVLink node) exchanging halos by
+    peer-memory stores through CUDA IPC, here both on cuda:0: bitwise the
+    single-domain dycore."""
+    import socket
+
+    import torch
+
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.dycore import Dycore
+    from paper_2205_04148_b200.state import initial_state
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    ni, nj, nk = 32, 24, 8
+    glob_cfg = RunConfig(ni=ni, nj=2 * nj, nk=nk, n_split=2, nq=2, dt_atmos=30.0)
+    ref = Dycore(glob_cfg, initial_state(glob_cfg))
+    for _ in range(2):
+        ref.step()
+    torch.cuda.synchronize()
+    h = glob_cfg.halo
+    full = ref.download(list(res[0]))
+    for r in range(2):
+        for n, got in res[r].items():
+            assert np.array_equal(got, _block(full[n], 0, r, ni, nj, h)[h:-h, h:-h]), (r, n)

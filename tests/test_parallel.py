@@ -143,3 +143,75 @@ def test_gloo_two_ranks_halo_exchange(px, py):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+@pytest.mark.parametrize("px,py", DECOMPS)
+def test_peer_halo_equals_global_periodic_fill(px, py):
+    """PeerHalo's store plan (my send strip of direction d -> the recv strip
+    of direction -d of neighbour peer[d]) fills every block's halo ring with
+    the single-domain periodic values; strips emulated by tensor slicing."""
+    from paper_2205_04148_b200.parallel import LoopbackPeers, PeerHalo, TorchPeerCopier
+
+    ni, nj, nk, h, nf = 9, 7, 3, 4, 3
+    grid = Grid(ni, nj, nk, halo=h)
+    glob = _global_fields(nf, px * ni, py * nj, grid.levels, h, seed=17)
+    stubs = []
+    for r in range(px * py):
+        ri, rj = r % px, r // px
+        fields = {f"f{t}": _local(grid, _block(glob[t], ri, rj, ni, nj, h), h, True) for t in range(nf)}
+        stubs.append(_Stub(grid, fields))
+    for r, s in enumerate(stubs):
+        halo = PeerHalo(s, px, py, r, LoopbackPeers(stubs, HaloPlan(ni, nj, h, px, py, r)),
+                        copier=TorchPeerCopier(grid))
+        halo.update([f"f{t}" for t in range(nf)])
+    for r, s in enumerate(stubs):
+        ri, rj = r % px, r // px
+        for t in range(nf):
+            got = grid.get(s.cur[f"f{t}"], ("I", "J", "K"), (h, h, 0), (ni + 2 * h, nj + 2 * h, grid.levels))
+            np.testing.assert_array_equal(got, _block(glob[t], ri, rj, ni, nj, h))
+
+
+def _ipc_worker(rank, world, port, px, py, q):
+    import torch.distributed as dist
+    import torch.multiprocessing as tmp
+
+    from paper_2205_04148_b200.parallel import IpcPeers, PeerHalo, TorchPeerCopier, ipc_sync
+
+    tmp.set_sharing_strategy("file_system")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ni, nj, nk, h, nf = 8, 6, 2, 3, 2
+        grid = Grid(ni, nj, nk, halo=h)
+        glob = _global_fields(nf, px * ni, py * nj, grid.levels, h, seed=23)
+        ri, rj = rank % px, rank // px
+        fields = {f"f{t}": _local(grid, _block(glob[t], ri, rj, ni, nj, h), h, True) for t in range(nf)}
+        stub = _Stub(grid, fields)
+        stub.alt = {}
+        peers = IpcPeers(stub, HaloPlan(ni, nj, h, px, py, rank))
+        halo = PeerHalo(stub, px, py, rank, peers, sync=ipc_sync(device=False), copier=TorchPeerCopier(grid))
+        halo.update([f"f{t}" for t in range(nf)])
+        ok = all(np.array_equal(grid.get(stub.cur[f"f{t}"], ("I", "J", "K"), (h, h, 0),
+                                          (ni + 2 * h, nj + 2 * h, grid.levels)),
+                                _block(glob[t], ri, rj, ni, nj, h)) for t in range(nf))
+        q.put((rank, ok))
+        dist.barrier()  # keep the shared buffers alive until every rank has checked
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("px,py", [(1, 2), (2, 1)])
+def test_ipc_peer_halo_two_ranks(px, py):
+    """The multi-process PeerHalo plumbing (IpcPeers handle exchange through
+    all_gather_object, buffer indexing, barrier ordering) on two gloo ranks,
+    with shared CPU tensors standing in for CUDA-IPC mappings."""
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, px, py, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
