@@ -197,6 +197,21 @@ int fv3b_halo_unpack_rects(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_halo_peer_rects(const fv3b_field* f, int nf, const double* s, int ns,
                          const fv3b_domain* d, void* stream);
 
+/*   fv3b_peer_barrier  stream-ordered barrier of a rank with its neighbours
+ *                       over peer-mapped 64-bit flag words (the ordering of
+ *                       fv3b_halo_peer_rects without host synchronisation).
+ *                       One thread bumps (bump != 0) or reads the rank's
+ *                       counter e, release-stores e into its word in every
+ *                       neighbour's flag array, then acquire-spins until each
+ *                       neighbour's word in its own array is >= e; after 10 s
+ *                       it sets the error word instead.  fields: none.
+ *                       scalars: [counter address bits, error-word address
+ *                       bits, bump, npeer, then (remote word, local word)
+ *                       address bits per neighbour], up to 8 neighbours.
+ *                       d may be NULL. */
+int fv3b_peer_barrier(const fv3b_field* f, int nf, const double* s, int ns,
+                      const fv3b_domain* d, void* stream);
+
 /*   fv3b_halo_gather / fv3b_halo_scatter  index-list halo movement for the
  *                       cubed-sphere update (edge strips arrive rotated and,
  *                       for vector pairs, component-swapped with a sign;

@@ -78,9 +78,18 @@ def entry(name: str):
 
 
 def call(name: str, fields: list[Field], scalars: list[float], domain: Domain, stream: int) -> None:
-    fn = entry(name)
+    call_prepared(name, prepare(fields, scalars), domain, stream)
+
+
+def prepare(fields: list[Field], scalars: list[float]) -> tuple:
+    """The ctypes argument arrays of a call, reusable while the buffers live."""
     farr = (Field * len(fields))(*fields)
     sarr = (ctypes.c_double * max(1, len(scalars)))(*scalars)
-    rc = fn(farr, len(fields), sarr, len(scalars), ctypes.byref(domain), ctypes.c_void_p(stream))
+    return farr, len(fields), sarr, len(scalars)
+
+
+def call_prepared(name: str, args: tuple, domain: Domain, stream: int) -> None:
+    farr, nf, sarr, ns = args
+    rc = entry(name)(farr, nf, sarr, ns, ctypes.byref(domain), ctypes.c_void_p(stream))
     if rc != 0:
         raise Fv3bError(name, rc, lib().fv3b_last_error().decode())

@@ -248,6 +248,78 @@ static int peer_call(const fv3b_field* f, int ntot, const double* s, int ns, con
 }
 
 // ---------------------------------------------------------------------------
+// Stream-ordered barrier among a rank and its neighbours over peer-mapped
+// flag words (parallel.FlagSync): one thread bumps (or reads) this rank's
+// update counter e, stores e with release semantics into the flag word it
+// owns in every neighbour's flag array, then spins (acquire loads, nanosleep
+// back-off) until every neighbour has stored >= e into this rank's array.
+// No host synchronisation, so a PeerHalo update is three stream-ordered
+// launches (arrive barrier, peer stores, stored barrier) and can be captured
+// in a CUDA graph.  The spin is bounded (10 s of globaltimer): a neighbour
+// that never arrives sets *err instead of hanging the device.
+// ---------------------------------------------------------------------------
+struct SigArgs {
+  unsigned long long* epoch;
+  unsigned long long* remote[RECT_MAX];  // my word in each neighbour's array
+  unsigned long long* local[RECT_MAX];   // each neighbour's word in my array
+  int* err;
+  int npeer, bump;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void signal_wait_kernel(const SigArgs a) {
+  if (threadIdx.x != 0) return;
+  unsigned long long e = *a.epoch;
+  if (a.bump) *a.epoch = ++e;
+  __threadfence_system();  // this stream's earlier writes (peer stores included) before the flags
+  for (int p = 0; p < a.npeer; ++p)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.remote[p]), "l"(e) : "memory");
+  const unsigned long long t0 = global_ns();
+  for (int p = 0; p < a.npeer; ++p) {
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.local[p]) : "memory");
+      if (v >= e) break;
+      if (global_ns() - t0 > 10000000000ull) {
+        atomicExch(a.err, 1);
+        return;
+      }
+      __nanosleep(200);
+    }
+  }
+  __threadfence_system();
+}
+
+static int signal_call(const double* s, int ns, void* stream) {
+  // scalars: [epoch addr bits, error-word addr bits, bump, npeer, (remote, local addr bits) x npeer]
+  if (s == nullptr || ns < 4) return fail(FV3B_EINVAL, "peer barrier: bad arguments");
+  SigArgs a;
+  auto ptr = [&](int i) {
+    uint64_t b;
+    memcpy(&b, &s[i], sizeof b);
+    return b;
+  };
+  a.epoch = reinterpret_cast<unsigned long long*>(ptr(0));
+  a.err = reinterpret_cast<int*>(ptr(1));
+  a.bump = s[2] != 0.0;
+  a.npeer = (int)s[3];
+  if (a.epoch == nullptr || a.err == nullptr || a.npeer < 0 || a.npeer > RECT_MAX || ns != 4 + 2 * a.npeer)
+    return fail(FV3B_EINVAL, "peer barrier: 0..%d neighbours, 4 + 2*n scalars, non-null counter", RECT_MAX);
+  for (int p = 0; p < a.npeer; ++p) {
+    a.remote[p] = reinterpret_cast<unsigned long long*>(ptr(4 + 2 * p));
+    a.local[p] = reinterpret_cast<unsigned long long*>(ptr(5 + 2 * p));
+    if (a.remote[p] == nullptr || a.local[p] == nullptr) return fail(FV3B_EINVAL, "peer barrier: null flag word");
+  }
+  signal_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(a);
+  return check_launch("fv3b_peer_barrier");
+}
+
+// ---------------------------------------------------------------------------
 // Index-list gather / scatter: the cubed-sphere halo update (cubesphere.py),
 // whose strips arrive rotated and component-swapped.  Entry s of a gather
 // list is (field slot, interior-relative cell offset); of a scatter list
@@ -379,6 +451,14 @@ extern "C" int fv3b_halo_unpack_rects(const fv3b_field* f, int nf, const double*
 extern "C" int fv3b_halo_peer_rects(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                                     void* stream) {
   return peer_call(f, nf, s, ns, d, stream);
+}
+
+extern "C" int fv3b_peer_barrier(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                 void* stream) {
+  (void)f;
+  (void)nf;
+  (void)d;
+  return signal_call(s, ns, stream);
 }
 
 extern "C" int fv3b_halo_gather(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,

@@ -270,10 +270,11 @@ class PeerHalo:
 
     ``peers.tensor(direction, name)`` is the tensor the neighbour in that
     direction currently holds under ``name`` (lockstep ranks share the
-    buffer assignment).  ``sync`` runs before and after the stores when the
-    ranks do not share one stream (cross-process ordering: the neighbours'
-    consumers of the old halo are done, and every store has landed before
-    anyone reads its halo)."""
+    buffer assignment).  ``sync(0)`` / ``sync(1)`` run before and after the
+    stores when the ranks do not share one stream: before, every neighbour
+    has finished reading its old halo; after, every store into this rank's
+    halo has landed.  :class:`FlagSync` does this on the device (graph-
+    capturable, no host round trip); :func:`ipc_sync` with host barriers."""
 
     def __init__(self, dycore, px: int, py: int, rank: int, peers, sync=None, copier=None):
         self.d = dycore
@@ -293,14 +294,14 @@ class PeerHalo:
         if timer is not None:
             timer.start("halo")
         if self.sync is not None:
-            self.sync()
+            self.sync(0)
         names = list(names)
         for c in range(0, len(names), MAX_FIELDS):
             chunk = names[c : c + MAX_FIELDS]
             self.copier([self.d.cur[n] for n in chunk],
                         [[self.peers.tensor(d, n) for n in chunk] for d in range(8)], self.rects)
         if self.sync is not None:
-            self.sync()
+            self.sync(1)
         if timer is not None:
             timer.stop("halo")
 
@@ -314,12 +315,17 @@ class DevicePeerCopier:
         self._lib = _lib
         self.grid = grid
         self.dom = grid.domain()
+        self._prepared: dict = {}  # buffer addresses -> ctypes argument arrays
 
     def __call__(self, src, dst, rects) -> None:
-        g = self.grid
-        fields = [g.abi(t) for t in src] + [g.abi(t) for row in dst for t in row]
-        s = [float(len(src)), float(len(rects))] + [float(x) for r in rects for x in r]
-        self._lib.call("fv3b_halo_peer_rects", fields, s, self.dom, torch.cuda.current_stream().cuda_stream)
+        key = tuple(t.data_ptr() for t in src) + tuple(t.data_ptr() for row in dst for t in row)
+        args = self._prepared.get(key)
+        if args is None:
+            g = self.grid
+            fields = [g.abi(t) for t in src] + [g.abi(t) for row in dst for t in row]
+            s = [float(len(src)), float(len(rects))] + [float(x) for r in rects for x in r]
+            args = self._prepared[key] = self._lib.prepare(fields, s)
+        self._lib.call_prepared("fv3b_halo_peer_rects", args, self.dom, torch.cuda.current_stream().cuda_stream)
 
 
 class TorchPeerCopier:
@@ -358,7 +364,7 @@ class IpcPeers:
     travel once, at construction, through ``all_gather_object`` on
     ``group`` (any backend)."""
 
-    def __init__(self, dycore, plan: HaloPlan, group=None):
+    def __init__(self, dycore, plan: HaloPlan, group=None, flags: torch.Tensor | None = None):
         import pickle
         from multiprocessing.reduction import ForkingPickler
 
@@ -368,6 +374,8 @@ class IpcPeers:
         self.d = dycore
         self.plan = plan
         mine = self._buffers(dycore)
+        if flags is not None:  # the FlagSync array travels as the last buffer
+            mine.append(flags)
         # CUDA tensors pickle as IPC handles (CPU tensors move to shared memory)
         shared = [bytes(ForkingPickler.dumps(t)) for t in mine]
         self._index = {t.data_ptr(): b for b, t in enumerate(mine)}
@@ -376,6 +384,13 @@ class IpcPeers:
         self._peer = {}
         for p in set(plan.peer):
             self._peer[p] = mine if p == plan.rank else [pickle.loads(b) for b in gathered[p]]
+        self.flags = flags
+
+    def flag_sync(self) -> FlagSync:
+        """The device-side barrier over the shared flag arrays."""
+        if self.flags is None:
+            raise ValueError("IpcPeers was built without a flag array")
+        return FlagSync(self.plan.rank, self.plan.peer, self.flags, {p: b[-1] for p, b in self._peer.items()})
 
     @staticmethod
     def _buffers(dycore) -> list:
@@ -397,7 +412,7 @@ def ipc_sync(group=None, device: bool = True):
     stream (``device``), then a barrier on ``group``."""
     import torch.distributed as dist
 
-    def sync():
+    def sync(phase: int):
         if device:
             torch.cuda.current_stream().synchronize()
         dist.barrier(group=group)
@@ -405,23 +420,80 @@ def ipc_sync(group=None, device: bool = True):
     return sync
 
 
+def _bits(addr: int) -> float:
+    return struct.unpack("d", struct.pack("Q", addr))[0]
+
+
+class FlagSync:
+    """Stream-ordered barrier of one rank with its neighbours for
+    :class:`PeerHalo` (``fv3b_peer_barrier``): every rank owns an int64
+    flag array [2, world] (phase 0 = arrived, 1 = stored; column p = rank
+    p's word); a barrier bumps (phase 0) or reuses (phase 1) the rank's
+    update counter, release-stores it into its column of each neighbour's
+    array and spins on its own array until every neighbour has caught up.
+    ``peer_flags[p]``: neighbour p's flag array as mapped in this process
+    (CUDA IPC across processes, the tensor itself in one process)."""
+
+    def __init__(self, rank: int, neighbours, flags: torch.Tensor, peer_flags: dict):
+        from . import _lib
+
+        self._lib = _lib
+        world = flags.shape[1]
+        self.flags = flags
+        self.epoch = torch.zeros(1, dtype=torch.int64, device=flags.device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=flags.device)
+        self._keep = dict(peer_flags)
+        nb = sorted(p for p in set(neighbours) if p != rank)
+        self.dom = _lib.Domain()
+        self._args = []
+        for phase in (0, 1):
+            sc = [_bits(self.epoch.data_ptr()), _bits(self.err.data_ptr()), 1.0 - phase, float(len(nb))]
+            for p in nb:
+                remote = peer_flags[p].data_ptr() + 8 * (phase * world + rank)
+                local = flags.data_ptr() + 8 * (phase * world + p)
+                sc += [_bits(remote), _bits(local)]
+            self._args.append(_lib.prepare([], sc))
+
+    def __call__(self, phase: int) -> None:
+        self._lib.call_prepared("fv3b_peer_barrier", self._args[phase], self.dom,
+                                torch.cuda.current_stream().cuda_stream)
+
+    def check(self) -> None:
+        """Raise if a barrier timed out (reads the device error word)."""
+        if int(self.err.item()):
+            raise RuntimeError("fv3b_peer_barrier: a neighbour did not arrive within 10 s")
+
+
+def new_flags(world: int, device) -> torch.Tensor:
+    """A rank's zeroed flag array for :class:`FlagSync`."""
+    return torch.zeros(2, world, dtype=torch.int64, device=device)
+
+
 class LoopbackCluster:
     """px x py ranks' dycores in one process, stepped in lockstep; messages
     are device copies between the ranks' buffers (tests / single-GPU
     validation of the decomposed path)."""
 
-    def __init__(self, dycores, px: int = 1, py: int = 1, halos=None, direct: bool = False):
+    def __init__(self, dycores, px: int = 1, py: int = 1, halos=None, direct: bool = False,
+                 flag_sync: bool = False):
         """``halos``: per-rank halo objects exposing pack / finish (default:
         a px x py doubly periodic decomposition; cubesphere.CubeHalo for
         the six tiles of a cube).  ``direct``: the decomposition's halo
         updates as peer-memory stores (:class:`PeerHalo`) instead of
-        pack / copy / unpack."""
+        pack / copy / unpack.  ``flag_sync`` (with ``direct``): every rank on
+        its own stream, ordered only by the device-side neighbour barriers
+        (:class:`FlagSync`), as separate processes would be."""
         self.d = dycores
+        self.streams = None
         if direct:
             self.halos = []
+            flags = [new_flags(len(dycores), d.device) for d in dycores] if flag_sync else None
+            if flag_sync:
+                self.streams = [torch.cuda.Stream() for _ in dycores]
             for r, d in enumerate(dycores):
                 plan = HaloPlan(d.grid.ni, d.grid.nj, d.grid.halo, px, py, r)
-                self.halos.append(PeerHalo(d, px, py, r, LoopbackPeers(dycores, plan)))
+                sync = FlagSync(r, plan.peer, flags[r], dict(enumerate(flags))) if flag_sync else None
+                self.halos.append(PeerHalo(d, px, py, r, LoopbackPeers(dycores, plan), sync=sync))
         else:
             self.halos = halos or [DecomposedHalo(d, px, py, r, transport=self, packer=None)
                                    for r, d in enumerate(dycores)]
@@ -434,8 +506,9 @@ class LoopbackCluster:
     def exchange_all(self, reqs) -> None:
         """One halo update on every rank (``reqs[r]``: rank r's field list)."""
         if isinstance(self.halos[0], PeerHalo):  # every rank's producers are queued: store the strips
-            for h, names in zip(self.halos, reqs):
-                h.update(names)
+            for r, (h, names) in enumerate(zip(self.halos, reqs)):
+                with self._on(r):
+                    h.update(names)
             return
         chunks = [h.pack(names) for h, names in zip(self.halos, reqs)]
         for r, ch in enumerate(chunks):
@@ -475,11 +548,25 @@ class LoopbackCluster:
         for d, (cur, alt) in zip(self.d, post):
             d.cur, d.alt = dict(cur), dict(alt)
 
+    def _on(self, r: int):
+        import contextlib
+
+        return torch.cuda.stream(self.streams[r]) if self.streams else contextlib.nullcontext()
+
     def step(self) -> None:
         gens = [d.phases() for d in self.d]
+        if self.streams:
+            for s in self.streams:
+                s.wait_stream(torch.cuda.current_stream())
         while True:
-            reqs = [next(g, None) for g in gens]
+            reqs = []
+            for r, g in enumerate(gens):
+                with self._on(r):
+                    reqs.append(next(g, None))
             if all(r is None for r in reqs):
-                return
+                break
             assert all(r is not None for r in reqs), "ranks out of lockstep"
             self.exchange_all(reqs)
+        if self.streams:
+            for s in self.streams:
+                torch.cuda.current_stream().wait_stream(s)

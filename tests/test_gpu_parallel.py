@@ -49,12 +49,14 @@ def test_device_packer_single_rank_equals_periodic_kernel():
         assert torch.equal(a.cur[n], b.cur[n]), n
 
 
-@pytest.mark.parametrize("direct,graph", [(False, False), (True, False), (True, True)])
+@pytest.mark.parametrize("mode", ["packed", "direct", "direct-graph", "flags"])
 @pytest.mark.parametrize("px,py", [(2, 2), (1, 2)])
-def test_loopback_decomposed_dycore_bitwise(px, py, direct, graph):
-    """direct: PeerHalo (fv3b_halo_peer_rects stores into the neighbours'
-    halos) instead of pack / copy / unpack; graph: the lockstep step
-    captured as CUDA graphs and replayed."""
+def test_loopback_decomposed_dycore_bitwise(px, py, mode):
+    """packed: pack / device copy / unpack; direct: PeerHalo
+    (fv3b_halo_peer_rects stores into the neighbours' halos), eager or
+    captured as CUDA graphs and replayed; flags: PeerHalo with every rank on
+    its own stream, ordered only by the device-side neighbour barriers
+    (fv3b_peer_barrier), as separate processes would be."""
     import torch
 
     from paper_2205_04148_b200.config import RunConfig
@@ -72,13 +74,17 @@ def test_loopback_decomposed_dycore_bitwise(px, py, direct, graph):
     for r in range(px * py):
         ri, rj = r % px, r // px
         blocks.append(Dycore(blk_cfg, {n: _block(a, ri, rj, ni, nj, h) for n, a in st.items()}))
-    cluster = LoopbackCluster(blocks, px, py, direct=direct)
+    graph = mode == "direct-graph"
+    cluster = LoopbackCluster(blocks, px, py, direct=mode != "packed", flag_sync=mode == "flags")
     if graph:
         cluster.capture()
     for _ in range(2):
         ref.step()
         cluster.replay() if graph else cluster.step()
     torch.cuda.synchronize()
+    if mode == "flags":
+        for h in cluster.halos:
+            h.sync.check()
     names = ["u", "v", "w", "delp", "pt", "gz", "pef", "q0", "q1", "q1_a4", "mfx", "cy"]
     full = ref.download(names)
     for r, d in enumerate(blocks):
@@ -89,7 +95,7 @@ def test_loopback_decomposed_dycore_bitwise(px, py, direct, graph):
             assert np.array_equal(got[n][h:-h, h:-h], want), (r, n)
 
 
-def _ipc_worker(rank, port, q):
+def _ipc_worker(rank, port, q, flags=False):
     """One rank of a 1 x 2 decomposition in its own process on cuda:0; the
     neighbour's state buffers are CUDA-IPC mappings (parallel.IpcPeers)."""
     import os
@@ -99,7 +105,7 @@ def _ipc_worker(rank, port, q):
 
     from paper_2205_04148_b200.config import RunConfig
     from paper_2205_04148_b200.dycore import Dycore
-    from paper_2205_04148_b200.parallel import HaloPlan, IpcPeers, PeerHalo, ipc_sync
+    from paper_2205_04148_b200.parallel import HaloPlan, IpcPeers, PeerHalo, ipc_sync, new_flags
     from paper_2205_04148_b200.state import initial_state
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -113,11 +119,15 @@ def _ipc_worker(rank, port, q):
         h = glob_cfg.halo
         ri, rj = rank % px, rank // px
         d = Dycore(blk_cfg, {n: _block(a, ri, rj, ni, nj, h) for n, a in st.items()})
-        peers = IpcPeers(d, HaloPlan(ni, nj, h, px, py, rank))
-        d.halo = PeerHalo(d, px, py, rank, peers, sync=ipc_sync())
+        peers = IpcPeers(d, HaloPlan(ni, nj, h, px, py, rank), flags=new_flags(2, "cuda") if flags else None)
+        sync = peers.flag_sync() if flags else ipc_sync()
+        d.halo = PeerHalo(d, px, py, rank, peers, sync=sync)
+        dist.barrier()
         for _ in range(2):
             d.step()
         torch.cuda.synchronize()
+        if flags:
+            sync.check()
         names = ["u", "v", "w", "delp", "pt", "gz", "q0", "q1"]
         got = d.download(names)
         q.put((rank, {n: got[n][h:-h, h:-h] for n in names}))
