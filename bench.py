@@ -211,7 +211,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     from paper_2205_04148_b200 import _lib
     from paper_2205_04148_b200.config import RunConfig
     from paper_2205_04148_b200.dycore import Dycore, kernels_per_step
-    from paper_2205_04148_b200.parallel import DecomposedHalo, grid_shape
+    from paper_2205_04148_b200.parallel import DecomposedHalo, HaloPlan, IpcPeers, PeerHalo, grid_shape, new_flags
     from paper_2205_04148_b200.state import initial_state
     from paper_2205_04148_b200 import perf_model
 
@@ -221,14 +221,21 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     px, py = grid_shape(world)
     state = initial_state(cfg)
     d = Dycore(cfg, state)
-    if world > 1:
+    if world > 1 and args.halo == "peer":
+        # halos stored straight into the neighbours' buffers (CUDA IPC over
+        # NVLink, fv3b_halo_peer_rects) behind device-side neighbour
+        # barriers (fv3b_peer_barrier): no host sync, so whole steps replay
+        # as CUDA graphs on every rank
+        peers = IpcPeers(d, HaloPlan(cfg.ni, cfg.nj, cfg.halo, px, py, rank), flags=new_flags(world, "cuda"))
+        d.halo = PeerHalo(d, px, py, rank, peers, sync=peers.flag_sync())
+    elif world > 1:
         # every rank owns one 192x192x80 block of a (px*192) x (py*192)
         # doubly periodic domain; halos move over NCCL (grouped send/recv)
         d.halo = DecomposedHalo(d, px, py, rank)
     torch.cuda.synchronize()
-    # single rank: whole timesteps replayed as CUDA graphs; decomposed:
-    # eager launches (the NCCL exchanges stay outside graph capture)
-    graphs = world == 1
+    # single rank and peer halos: whole timesteps replayed as CUDA graphs;
+    # NCCL halos: eager launches (the exchanges stay outside graph capture)
+    graphs = world == 1 or args.halo == "peer"
     run_step = d.replay if graphs else d.step
 
     def barrier():
@@ -359,6 +366,8 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         "config": {"workload": "C2 doubly periodic 192x192x80 fp64 dycore timestep (n_split=6, nq=8)",
                    "ni": cfg.ni, "nj": cfg.nj, "nk": cfg.nk, "n_split": cfg.n_split, "nq": cfg.nq,
                    "decomposition": f"{px}x{py}", "l2": "state 1.3 GB/GPU > 126 MB L2 (no flush)",
+                   "halo": "periodic kernel" if world == 1 else
+                           ("peer-memory stores over CUDA IPC + device barriers" if args.halo == "peer" else "NCCL send/recv"),
                    "timing": ("CUDA-graph replay of whole timesteps" if graphs else "eager launches, NCCL halo exchange") + ", CUDA events, max over ranks"},
         "e2e": {"value": cells / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes},
@@ -392,6 +401,8 @@ def main() -> None:
     ap.add_argument("--ni", type=int, default=192)
     ap.add_argument("--nk", type=int, default=80)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--halo", choices=("nccl", "peer"), default="nccl",
+                    help="N > 1 halo transport: NCCL send/recv, or peer-memory stores over CUDA IPC")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -399,7 +410,14 @@ def main() -> None:
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
-    if world > 1:
+    if world > 1 and os.environ.get("FV3B_SAME_GPU") == "1":
+        # functional check of the N > 1 code paths on a one-GPU box: every
+        # rank on cuda:0 (contexts time-slice; no timing meaning), gloo
+        import torch.distributed as dist
+
+        local = 0
+        dist.init_process_group("gloo")
+    elif world > 1:
         import torch
         import torch.distributed as dist
 
@@ -407,6 +425,10 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
         run_ours(args, rank, world, local)
+        if world > 1:  # peers' IPC mappings stay valid until every rank is done
+            import torch.distributed as dist
+
+            dist.barrier()
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -83,8 +83,8 @@ def test_loopback_decomposed_dycore_bitwise(px, py, mode):
         cluster.replay() if graph else cluster.step()
     torch.cuda.synchronize()
     if mode == "flags":
-        for h in cluster.halos:
-            h.sync.check()
+        for hal in cluster.halos:
+            hal.sync.check()
     names = ["u", "v", "w", "delp", "pt", "gz", "pef", "q0", "q1", "q1_a4", "mfx", "cy"]
     full = ref.download(names)
     for r, d in enumerate(blocks):

@@ -37,16 +37,28 @@ def main():
     single = Dycore(glob)
     packed = LoopbackCluster([Dycore(blk) for _ in range(4)], 2, 2)
     direct = LoopbackCluster([Dycore(blk) for _ in range(4)], 2, 2, direct=True)
+    flags = LoopbackCluster([Dycore(blk) for _ in range(4)], 2, 2, direct=True, flag_sync=True)
     for g, names in groups.items():
         out = {"group": g, "fields": len(names)}
         out["single_us"] = timed(lambda: single.halo.update(names))
         out["packed_us"] = timed(lambda: packed.exchange_all([names] * 4))
         out["direct_us"] = timed(lambda: direct.exchange_all([names] * 4))
+
+        def flagged():
+            for s in flags.streams:
+                s.wait_stream(torch.cuda.current_stream())
+            flags.exchange_all([names] * 4)
+            for s in flags.streams:
+                torch.cuda.current_stream().wait_stream(s)
+
+        out["flags_us"] = timed(flagged)
         # the same as captured graphs (launch overhead removed)
-        for key, cl in (("packed_graph_us", packed), ("direct_graph_us", direct)):
+        for key, fn in (("packed_graph_us", lambda: packed.exchange_all([names] * 4)),
+                        ("direct_graph_us", lambda: direct.exchange_all([names] * 4)),
+                        ("flags_graph_us", flagged)):
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr):
-                cl.exchange_all([names] * 4)
+                fn()
             out[key] = timed(gr.replay)
         print(json.dumps({k: (round(v, 1) if isinstance(v, float) else v) for k, v in out.items()}), flush=True)
 
