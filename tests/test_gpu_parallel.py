@@ -136,10 +136,13 @@ def _ipc_worker(rank, port, q, flags=False):
         dist.destroy_process_group()
 
 
-def test_ipc_peer_halo_two_processes_bitwise():
+@pytest.mark.parametrize("flags", [False, True])
+def test_ipc_peer_halo_two_processes_bitwise(flags):
     """Two processes (one per rank, as on an NVLink node) exchanging halos by
-    peer-memory stores through CUDA IPC, here both on cuda:0: bitwise the
-    single-domain dycore."""
+    peer-memory stores through CUDA IPC, here both on cuda:0, ordered by
+    host barriers or by the device-side neighbour barriers (the contexts
+    time-slice; the barrier spin is bounded): bitwise the single-domain
+    dycore."""
     import socket
 
     import torch
@@ -153,7 +156,7 @@ def test_ipc_peer_halo_two_processes_bitwise():
         port = s.getsockname()[1]
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, port, q, flags)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
