@@ -226,6 +226,16 @@ int fv3b_halo_gather(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_halo_scatter(const fv3b_field* f, int nf, const double* s, int ns,
                       const fv3b_domain* d, void* stream);
 
+/*   fv3b_memcpy2d  host I/O helper: `height` rows of `width` bytes from src
+ *                  (row pitch spitch bytes) to dst (pitch dpitch) on `stream`,
+ *                  host or device pointers (unified addressing; pinned host
+ *                  memory for asynchrony).  Used by tools/io_variants.py to
+ *                  measure interior-column transfers of halo-inclusive
+ *                  (I, J, K) arrays (not faster than whole arrays: the
+ *                  bidirectional PCIe rate drops with row-wise DMA). */
+int fv3b_memcpy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                  int64_t width, int64_t height, void* stream);
+
 /*   fv3b_transpose  state layout conversion for host I/O: copy the d->ni x
  *                   d->nj x d->nk region at f[0].data to f[1].data where one
  *                   field has unit K stride (the reference's numpy (I, J, K)

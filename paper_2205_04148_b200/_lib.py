@@ -93,3 +93,14 @@ def call_prepared(name: str, args: tuple, domain: Domain, stream: int) -> None:
     rc = entry(name)(farr, nf, sarr, ns, ctypes.byref(domain), ctypes.c_void_p(stream))
     if rc != 0:
         raise Fv3bError(name, rc, lib().fv3b_last_error().decode())
+
+
+def memcpy2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: int, stream: int) -> None:
+    """``fv3b_memcpy2d``: ``height`` rows of ``width`` bytes, pitches in bytes."""
+    fn = lib().fv3b_memcpy2d
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                   ctypes.c_int64, ctypes.c_void_p]
+    rc = fn(dst, dpitch, src, spitch, width, height, stream)
+    if rc != 0:
+        raise Fv3bError("fv3b_memcpy2d", rc, lib().fv3b_last_error().decode())

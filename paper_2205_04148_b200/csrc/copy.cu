@@ -180,3 +180,19 @@ extern "C" int fv3b_face_thickness(const fv3b_field* f, int nf, const double* s,
   fv3b::face_thickness_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(dp, du, dv, d->ni, d->nj);
   return fv3b::check_launch("fv3b_face_thickness");
 }
+
+// Host-I/O helper: one strided copy of `height` rows of `width` bytes
+// (pitches in bytes) between pinned host and device memory, on `stream`
+// (cudaMemcpy2DAsync, direction from the unified address space).  Measured
+// for moving only the interior columns of the host state (tools/io_variants.py):
+// 8% fewer bytes but no faster than whole arrays with both directions busy.
+extern "C" int fv3b_memcpy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                             int64_t height, void* stream) {
+  if (dst == nullptr || src == nullptr || width < 0 || height < 0 || dpitch < width || spitch < width)
+    return fv3b::fail(FV3B_EINVAL, "fv3b_memcpy2d: bad arguments");
+  if (width == 0 || height == 0) return FV3B_OK;
+  const cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)height,
+                                          cudaMemcpyDefault, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fv3b::fail(FV3B_ELAUNCH, "fv3b_memcpy2d: %s", cudaGetErrorString(e));
+  return FV3B_OK;
+}
