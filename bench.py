@@ -328,6 +328,8 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         doms["remap_map"] = (cfg.ni, cfg.nj, cfg.nk + 1, len(cfg.remapped()))
     if "remap_map_winds" in doms:
         doms["remap_map_winds"] = (cfg.ni, cfg.nj, cfg.nk + 1, 2)
+    if "moist_pk" in doms:
+        doms["moist_pk"] = (cfg.ni, cfg.nj, cfg.nk + 1, len(cfg.moist_names()))
     if "remap_tracers" in doms:
         doms["remap_tracers"] = (cfg.ni, cfg.nj, cfg.nk + 1, len(cfg.remapped()) + 2)
     report = perf_model.build_report({n: per_node[n] for n in progs}, doms, peak * 1e9)

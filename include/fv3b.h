@@ -116,6 +116,20 @@ int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int ns,
                    const fv3b_domain* d, void* stream);
 
+/* K5c pressure / heat-capacity diagnostics of the remapped state (FV3
+ *     fv_mapz pe, pk, pkz and moist_cv; oracle/thermo.py):
+ *     pe[0] = ptop, pe[k+1] = pe[k] + delp[k]; peln = log(pe); pk =
+ *     exp(akap * peln) (deterministic fdlibm log / exp, detmath.cuh); pkz =
+ *     (pk[k+1] - pk[k]) / (akap * (peln[k+1] - peln[k])); cvm = (1 - (qv + ql
+ *     + qs)) cv_air + qv cv_vap + ql c_liq + qs c_ice (ql = liquid + rain,
+ *     qs = ice + snow + graupel).  Program domain nk = interface levels.
+ *     fields: delp, 0..6 moist tracers (vapour, liquid, rain, ice, snow,
+ *     graupel; absent ones are 0), pe, peln, pk (interfaces), pkz, cvm
+ *     (layers; outputs must not alias).  scalars: ptop, akap, cv_air,
+ *     cv_vap, c_liq, c_ice. */
+int fv3b_moist_pk(const fv3b_field* f, int nf, const double* s, int ns,
+                  const fv3b_domain* d, void* stream);
+
 /* K2  c_sw.stn — C-grid half step.  fields: u, v, delp, pt, w (3-D); dx, dy,
  *     dxc, dyc, rdxc, rdyc, rarea, rarea_c, fc (2-D); uc, vc, delpc, ptc, wc
  *     (3-D outputs).  scalars: dt2. */

@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import interp, remap_map
+from . import interp, remap_map, thermo
 
 PERIODIC = interp.PERIODIC
 
@@ -131,6 +131,7 @@ class OracleDycore:
         remap_map.remap_map(st, cfg.remapped(), ak, bk, cfg.nk, self._h)
         for w, dw in (("u", "du"), ("v", "dv")):
             remap_map.remap_map(st, [w], ak, bk, cfg.nk, self._h, delp_key=dw)
+        thermo.apply(st, cfg.tracer_names()[:thermo.SPECIES], cfg.nk, self._h, thermo.constants(c))
 
     def step(self) -> None:
         for names in self.phases():

@@ -37,6 +37,8 @@ class RunConfig:
         "ptop": 300.0, "rdgas": 287.05, "grav": 9.80665, "gama": 1.4, "p_fac": 0.05,
         "dddmp": 0.2, "d2_bg": 0.0, "da_min": 1.0e8, "damp_w": 0.02,
         "ppm_p1": 7.0 / 12.0, "ppm_p2": -1.0 / 12.0,
+        # heat capacities of the post-remap diagnostics (FV3 constants; oracle/thermo.py)
+        "cp_air": 1004.6, "rvgas": 461.50, "c_liq": 4185.5, "c_ice": 1972.0,
     })
 
     @property
@@ -56,6 +58,17 @@ class RunConfig:
         remapped; DESIGN.md)."""
         return self.tracer_names() + ["pt", "w"]
 
+    def moist_names(self) -> list[str]:
+        """FV3's six water species (vapour, liquid, rain, ice, snow, graupel)
+        among the tracers: q0..q5 (fewer when nq < 6; absent species are 0)."""
+        return self.tracer_names()[:6]
+
+    def moist_scalars(self) -> list[float]:
+        """fv3b_moist_pk scalars: ptop, akap = rdgas / cp_air, cv_air =
+        cp_air - rdgas, cv_vap = 3 rvgas, c_liq, c_ice."""
+        c = self.consts
+        return [c["ptop"], c["rdgas"] / c["cp_air"], c["cp_air"] - c["rdgas"], 3.0 * c["rvgas"], c["c_liq"], c["c_ice"]]
+
     def target_coordinate(self):
         """ak, bk (nk+1) of the vertical remapping's target interfaces
         pe2 = ak + bk * ps: pure sigma below ptop, bk = k / nk."""
@@ -68,5 +81,7 @@ class RunConfig:
 # Prognostic / diagnostic state fields.  3-D fields have nk+1 levels
 # (interface-capable); 2-D fields are metrics and the surface w.
 STATE_3D = ["u", "v", "w", "delp", "pt", "gz", "pef", "uc", "vc", "cx", "cy", "xfa", "yfa", "mfx", "mfy", "dp1"]
+# post-remap diagnostics (fv3b_moist_pk): interface pe, peln, pk; layer pkz, cvm
+DIAG_3D = ["pe", "peln", "pk", "pkz", "cvm"]
 METRICS_2D = ["dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxc", "rdyc", "rdxa", "rdya", "area", "rarea", "rarea_c",
               "f0", "fc", "ws"]

@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .config import METRICS_2D, STATE_3D, RunConfig
+from .config import DIAG_3D, METRICS_2D, STATE_3D, RunConfig
 from .device import Grid
 
 C_METRICS = ("dx", "dy", "dxc", "dyc", "rdxc", "rdyc", "rarea", "rarea_c", "fc")
@@ -53,7 +53,7 @@ class Dycore:
         self.dom_layers = self.grid.domain(placement, nk=cfg.nk)
         self.dom_ifaces = self.grid.domain(placement, nk=cfg.nk + 1)
         g = self.grid
-        names3 = STATE_3D + cfg.tracer_names() + [f"{q}_{a}" for q in cfg.remapped() + ["u", "v"]
+        names3 = STATE_3D + DIAG_3D + cfg.tracer_names() + [f"{q}_{a}" for q in cfg.remapped() + ["u", "v"]
                                                   for a in ("a2", "a3", "a4")]
         self.cur: dict[str, torch.Tensor] = {n: g.new3(device) for n in names3}
         self.cur.update({n: g.new2(device) for n in METRICS_2D})
@@ -325,6 +325,14 @@ class Dycore:
     def _remap_groups(self):
         return [(self.f("delp"), self.cfg.remapped()), (self.s("du"), ["u"]), (self.s("dv"), ["v"])]
 
+    def moist_pk(self) -> None:
+        """Pressure and heat-capacity diagnostics of the remapped state: pe,
+        peln, pk at the interfaces, pkz and the moist cv at the layers
+        (fv3b_moist_pk; oracle/thermo.py)."""
+        fields = [self.f("delp")] + [self.f(q) for q in self.cfg.moist_names()]
+        fields += [self.f(n) for n in DIAG_3D]
+        self.launch("moist_pk", "fv3b_moist_pk", fields, self.cfg.moist_scalars(), self.dom_ifaces)
+
     def remap_map(self) -> None:
         """Lagrangian -> Eulerian: every remapped field's profile integrated
         over the target layers (pe2 = ak + bk * ps of its thickness), each
@@ -366,6 +374,7 @@ class Dycore:
         self.tracer_2d()
         self.remap()
         self.remap_map()
+        self.moist_pk()
 
     def step(self) -> None:
         """Enqueue one full timestep on the current stream."""
@@ -408,4 +417,4 @@ KERNELS = {"fv3b_c_grid": 3, "fv3b_d_sw": 2}
 
 def kernels_per_step(cfg: RunConfig) -> int:
     per_sub = 3 + KERNELS["fv3b_c_grid"] + KERNELS["fv3b_d_sw"] + 1 + 1
-    return cfg.n_split * per_sub + 1 + 1 + 2 + 2  # tracer halo, tracer_2d, face thickness + profiles, maps
+    return cfg.n_split * per_sub + 1 + 1 + 2 + 2 + 1  # tracer halo, tracer_2d, face thickness + profiles, maps, moist_pk

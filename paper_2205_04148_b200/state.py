@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .config import METRICS_2D, STATE_3D, RunConfig
+from .config import DIAG_3D, METRICS_2D, STATE_3D, RunConfig
 
 DX = 1.0e4
 
@@ -63,7 +63,7 @@ def initial_state(cfg: RunConfig) -> dict[str, np.ndarray]:
         gz[..., k] = gz[..., k + 1] + cfg.consts["rdgas"] * pt[..., k] * dm[..., k] / pm
     st["gz"] = gz
     st["pef"] = pem.copy()
-    for n in ("uc", "vc", "cx", "cy", "xfa", "yfa", "mfx", "mfy", "dp1"):
+    for n in ("uc", "vc", "cx", "cy", "xfa", "yfa", "mfx", "mfy", "dp1", *DIAG_3D):
         st[n] = np.zeros((I, J, L))
     for t in range(cfg.nq):
         st[f"q{t}"] = 1.0e-3 * (1.5 + np.sin(X + t)[..., None] * np.cos(Y - t)[..., None]) * \

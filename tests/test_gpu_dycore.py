@@ -10,8 +10,8 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-FIELDS = ["u", "v", "w", "delp", "pt", "gz", "pef", "q0", "q7", "q3_a4", "mfx", "cy"]
-INTERFACE = ("gz", "pef")
+FIELDS = ["u", "v", "w", "delp", "pt", "gz", "pef", "q0", "q7", "q3_a4", "mfx", "cy", "pe", "peln", "pk", "pkz", "cvm"]
+INTERFACE = ("gz", "pef", "pe", "peln", "pk")
 
 
 def _run(cfg, steps, graph, names=None):
