@@ -28,7 +28,8 @@ def _run(delp, qs, nk, sc):
         return t
 
     outs = [g.new3("cuda") for _ in range(5)]
-    fields = [g.abi(up(delp))] + [g.abi(up(q)) for q in qs] + [g.abi(o) for o in outs]
+    ins = [up(delp)] + [up(q) for q in qs]  # (kept alive until the launch has run)
+    fields = [g.abi(t) for t in ins] + [g.abi(o) for o in outs]
     _lib.call("fv3b_moist_pk", fields, sc, g.domain(nk=nk + 1), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     res = {}
