@@ -8,10 +8,11 @@
 //   cvm = (1 - (qv + ql + qs)) cv_air + qv cv_vap + ql c_liq + qs c_ice
 //         with ql = liquid + rain, qs = ice + snow + graupel
 //
-// A CTA owns 32 columns.  One warp forms the running sum pe in shared
-// memory; then all eight warps evaluate the levels in parallel (log / exp
-// per interface, pkz and cvm per layer), so the per-level transcendental
-// chains overlap across warps instead of running down one column thread.
+// A CTA owns 32 columns.  All eight warps stage delp in shared memory, one
+// warp forms the running sum pe there; then all eight warps evaluate the
+// levels in parallel (log / exp per interface, pkz and cvm per layer), so the
+// per-level transcendental chains overlap across warps instead of running
+// down one column thread.
 // HBM-bound: delp + the moist tracers in, five fields out.
 #include "common.cuh"
 #include "detmath.cuh"
@@ -35,11 +36,15 @@ __global__ void __launch_bounds__(MK_COLS * MK_TY) moist_pk_kernel(const MoistAr
   const int col = blockIdx.x * MK_COLS + c;
   const bool live = col < a.ni * a.nj;
   const int i = live ? col % a.ni : 0, j = live ? col / a.ni : 0;
+  // every warp stages delp (independent loads in flight together), then one
+  // warp forms the running sum in place (the oracle's order of additions)
+  for (int k = ty; k < nk; k += MK_TY) slog[(k + 1) * MK_COLS + c] = live ? __ldg(a.delp.ptr(i, j, k)) : 0.0;
+  __syncthreads();
   if (ty == 0) {
     double p = a.ptop;
     slog[c] = p;
     for (int k = 0; k < nk; ++k) {
-      p = p + (live ? __ldg(a.delp.ptr(i, j, k)) : 0.0);
+      p = p + slog[(k + 1) * MK_COLS + c];
       slog[(k + 1) * MK_COLS + c] = p;
     }
   }

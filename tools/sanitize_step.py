@@ -26,14 +26,15 @@ for name, dom, place in (("fv_tp_2d", (37, 21, 4), (False,) * 4), ("c_sw", (37, 
     run_b200(name, synthetic_inputs(name, dom, 1), dom, placement=place)
 torch.cuda.synchronize()
 print("programs done")
-# the peer-memory halo path: a 1 x 2 loopback decomposition, each rank on its
-# own stream, ordered by the device-side neighbour barriers
+# the peer-memory halo path (fv3b_halo_peer_rects): a 1 x 2 loopback
+# decomposition in stream order.  The device-side neighbour barriers
+# (fv3b_peer_barrier) cannot run under the sanitizer: it serialises kernels,
+# so a rank's spin never sees the other stream arrive (the spin is bounded
+# and reports a timeout instead of hanging).
 from paper_2205_04148_b200.parallel import LoopbackCluster
 
 blk = RunConfig(ni=20, nj=12, nk=6, n_split=1, dt_atmos=20.0)
-cl = LoopbackCluster([Dycore(blk, initial_state(blk)) for _ in range(2)], 1, 2, direct=True, flag_sync=True)
+cl = LoopbackCluster([Dycore(blk, initial_state(blk)) for _ in range(2)], 1, 2, direct=True)
 cl.step()
 torch.cuda.synchronize()
-for hal in cl.halos:
-    hal.sync.check()
 print("peer halos done")
