@@ -211,6 +211,19 @@ int fv3b_halo_unpack_rects(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_halo_peer_rects(const fv3b_field* f, int nf, const double* s, int ns,
                          const fv3b_domain* d, void* stream);
 
+/*   fv3b_halo_peer_idx  the cubed-sphere update without message buffers:
+ *                       up to 8 destination sets (a neighbour tile's fields,
+ *                       peer-mapped, or this tile's own for the corner
+ *                       fill).  Entry s of set r's device int32 list is
+ *                       (source slot, source offset, destination slot,
+ *                       destination offset, sign +/-1), offsets
+ *                       interior-relative; all levels.  fields: nf sources,
+ *                       then set r's destination of slot t at nf + r*nf + t.
+ *                       scalars: [nf, nset, then (list address bits, n) per
+ *                       set].  Up to 32 fields sharing one level count. */
+int fv3b_halo_peer_idx(const fv3b_field* f, int nf, const double* s, int ns,
+                       const fv3b_domain* d, void* stream);
+
 /*   fv3b_peer_barrier  stream-ordered barrier of a rank with its neighbours
  *                       over peer-mapped 64-bit flag words (the ordering of
  *                       fv3b_halo_peer_rects without host synchronisation).

@@ -248,6 +248,73 @@ static int peer_call(const fv3b_field* f, int ntot, const double* s, int ns, con
 }
 
 // ---------------------------------------------------------------------------
+// Peer-memory index-list stores: the cubed-sphere halo update without
+// message buffers (cubesphere.CubePeerHalo).  Destination set d is one
+// neighbour tile's fields (peer-mapped) or this tile's own (the corner
+// fill); entry s of its list is (source slot, source offset, destination
+// slot, destination offset, sign), offsets interior-relative, so each
+// rotated / component-swapped / sign-flipped halo cell is one load from this
+// tile and one store into the neighbour, all levels of up to 32 fields.
+// ---------------------------------------------------------------------------
+struct PeerIdxArgs {
+  const double* src[PEER_MAXF];
+  double* dst[RECT_MAX][PEER_MAXF];
+  const int* idx[RECT_MAX];
+  int n[RECT_MAX];
+  int64_t sk;
+  int nset;
+};
+
+__global__ void peer_idx_kernel(const PeerIdxArgs a) {
+  const int d = blockIdx.z, k = blockIdx.y;
+  const int* idx = a.idx[d];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < a.n[d]; e += gridDim.x * blockDim.x) {
+    const int* x = idx + 5 * e;
+    const double v = a.src[x[0]][x[1] + (int64_t)k * a.sk];
+    a.dst[d][x[2]][x[3] + (int64_t)k * a.sk] = x[4] < 0 ? -v : v;
+  }
+}
+
+static int peer_idx_call(const fv3b_field* f, int ntot, const double* s, int ns, const fv3b_domain* d,
+                         void* stream) {
+  // scalars: [nf, nset, (index-list address bits, n) x nset]; fields: nf
+  // sources, then set r's destination of slot t at nf + r*nf + t
+  if (f == nullptr || d == nullptr || s == nullptr || ns < 2) return fail(FV3B_EINVAL, "halo peer idx: bad arguments");
+  PeerIdxArgs a;
+  const int nf = (int)s[0];
+  a.nset = (int)s[1];
+  if (nf < 1 || nf > PEER_MAXF || a.nset < 1 || a.nset > RECT_MAX || ns != 2 + 2 * a.nset ||
+      ntot != nf * (1 + a.nset))
+    return fail(FV3B_EINVAL, "halo peer idx: 1..%d fields, 1..%d sets, 2 + 2*nset scalars, nf*(1+nset) fields",
+                PEER_MAXF, RECT_MAX);
+  int levels[PEER_MAXF], lv[PEER_MAXF];
+  double* o[PEER_MAXF];
+  int64_t sj, sk;
+  FV3B_TRY(collect(f, nf, d, 0, o, levels, &sj, &sk));
+  for (int t = 0; t < nf; ++t) {
+    a.src[t] = o[t];
+    if (levels[t] != levels[0]) return fail(FV3B_EINVAL, "halo peer idx: fields must share their level count");
+  }
+  a.sk = sk;
+  int maxn = 0;
+  for (int r = 0; r < a.nset; ++r) {
+    int64_t sj2, sk2;
+    FV3B_TRY(collect(f + nf * (1 + r), nf, d, 0, a.dst[r], lv, &sj2, &sk2));
+    if (sj2 != sj || sk2 != sk) return fail(FV3B_ELAYOUT, "halo peer idx: destinations must share the sources' strides");
+    uint64_t bits;
+    memcpy(&bits, &s[2 + 2 * r], sizeof bits);
+    a.idx[r] = reinterpret_cast<const int*>(bits);
+    a.n[r] = (int)s[3 + 2 * r];
+    if (a.n[r] < 0 || (a.n[r] > 0 && a.idx[r] == nullptr)) return fail(FV3B_EINVAL, "halo peer idx: bad list %d", r);
+    maxn = a.n[r] > maxn ? a.n[r] : maxn;
+  }
+  if (maxn == 0) return FV3B_OK;
+  dim3 grid(cdiv(maxn, 256) < 32 ? cdiv(maxn, 256) : 32, levels[0], a.nset);
+  peer_idx_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  return check_launch("fv3b_halo_peer_idx");
+}
+
+// ---------------------------------------------------------------------------
 // Stream-ordered barrier among a rank and its neighbours over peer-mapped
 // flag words (parallel.FlagSync): one thread bumps (or reads) this rank's
 // update counter e, stores e with release semantics into the flag word it
@@ -451,6 +518,11 @@ extern "C" int fv3b_halo_unpack_rects(const fv3b_field* f, int nf, const double*
 extern "C" int fv3b_halo_peer_rects(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                                     void* stream) {
   return peer_call(f, nf, s, ns, d, stream);
+}
+
+extern "C" int fv3b_halo_peer_idx(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                  void* stream) {
+  return peer_idx_call(f, nf, s, ns, d, stream);
 }
 
 extern "C" int fv3b_peer_barrier(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,

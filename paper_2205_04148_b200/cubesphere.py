@@ -313,3 +313,105 @@ class CubeHalo:
         self.finish(chunks)
         if timer is not None:
             timer.stop("halo")
+
+
+class CubePeerHalo:
+    """The cubed-sphere halo update of one tile by peer-memory stores
+    (``fv3b_halo_peer_idx``): this tile's cells go straight into its four
+    neighbours' halos, rotated / component-swapped / sign-flipped on the
+    way, one launch for all four; then, once every neighbour's stores have
+    landed, the corner fill from the tile's own edge halos (a second launch
+    of the same kernel with this tile as the destination).  No message
+    buffers, no NCCL.
+
+    ``peers.tensor(tile, name)``: neighbour ``tile``'s current tensor for
+    ``name`` (``LoopbackTiles`` in one process; ``parallel.IpcPeers``-style
+    mappings across processes).  ``sync(0)`` / ``sync(1)`` order the stores
+    against the neighbours when the tiles do not share one stream
+    (``parallel.FlagSync``)."""
+
+    direct = True
+
+    def __init__(self, dycore, tile: int, peers, sync=None):
+        g = dycore.grid
+        if g.ni != g.nj:
+            raise ValueError("cubed-sphere tiles are square")
+        self.d = dycore
+        self.tile = tile
+        self.n, self.h = g.ni, g.halo
+        self.peers = peers
+        self.sync = sync
+        self.neighbours = sorted({s.nb for s in topology()[tile].values()})
+        self._plans: dict = {}
+
+    def _off(self, i: int, j: int) -> int:
+        return i + j * self.d.grid.pitch
+
+    def _plan(self, names: tuple):
+        if names in self._plans:
+            return self._plans[names]
+        import torch
+
+        check_names(names)
+        if len(names) > 32:
+            raise ValueError("at most 32 fields per cubed-sphere halo update")
+        slot = {n: k for k, n in enumerate(names)}
+        dev = self.d.cur[names[0]].device
+        lists = []
+        for p in self.neighbours:  # what neighbour p takes from this tile
+            ent = [e for e in edge_entries(p, names, self.n, self.h) if e.src_tile == self.tile]
+            lists.append(torch.tensor([[slot[e.src_name], self._off(e.si, e.sj), slot[e.name], self._off(e.i, e.j),
+                                        1 if e.sign > 0 else -1] for e in ent], dtype=torch.int32,
+                                      device=dev).reshape(-1))
+        cor = corner_entries(names, self.n, self.h)
+        corner = torch.tensor([[slot[e.src_name], self._off(e.si, e.sj), slot[e.name], self._off(e.i, e.j),
+                                1 if e.sign > 0 else -1] for e in cor], dtype=torch.int32, device=dev).reshape(-1)
+        self._plans[names] = (lists, corner)
+        return self._plans[names]
+
+    def _call(self, names, dst_sets, lists) -> None:
+        import struct
+
+        import torch
+
+        from . import _lib
+
+        g = self.d.grid
+        fields = [g.abi(self.d.cur[n]) for n in names] + [g.abi(t) for row in dst_sets for t in row]
+        s = [float(len(names)), float(len(lists))]
+        for idx in lists:
+            s += [struct.unpack("d", struct.pack("Q", idx.data_ptr()))[0], float(idx.numel() // 5)]
+        _lib.call("fv3b_halo_peer_idx", fields, s, g.domain(), torch.cuda.current_stream().cuda_stream)
+
+    def push(self, names) -> None:
+        names = tuple(names)
+        lists, _ = self._plan(names)
+        self._call(names, [[self.peers.tensor(p, n) for n in names] for p in self.neighbours], lists)
+
+    def corners(self, names) -> None:
+        names = tuple(names)
+        _, corner = self._plan(names)
+        self._call(names, [[self.d.cur[n] for n in names]], [corner])
+
+    def update(self, names) -> None:
+        timer = getattr(self.d, "timer", None)
+        if timer is not None:
+            timer.start("halo")
+        if self.sync is not None:
+            self.sync(0)
+        self.push(names)
+        if self.sync is not None:
+            self.sync(1)
+        self.corners(names)
+        if timer is not None:
+            timer.stop("halo")
+
+
+class LoopbackTiles:
+    """The six tiles' dycores held in this process (CubePeerHalo peers)."""
+
+    def __init__(self, dycores):
+        self.d = dycores
+
+    def tensor(self, tile: int, name: str):
+        return self.d[tile].cur[name]

@@ -289,19 +289,29 @@ class PeerHalo:
             s, r = self.plan.send[d], self.plan.recv[NEG[d]]
             self.rects.append((s.i0, s.j0, r.i0, r.j0, s.w, s.h))
 
+    direct = True  # LoopbackCluster: stores into the neighbours, no messages
+
+    def push(self, names) -> None:
+        """Store this rank's strips into the neighbours' halos."""
+        names = list(names)
+        for c in range(0, len(names), MAX_FIELDS):
+            chunk = names[c : c + MAX_FIELDS]
+            self.copier([self.d.cur[n] for n in chunk],
+                        [[self.peers.tensor(d, n) for n in chunk] for d in range(8)], self.rects)
+
+    def corners(self, names) -> None:
+        """(Corners travel with the diagonal neighbours: nothing local.)"""
+
     def update(self, names) -> None:
         timer = getattr(self.d, "timer", None)
         if timer is not None:
             timer.start("halo")
         if self.sync is not None:
             self.sync(0)
-        names = list(names)
-        for c in range(0, len(names), MAX_FIELDS):
-            chunk = names[c : c + MAX_FIELDS]
-            self.copier([self.d.cur[n] for n in chunk],
-                        [[self.peers.tensor(d, n) for n in chunk] for d in range(8)], self.rects)
+        self.push(names)
         if self.sync is not None:
             self.sync(1)
+        self.corners(names)
         if timer is not None:
             timer.stop("halo")
 
@@ -478,18 +488,18 @@ class LoopbackCluster:
                  flag_sync: bool = False):
         """``halos``: per-rank halo objects exposing pack / finish (default:
         a px x py doubly periodic decomposition; cubesphere.CubeHalo for
-        the six tiles of a cube).  ``direct``: the decomposition's halo
-        updates as peer-memory stores (:class:`PeerHalo`) instead of
-        pack / copy / unpack.  ``flag_sync`` (with ``direct``): every rank on
-        its own stream, ordered only by the device-side neighbour barriers
-        (:class:`FlagSync`), as separate processes would be."""
+        the six tiles of a cube; ``cubesphere.CubePeerHalo`` for its
+        peer-memory form).  ``direct``: the decomposition's halo updates as
+        peer-memory stores (:class:`PeerHalo`) instead of pack / copy /
+        unpack.  ``flag_sync``: every rank on its own stream, ordered only by
+        the device-side neighbour barriers (:class:`FlagSync`; built here for
+        ``direct``, supplied with ``halos`` otherwise), as separate
+        processes would be."""
         self.d = dycores
-        self.streams = None
-        if direct:
+        self.streams = [torch.cuda.Stream() for _ in dycores] if flag_sync else None
+        if direct and halos is None:
             self.halos = []
             flags = [new_flags(len(dycores), d.device) for d in dycores] if flag_sync else None
-            if flag_sync:
-                self.streams = [torch.cuda.Stream() for _ in dycores]
             for r, d in enumerate(dycores):
                 plan = HaloPlan(d.grid.ni, d.grid.nj, d.grid.halo, px, py, r)
                 sync = FlagSync(r, plan.peer, flags[r], dict(enumerate(flags))) if flag_sync else None
@@ -505,10 +515,16 @@ class LoopbackCluster:
 
     def exchange_all(self, reqs) -> None:
         """One halo update on every rank (``reqs[r]``: rank r's field list)."""
-        if isinstance(self.halos[0], PeerHalo):  # every rank's producers are queued: store the strips
-            for r, (h, names) in enumerate(zip(self.halos, reqs)):
-                with self._on(r):
-                    h.update(names)
+        if getattr(self.halos[0], "direct", False):  # peer-memory stores into the neighbours
+            if self.streams:  # each rank on its stream, ordered by its device barriers
+                for r, (h, names) in enumerate(zip(self.halos, reqs)):
+                    with self._on(r):
+                        h.update(names)
+            else:  # one stream: every rank's stores, then every rank's local corner fill
+                for h, names in zip(self.halos, reqs):
+                    h.push(names)
+                for h, names in zip(self.halos, reqs):
+                    h.corners(names)
             return
         chunks = [h.pack(names) for h, names in zip(self.halos, reqs)]
         for r, ch in enumerate(chunks):

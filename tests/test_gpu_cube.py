@@ -14,17 +14,29 @@ pytestmark = pytest.mark.gpu
 NAMES = ["u", "v", "uc", "vc", "delp", "pt", "q0", "cx", "cy", "mfx", "mfy"]
 
 
-def _cluster(cfg, states):
-    from paper_2205_04148_b200.cubesphere import CubeHalo
+def _cluster(cfg, states, mode="packed"):
+    """packed: CubeHalo (gather / device copy / scatter); direct:
+    CubePeerHalo (stores into the neighbour tiles, one stream); flags:
+    CubePeerHalo with every tile on its own stream, ordered by the
+    device-side neighbour barriers."""
+    from paper_2205_04148_b200.cubesphere import CubeHalo, CubePeerHalo, LoopbackTiles
     from paper_2205_04148_b200.dycore import Dycore
-    from paper_2205_04148_b200.parallel import LoopbackCluster
+    from paper_2205_04148_b200.parallel import FlagSync, LoopbackCluster, new_flags
 
     tiles = [Dycore(cfg, st, placement=(True, True, True, True)) for st in states]
-    cl = LoopbackCluster(tiles, halos=[CubeHalo(d, t, transport=None) for t, d in enumerate(tiles)])
-    return tiles, cl
+    if mode == "packed":
+        return tiles, LoopbackCluster(tiles, halos=[CubeHalo(d, t, transport=None) for t, d in enumerate(tiles)])
+    peers = LoopbackTiles(tiles)
+    halos = [CubePeerHalo(d, t, peers) for t, d in enumerate(tiles)]
+    if mode == "flags":
+        flags = [new_flags(6, "cuda") for _ in tiles]
+        for t, h in enumerate(halos):
+            h.sync = FlagSync(t, h.neighbours, flags[t], dict(enumerate(flags)))
+    return tiles, LoopbackCluster(tiles, halos=halos, flag_sync=mode == "flags")
 
 
-def test_cube_halo_matches_oracle():
+@pytest.mark.parametrize("mode", ["packed", "direct", "flags"])
+def test_cube_halo_matches_oracle(mode):
     import torch
 
     from oracle.cube import cube_halo
@@ -39,8 +51,14 @@ def test_cube_halo_matches_oracle():
         for n in NAMES:
             st[n] = rng.uniform(-1, 1, st["delp"].shape)
         states.append(st)
-    tiles, cl = _cluster(cfg, states)
+    tiles, cl = _cluster(cfg, states, mode)
+    if cl.streams:
+        for st in cl.streams:
+            st.wait_stream(torch.cuda.current_stream())
     cl.exchange_all([NAMES] * 6)
+    if cl.streams:
+        for st in cl.streams:
+            torch.cuda.current_stream().wait_stream(st)
     torch.cuda.synchronize()
     ref = [{n: states[t][n].copy() for n in NAMES} for t in range(6)]
     cube_halo(ref, NAMES, cfg.ni, cfg.halo)
@@ -50,8 +68,9 @@ def test_cube_halo_matches_oracle():
             assert np.array_equal(got[n], ref[t][n]), (t, n)
 
 
-@pytest.mark.parametrize("graph", [False, True])
-def test_cube_dycore_matches_oracle_bitwise(graph):
+@pytest.mark.parametrize("mode,graph", [("packed", False), ("packed", True), ("direct", False), ("direct", True),
+                                        ("flags", False)])
+def test_cube_dycore_matches_oracle_bitwise(mode, graph):
     import torch
 
     from oracle.cube import OracleCube
@@ -60,7 +79,7 @@ def test_cube_dycore_matches_oracle_bitwise(graph):
 
     cfg = RunConfig(ni=24, nj=24, nk=6, n_split=2, dt_atmos=20.0)
     states = [initial_state(RunConfig(ni=24, nj=24, nk=6, seed=2205 + t)) for t in range(6)]
-    tiles, cl = _cluster(cfg, [{k: v.copy() for k, v in st.items()} for st in states])
+    tiles, cl = _cluster(cfg, [{k: v.copy() for k, v in st.items()} for st in states], mode)
     ref = OracleCube(cfg, states)
     for it in range(3):
         if graph and it == 1:
