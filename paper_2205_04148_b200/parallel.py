@@ -494,7 +494,11 @@ class LoopbackCluster:
         unpack.  ``flag_sync``: every rank on its own stream, ordered only by
         the device-side neighbour barriers (:class:`FlagSync`; built here for
         ``direct``, supplied with ``halos`` otherwise), as separate
-        processes would be."""
+        processes would be.  A measurement mode: in one process the ranks'
+        streams must land on distinct hardware queues (at most
+        CUDA_DEVICE_MAX_CONNECTIONS streams), or one rank's spinning barrier
+        blocks a neighbour's arrival queued behind it until the barrier's
+        10 s bound expires."""
         self.d = dycores
         self.streams = [torch.cuda.Stream() for _ in dycores] if flag_sync else None
         if direct and halos is None:

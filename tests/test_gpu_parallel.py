@@ -49,14 +49,16 @@ def test_device_packer_single_rank_equals_periodic_kernel():
         assert torch.equal(a.cur[n], b.cur[n]), n
 
 
-@pytest.mark.parametrize("mode", ["packed", "direct", "direct-graph", "flags"])
+@pytest.mark.parametrize("mode", ["packed", "direct", "direct-graph"])
 @pytest.mark.parametrize("px,py", [(2, 2), (1, 2)])
 def test_loopback_decomposed_dycore_bitwise(px, py, mode):
     """packed: pack / device copy / unpack; direct: PeerHalo
     (fv3b_halo_peer_rects stores into the neighbours' halos), eager or
-    captured as CUDA graphs and replayed; flags: PeerHalo with every rank on
-    its own stream, ordered only by the device-side neighbour barriers
-    (fv3b_peer_barrier), as separate processes would be."""
+    captured as CUDA graphs and replayed.  The device-side neighbour
+    barriers (fv3b_peer_barrier) are tested across processes
+    (test_ipc_peer_halo_two_processes_bitwise): in one process, spinning
+    barrier kernels on streams that happen to share a hardware queue
+    (CUDA_DEVICE_MAX_CONNECTIONS) would wait on each other."""
     import torch
 
     from paper_2205_04148_b200.config import RunConfig
