@@ -374,7 +374,11 @@ class IpcPeers:
     travel once, at construction, through ``all_gather_object`` on
     ``group`` (any backend)."""
 
-    def __init__(self, dycore, plan: HaloPlan, group=None, flags: torch.Tensor | None = None):
+    def __init__(self, dycore, plan: HaloPlan | None, group=None, flags: torch.Tensor | None = None,
+                 neighbours=None, rank: int | None = None):
+        """``plan``: a px x py decomposition's HaloPlan (neighbours and rank
+        from it); otherwise ``neighbours`` (ranks) and ``rank`` (e.g. the
+        cubed sphere's four adjacent tiles, :meth:`tiles`)."""
         import pickle
         from multiprocessing.reduction import ForkingPickler
 
@@ -383,6 +387,8 @@ class IpcPeers:
 
         self.d = dycore
         self.plan = plan
+        self.rank = plan.rank if plan is not None else rank
+        nbrs = set(plan.peer) if plan is not None else set(neighbours)
         mine = self._buffers(dycore)
         if flags is not None:  # the FlagSync array travels as the last buffer
             mine.append(flags)
@@ -392,15 +398,30 @@ class IpcPeers:
         gathered: list = [None] * dist.get_world_size(group)
         dist.all_gather_object(gathered, shared, group=group)
         self._peer = {}
-        for p in set(plan.peer):
-            self._peer[p] = mine if p == plan.rank else [pickle.loads(b) for b in gathered[p]]
+        for p in nbrs:
+            self._peer[p] = mine if p == self.rank else [pickle.loads(b) for b in gathered[p]]
         self.flags = flags
+        self.neighbours = sorted(nbrs)
 
     def flag_sync(self) -> FlagSync:
         """The device-side barrier over the shared flag arrays."""
         if self.flags is None:
             raise ValueError("IpcPeers was built without a flag array")
-        return FlagSync(self.plan.rank, self.plan.peer, self.flags, {p: b[-1] for p, b in self._peer.items()})
+        return FlagSync(self.rank, self.neighbours, self.flags, {p: b[-1] for p, b in self._peer.items()})
+
+    def rank_tensor(self, p: int, name: str) -> torch.Tensor:
+        """Rank p's tensor that holds ``name`` in the shared buffer assignment."""
+        return self._peer[p][self._index[self.d.cur[name].data_ptr()]]
+
+    def tiles(self):
+        """The ``tensor(tile, name)`` view CubePeerHalo takes."""
+        ipc = self
+
+        class _Tiles:
+            def tensor(self, tile: int, name: str) -> torch.Tensor:
+                return ipc.rank_tensor(tile, name)
+
+        return _Tiles()
 
     @staticmethod
     def _buffers(dycore) -> list:
@@ -414,7 +435,7 @@ class IpcPeers:
         return out
 
     def tensor(self, direction: int, name: str) -> torch.Tensor:
-        return self._peer[self.plan.peer[direction]][self._index[self.d.cur[name].data_ptr()]]
+        return self.rank_tensor(self.plan.peer[direction], name)
 
 
 def ipc_sync(group=None, device: bool = True):

@@ -98,3 +98,73 @@ def test_cube_dycore_matches_oracle_bitwise(mode, graph):
             a, b = got[n][h:-h, h:-h, :top], ref.tiles[t].state[n][h:-h, h:-h, :top]
             assert np.isfinite(b).all(), (t, n)
             assert np.array_equal(a, b), (t, n, float(np.max(np.abs(a - b))))
+
+
+def _cube_worker(tile, port, q):
+    """One tile of the cube per process (cuda:0 for all); the neighbours'
+    buffers are CUDA-IPC mappings, stores ordered by host barriers."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.cubesphere import CubePeerHalo, topology
+    from paper_2205_04148_b200.dycore import Dycore
+    from paper_2205_04148_b200.parallel import IpcPeers, ipc_sync
+    from paper_2205_04148_b200.state import initial_state
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=tile, world_size=6)
+    try:
+        torch.cuda.set_device(0)
+        cfg = RunConfig(ni=16, nj=16, nk=5, n_split=1, dt_atmos=20.0)
+        d = Dycore(cfg, initial_state(RunConfig(ni=16, nj=16, nk=5, seed=2205 + tile)),
+                   placement=(True, True, True, True))
+        nbrs = sorted({s.nb for s in topology()[tile].values()})
+        ipc = IpcPeers(d, None, neighbours=nbrs, rank=tile)
+        d.halo = CubePeerHalo(d, tile, ipc.tiles(), sync=ipc_sync())
+        dist.barrier()
+        d.step()
+        torch.cuda.synchronize()
+        names = ["u", "v", "w", "delp", "pt", "gz", "q0", "mfx", "cy"]
+        h = cfg.halo
+        got = d.download(names)
+        q.put((tile, {n: got[n][h:-h, h:-h] for n in names}))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_cube_ipc_six_processes_bitwise():
+    """The six tiles as six processes (one per GPU on a node; here all on
+    cuda:0) exchanging rotated halos by CUDA-IPC peer stores: one FULL_TILE
+    step bitwise the oracle cube."""
+    import socket
+
+    import torch
+
+    from oracle.cube import OracleCube
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.state import initial_state
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_cube_worker, args=(t, port, q)) for t in range(6)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    cfg = RunConfig(ni=16, nj=16, nk=5, n_split=1, dt_atmos=20.0)
+    ref = OracleCube(cfg, [initial_state(RunConfig(ni=16, nj=16, nk=5, seed=2205 + t)) for t in range(6)])
+    ref.step()
+    h = cfg.halo
+    for t in range(6):
+        for n, got in res[t].items():
+            top = cfg.nk + 1 if n == "gz" else cfg.nk
+            want = ref.tiles[t].state[n][h:-h, h:-h, :top]
+            assert np.array_equal(got[..., :top], want), (t, n)
