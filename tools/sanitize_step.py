@@ -38,3 +38,13 @@ cl = LoopbackCluster([Dycore(blk, initial_state(blk)) for _ in range(2)], 1, 2, 
 cl.step()
 torch.cuda.synchronize()
 print("peer halos done")
+# the cubed sphere by peer stores (fv3b_halo_peer_idx): six FULL_TILE tiles in stream order
+from paper_2205_04148_b200.cubesphere import CubePeerHalo, LoopbackTiles
+
+cub = RunConfig(ni=12, nj=12, nk=4, n_split=1, dt_atmos=20.0)
+tiles = [Dycore(cub, initial_state(RunConfig(ni=12, nj=12, nk=4, seed=7 + t)), placement=(True,) * 4)
+         for t in range(6)]
+peers = LoopbackTiles(tiles)
+LoopbackCluster(tiles, halos=[CubePeerHalo(d, t, peers) for t, d in enumerate(tiles)]).step()
+torch.cuda.synchronize()
+print("cube peer halos done")
