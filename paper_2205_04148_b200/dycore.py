@@ -92,16 +92,47 @@ class Dycore:
     # -- host I/O through pinned buffers (the end-to-end path) ---------------
 
     def prognostic(self) -> list[str]:
-        """Fields a timestep evolves (the state a host caller owns)."""
-        return ["u", "v", "w", "delp", "pt", "gz"] + self.cfg.tracer_names()
+        """Fields a timestep evolves (the state a host caller owns).  The
+        order is step_host's transfer order: gz (downloaded early), the other
+        dynamics fields, then the tracers (uploaded during the substeps)."""
+        return ["gz", "u", "v", "w", "delp", "pt"] + self.cfg.tracer_names()
 
     def host_buffers(self, names=None) -> dict[str, torch.Tensor]:
         """Pinned host tensors in the reference array convention (I, J, K,
         halo-inclusive, C order) for ``names`` (default: the prognostic
-        state)."""
+        state), as consecutive views of one pinned block, so step_host moves
+        each run of fields it transfers together as one copy."""
+        names = list(names or self.prognostic())
+        block = torch.zeros((len(names),) + self._host_shape(), dtype=torch.float64).pin_memory()
+        return {n: block[t] for t, n in enumerate(names)}
+
+    def _host_shape(self) -> tuple[int, int, int]:
         h, c = self.cfg.halo, self.cfg
-        shape = (c.ni + 2 * h, c.nj + 2 * h, c.nk + 1)
-        return {n: torch.empty(shape, dtype=torch.float64).pin_memory() for n in (names or self.prognostic())}
+        return (c.ni + 2 * h, c.nj + 2 * h, c.nk + 1)
+
+    @staticmethod
+    def _runs(names, a: dict, b: dict) -> list[tuple[torch.Tensor, torch.Tensor]]:
+        """(a-view, b-view) pairs covering ``names`` in order, consecutive
+        fields merged into one flat view wherever both sides are adjacent in
+        one storage (one DMA instead of one per field)."""
+        out = []
+        for n in names:
+            x, y = a[n], b[n]
+            if out:
+                px, py, pn = out[-1]
+                if (x.untyped_storage().data_ptr() == px.untyped_storage().data_ptr()
+                        and y.untyped_storage().data_ptr() == py.untyped_storage().data_ptr()
+                        and x.is_contiguous() and y.is_contiguous()
+                        and x.storage_offset() == px.storage_offset() + px.numel()
+                        and y.storage_offset() == py.storage_offset() + py.numel()):
+                    out[-1] = (torch.empty(0, dtype=x.dtype, device=x.device).set_(
+                                   x.untyped_storage(), px.storage_offset(), (px.numel() + x.numel(),)),
+                               torch.empty(0, dtype=y.dtype, device=y.device).set_(
+                                   y.untyped_storage(), py.storage_offset(), (py.numel() + y.numel(),)),
+                               pn + [n])
+                    continue
+            out.append((x.reshape(-1) if x.is_contiguous() else x, y.reshape(-1) if y.is_contiguous() else y, [n]))
+        return [(x, y) for x, y, _ in out]
 
     def _staging(self) -> torch.Tensor:
         if getattr(self, "_stage", None) is None:
@@ -151,17 +182,20 @@ class Dycore:
         (three-deep ring: a call's uploads never wait for the compute of the
         call before last), output stage o (two-deep), and the slots' free events."""
         if getattr(self, "_io", None) is None or set(self._io[0][0]) != set(names):
-            h, c = self.cfg.halo, self.cfg
-            shape = (c.ni + 2 * h, c.nj + 2 * h, c.nk + 1)
-            mk = lambda: {n: torch.empty(shape, dtype=torch.float64, device=self.device) for n in names}
+            shape = self._host_shape()
+
+            def mk():  # one device block per stage, fields in transfer order (see _runs)
+                block = torch.empty((len(names),) + shape, dtype=torch.float64, device=self.device)
+                return {n: block[t] for t, n in enumerate(names)}
+
             self._io = ([mk() for _ in range(3)], [mk() for _ in range(2)])
             self._io_free = ([None] * 3, [None] * 2)  # inputs consumed / outputs downloaded
         return self._io
 
     def _io_streams(self) -> tuple[torch.cuda.Stream, torch.cuda.Stream]:
         if getattr(self, "_up", None) is None:
-            self._up, self._down = torch.cuda.Stream(), torch.cuda.Stream()
-            self._io_calls, self._prev_out, self._prev_done = 0, set(), None
+            self._up, self._down, self._xs = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+            self._io_calls, self._prev_out, self._prev_done, self._prev_x = 0, set(), None, None
         return self._up, self._down
 
     def step_host(self, h_in: dict[str, torch.Tensor], h_out: dict[str, torch.Tensor]) -> torch.cuda.Event:
@@ -175,13 +209,22 @@ class Dycore:
         tracers' uploads run during the acoustic substeps (first needed by
         tracer_2d); gz is final after the substeps and downloads during
         tracer advection and remapping; everything the remapping rewrites
-        (tracers, delp, pt, w, u, v) downloads at the end of the step.  Device staging is a ring (three input stages, two output
-        stages), so successive calls pipeline: the next call's uploads
-        overlap this call's compute, this call's downloads the next call's
-        compute.  A call whose inputs are the previous call's outputs (a
-        chained integration) waits for those downloads before uploading."""
+        (tracers, delp, pt, w, u, v) downloads at the end of the step.
+        Device staging is a ring (three input stages, two output stages), so
+        successive calls pipeline: the next call's uploads overlap this
+        call's compute, this call's downloads the next call's compute.  A
+        call whose inputs are the previous call's outputs (a chained
+        integration) waits for those downloads before uploading.
+
+        The layout transposes off the compute path run on a third stream:
+        the tracers' (during the substeps), and every output's.  Inputs land
+        in the other buffer of each ping-pong pair (cur / alt swapped first),
+        so the previous call's output transposes, still reading the old
+        buffers, overlap this call's start; the first program that writes a
+        ping-pong buffer (d_sw) waits for them."""
         comp = torch.cuda.current_stream()
         up, down = self._io_streams()
+        xs = self._xs
         tracers = set(self.cfg.tracer_names())
         trc = [n for n in h_in if n in tracers]           # uploaded during the substeps
         dyn = [n for n in h_in if n not in tracers]       # uploaded before the step
@@ -197,43 +240,63 @@ class Dycore:
         if self._prev_done is not None and self._prev_out & {t.data_ptr() for t in h_in.values()}:
             up.wait_event(self._prev_done)
         with torch.cuda.stream(up):
-            for n in dyn:
-                sin[n].copy_(h_in[n], non_blocking=True)
+            for dst, src in self._runs(dyn, sin, h_in):
+                dst.copy_(src, non_blocking=True)
             e_dyn = up.record_event()
-            for n in trc:
-                sin[n].copy_(h_in[n], non_blocking=True)
+            for dst, src in self._runs(trc, sin, h_in):
+                dst.copy_(src, non_blocking=True)
             e_trc = up.record_event()
+        # inputs into the other buffer of each pair (the previous outputs stay
+        # readable); a field without a second buffer waits for the readers
+        pairs = all(n in self.alt for n in h_in)
+        if pairs:
+            self.swap(*h_in)
+        elif self._prev_x is not None:
+            comp.wait_event(self._prev_x)
         comp.wait_event(e_dyn)
         for n in dyn:
             self._transpose(sin[n], self._window(self.cur[n]))
+        start = comp.record_event()
+        xs.wait_event(start)  # (the tracers' buffers are this call's from here on)
+        xs.wait_event(e_trc)
+        with torch.cuda.stream(xs):
+            for n in trc:
+                self._transpose(sin[n], self._window(self.cur[n]))
+        e_xtrc = xs.record_event()
         if out_free[so] is not None:  # downloaded two calls ago
-            comp.wait_event(out_free[so])
+            xs.wait_event(out_free[so])
 
-        def out(names):  # device transpose on the compute stream, download on the download stream
+        def out(names):  # device transpose on the transpose stream, download on the download stream
             if not names:
                 return
-            for n in names:
-                self._transpose(self._window(self.cur[n]), sout[n])
-            e_out = comp.record_event()
+            xs.wait_event(comp.record_event())
+            with torch.cuda.stream(xs):
+                for n in names:
+                    self._transpose(self._window(self.cur[n]), sout[n])
+            e_out = xs.record_event()
             down.wait_event(e_out)
             with torch.cuda.stream(down):
-                for n in names:
-                    h_out[n].copy_(sout[n], non_blocking=True)
+                for dst, src in self._runs(names, h_out, sout):
+                    dst.copy_(src, non_blocking=True)
+            return e_out
 
-        tracer_point, consumed = set(self.cfg.tracer_names()), False
+        tracer_point, consumed, point = set(self.cfg.tracer_names()), False, 0
         for names in self.phases():
+            point += 1
+            if point == 2 and self._prev_x is not None:  # before the first ping-pong write (d_sw)
+                comp.wait_event(self._prev_x)
             if tracer_point & set(names):  # the tracer halo point: substeps done
-                comp.wait_event(e_trc)
-                for n in trc:
-                    self._transpose(sin[n], self._window(self.cur[n]))
+                comp.wait_event(e_xtrc)
                 in_free[si], consumed = comp.record_event(), True
                 out(early)
             self.halo.update(names)
         if not consumed:  # no tracers in the run
-            comp.wait_event(e_trc)
+            comp.wait_event(e_xtrc)
             in_free[si] = comp.record_event()
             out(early)
-        out(late)
+        e_late = out(late)
+        # the next call may not overwrite what the output transposes read
+        self._prev_x = e_late if e_late is not None else xs.record_event()
         done = down.record_event()
         out_free[so] = done
         self._prev_done, self._prev_out = done, {t.data_ptr() for t in h_out.values()}
