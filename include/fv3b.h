@@ -263,6 +263,12 @@ int fv3b_halo_scatter(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_memcpy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch,
                   int64_t width, int64_t height, void* stream);
 
+/*   fv3b_enable_peer_access  multi-GPU helper: kernels on the current
+ *                  device may access device `peer`'s memory (NVLink P2P;
+ *                  parallel.IpcPeers calls it for every neighbour on another
+ *                  GPU).  Already enabled is not an error. */
+int fv3b_enable_peer_access(int peer);
+
 /*   fv3b_transpose  state layout conversion for host I/O: copy the d->ni x
  *                   d->nj x d->nk region at f[0].data to f[1].data where one
  *                   field has unit K stride (the reference's numpy (I, J, K)

@@ -104,3 +104,13 @@ def memcpy2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: i
     rc = fn(dst, dpitch, src, spitch, width, height, stream)
     if rc != 0:
         raise Fv3bError("fv3b_memcpy2d", rc, lib().fv3b_last_error().decode())
+
+
+def enable_peer_access(peer: int) -> None:
+    """``fv3b_enable_peer_access`` for the current device."""
+    fn = lib().fv3b_enable_peer_access
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.c_int]
+    rc = fn(peer)
+    if rc != 0:
+        raise Fv3bError("fv3b_enable_peer_access", rc, lib().fv3b_last_error().decode())

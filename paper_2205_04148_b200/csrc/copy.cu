@@ -196,3 +196,20 @@ extern "C" int fv3b_memcpy2d(void* dst, int64_t dpitch, const void* src, int64_t
   if (e != cudaSuccess) return fv3b::fail(FV3B_ELAUNCH, "fv3b_memcpy2d: %s", cudaGetErrorString(e));
   return FV3B_OK;
 }
+
+// Multi-GPU helper of parallel.IpcPeers: let kernels on the current device
+// load / store the memory of `peer` (NVLink P2P).  Already enabled is fine.
+extern "C" int fv3b_enable_peer_access(int peer) {
+  int dev = -1, ok = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fv3b::fail(FV3B_ELAUNCH, "fv3b_enable_peer_access: no device");
+  if (peer == dev) return FV3B_OK;
+  if (cudaDeviceCanAccessPeer(&ok, dev, peer) != cudaSuccess || !ok)
+    return fv3b::fail(FV3B_ELAUNCH, "fv3b_enable_peer_access: device %d cannot access device %d", dev, peer);
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // (not sticky: clear it)
+    return FV3B_OK;
+  }
+  if (e != cudaSuccess) return fv3b::fail(FV3B_ELAUNCH, "fv3b_enable_peer_access: %s", cudaGetErrorString(e));
+  return FV3B_OK;
+}

@@ -400,6 +400,15 @@ class IpcPeers:
         self._peer = {}
         for p in nbrs:
             self._peer[p] = mine if p == self.rank else [pickle.loads(b) for b in gathered[p]]
+        # neighbours on other GPUs: this device's kernels store into their memory
+        if mine and mine[0].is_cuda:
+            from . import _lib
+
+            here = mine[0].device.index
+            for p, bufs in self._peer.items():
+                if bufs and bufs[0].device.index != here:
+                    with torch.cuda.device(here):
+                        _lib.enable_peer_access(bufs[0].device.index)
         self.flags = flags
         self.neighbours = sorted(nbrs)
 
