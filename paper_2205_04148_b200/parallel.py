@@ -541,6 +541,8 @@ class LoopbackCluster:
         else:
             self.halos = halos or [DecomposedHalo(d, px, py, r, transport=self, packer=None)
                                    for r, d in enumerate(dycores)]
+        if flag_sync and not all(getattr(h, "direct", False) and h.sync is not None for h in self.halos):
+            raise ValueError("flag_sync needs peer-store halos with device barriers (direct=True, or such halos)")
         for d, h in zip(dycores, self.halos):
             d.halo = h
 
