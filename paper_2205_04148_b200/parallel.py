@@ -530,7 +530,7 @@ class LoopbackCluster:
         blocks a neighbour's arrival queued behind it until the barrier's
         10 s bound expires."""
         self.d = dycores
-        self.streams = [torch.cuda.Stream() for _ in dycores] if flag_sync else None
+        self.streams = None
         if direct and halos is None:
             self.halos = []
             flags = [new_flags(len(dycores), d.device) for d in dycores] if flag_sync else None
@@ -543,6 +543,8 @@ class LoopbackCluster:
                                    for r, d in enumerate(dycores)]
         if flag_sync and not all(getattr(h, "direct", False) and h.sync is not None for h in self.halos):
             raise ValueError("flag_sync needs peer-store halos with device barriers (direct=True, or such halos)")
+        if flag_sync:
+            self.streams = [torch.cuda.Stream() for _ in dycores]
         for d, h in zip(dycores, self.halos):
             d.halo = h
 
