@@ -159,3 +159,33 @@ def test_step_host_overlapped_io_matches_step():
     for n in hin:
         top = cfg.nk + 1 if n in INTERFACE else cfg.nk
         assert torch.equal(oa[n][h:-h, h:-h, :top], ob[n][h:-h, h:-h, :top]), n
+
+
+def test_step_host_unpaired_field_matches_step():
+    """step_host with a field that has no second (ping-pong) buffer: inputs
+    cannot be swapped in, so the call waits for the previous call's output
+    transposes before loading (the other branch of step_host)."""
+    import torch
+
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.dycore import Dycore
+    from paper_2205_04148_b200.state import initial_state
+
+    cfg = RunConfig(ni=32, nj=24, nk=10, n_split=2, dt_atmos=45.0)
+    st = initial_state(cfg)
+    a, b = Dycore(cfg, st), Dycore(cfg, st)
+    names = a.prognostic() + ["pef"]
+    assert "pef" not in a.alt
+    hin, oa, ob = a.host_buffers(names), a.host_buffers(names), b.host_buffers(names)
+    for n, t in hin.items():
+        t.copy_(torch.from_numpy(st[n]))
+    for _ in range(3):
+        a.step_host(hin, oa)
+        b.load_host(hin)
+        b.step()
+        b.store_host(ob)
+    torch.cuda.synchronize()
+    h = cfg.halo
+    for n in names:
+        top = cfg.nk + 1 if n in INTERFACE else cfg.nk
+        assert torch.equal(oa[n][h:-h, h:-h, :top], ob[n][h:-h, h:-h, :top]), n
