@@ -14,6 +14,9 @@
 namespace fv3b {
 
 constexpr int HALO_MAXF = 32;
+#ifndef FV3B_HALO_KU  // levels per thread of the periodic fill (tools/build_variant.py sweeps)
+#define FV3B_HALO_KU 8
+#endif
 
 struct HaloArgs {
   double* o[HALO_MAXF];  // interior origins
@@ -28,7 +31,7 @@ struct HaloArgs {
 __global__ void halo_periodic_kernel(const HaloArgs a) {
   // each thread copies one ring cell on HALO_KU consecutive levels: the
   // independent loads are issued together (the copy is latency-bound)
-  constexpr int HALO_KU = 8;
+  constexpr int HALO_KU = FV3B_HALO_KU;
   const int W = a.ni + 2 * a.h, h = a.h;
   const int f = blockIdx.z, kb = blockIdx.y * HALO_KU;
   const int nl = min(HALO_KU, a.levels[f] - kb);
@@ -461,7 +464,7 @@ extern "C" int fv3b_halo_periodic(const fv3b_field* f, int nf, const double* s, 
   int maxl = 1;
   for (int t = 0; t < nf; ++t) maxl = a.levels[t] > maxl ? a.levels[t] : maxl;
   const int ring = 2 * (d->ni + 2 * a.h) * a.h + 2 * a.h * d->nj;
-  dim3 grid(cdiv(ring, 256) < 16 ? cdiv(ring, 256) : 16, cdiv(maxl, 8), nf);
+  dim3 grid(cdiv(ring, 256) < 16 ? cdiv(ring, 256) : 16, cdiv(maxl, FV3B_HALO_KU), nf);
   halo_periodic_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
   return check_launch("fv3b_halo_periodic");
 }
