@@ -63,6 +63,8 @@ def _run_device(delp, qs, nk, ptop=300.0):
     (48, 48, 80, 8, 0.5, 3),
     (17, 3, 7, 16, 0.95, 4),
     (192, 192, 80, 2, 0.3, 5),  # the C2 column count
+    (5, 3, 1, 2, 0.5, 6),       # a single layer: the whole column into one target layer
+    (1, 1, 2, 1, 0.9, 7),       # a single column
 ])
 def test_remap_map_bitwise_vs_oracle(ni, nj, nk, nq, spread, seed):
     delp, qs = _case(ni, nj, nk, nq, seed, spread)

@@ -46,6 +46,8 @@ def _run(delp, qs, nk, sc):
     (48, 48, 60, 6, 25.0, 1e-6, 4),               # akap * peln from -345 to +290
     (20, 6, 30, 1, -3.0, 0.5, 5),                 # negative exponents, |x| < 0.5 ln2 .. 35
     (192, 192, 80, 6, 287.05 / 1004.6, 300.0, 6),  # the C2 column count
+    (5, 3, 1, 2, 287.05 / 1004.6, 300.0, 7),      # a single layer (program domain nk = 2)
+    (1, 1, 2, 6, 287.05 / 1004.6, 300.0, 8),      # a single column
 ])
 def test_moist_pk_bitwise_vs_oracle(ni, nj, nk, nw, akap, ptop, seed):
     from paper_2205_04148_b200.config import RunConfig
