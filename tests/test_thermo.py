@@ -29,8 +29,10 @@ def test_det_exp_edges():
     assert det_exp(1e-300) == 1.0
     x = np.array([np.inf, -np.inf, np.nan, 710.0, -750.0])
     got = det_exp(x)
-    np.testing.assert_array_equal(np.isnan(got), np.isnan(np.exp(x)))
-    np.testing.assert_array_equal(got[~np.isnan(got)], np.exp(x)[~np.isnan(got)])
+    with np.errstate(over="ignore"):
+        want = np.exp(x)
+    np.testing.assert_array_equal(np.isnan(got), np.isnan(want))
+    np.testing.assert_array_equal(got[~np.isnan(got)], want[~np.isnan(got)])
     # exp(log(x)) round trip near 1 ulp
     v = np.random.default_rng(3).uniform(1.0, 1e5, 1000)
     assert np.allclose(det_exp(det_log(v)), v, rtol=4e-16 * 8)
