@@ -263,6 +263,8 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         barrier()
     ms = t0.elapsed_time(t1) / args.steps
     clocks = clk.summary()
+    if world > 1 and args.halo == "peer":
+        d.halo.sync.check()  # a timed-out neighbour barrier voids the run instead of reporting it
 
     # end to end: pinned host state in, step, host state out (Dycore.step_host:
     # uploads and downloads on their own streams, the tracers' uploads overlap
