@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define FV3B_ABI_VERSION 3
+#define FV3B_ABI_VERSION 4
 
 enum {
   FV3B_OK = 0,
@@ -67,6 +67,27 @@ typedef struct {
 
 int fv3b_abi_version(void);
 const char* fv3b_last_error(void);
+
+/* Launch-configuration knobs (the launch-config tuner, tools/tune.py, and the
+ * parity tests that force a level-march shape).  Process-wide; a value of 0
+ * restores the automatic choice.  The level-marching tile kernels give each
+ * CTA a chunk of `kchunk` consecutive levels; automatically the chunk makes
+ * the launch one wave of equal chunks.  A kernel-specific knob wins over
+ * FV3B_TUNE_KCHUNK.  Replaces the reference's schedule menu
+ * (scheduling.py:28 tile sizes, :266-315 enumerate_schedules) for the knobs
+ * that are run-time choices here. */
+enum {
+  FV3B_TUNE_KCHUNK = 0,               /* every level-marching tile kernel */
+  FV3B_TUNE_KCHUNK_DSW_TRANSPORT = 1, /* d_sw delp / pt / w transport */
+  FV3B_TUNE_KCHUNK_DSW_MOMENTUM = 2,  /* d_sw u / v momentum */
+  FV3B_TUNE_KCHUNK_CSW = 3,           /* c_sw (c_grid) */
+  FV3B_TUNE_KCHUNK_TRACER = 4,        /* tracer_2d */
+  FV3B_TUNE_KCHUNK_FV_TP_2D = 5,      /* fv_tp_2d program */
+  FV3B_TUNE_RIEM_COLS = 6,            /* columns per CTA of the vertical solver (0 = automatic) */
+  FV3B_TUNE_COUNT = 7
+};
+int fv3b_tune_set(int knob, int value); /* value >= 0; FV3B_EINVAL for an unknown knob */
+int fv3b_tune_get(int knob);            /* current value (0 = automatic), -1 for an unknown knob */
 
 /* K0  copy.stn — `out = inp` over the interior (PAPER.md:589 copy stencil).
  *     fields: inp, out.  scalars: none. */

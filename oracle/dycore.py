@@ -110,13 +110,7 @@ class OracleDycore:
             st[n][...] = 0.0
         st["dp1"][...] = st["delp"]
         for _ in range(cfg.n_split):
-            yield ["u", "v", "w", "delp", "pt", "gz"]
-            self.call("c_grid", {**c, "dt2": 0.5 * dt})
-            yield ["uc", "vc"]
-            self.call("d_sw", {**c, "dt": dt})
-            self.call("nh_d", {**c, "dt": dt})
-            yield ["pef", "gz"]
-            self.call("p_grad_d", {**c, "dt": dt})
+            yield from self.acoustic_phases()
         yield cfg.tracer_names() + ["cx", "cy", "xfa", "yfa", "mfx", "mfy", "delp"]
         self.call("tracer_2d", c)
         self.call("remap_tracers", c)
@@ -132,6 +126,28 @@ class OracleDycore:
         for w, dw in (("u", "du"), ("v", "dv")):
             remap_map.remap_map(st, [w], ak, bk, cfg.nk, self._h, delp_key=dw)
         thermo.apply(st, cfg.tracer_names()[:thermo.SPECIES], cfg.nk, self._h, thermo.constants(c))
+
+    def acoustic_phases(self):
+        """One acoustic substep (config C1), mirroring ``Dycore.acoustic_phases``
+        (the caller zeroes the accumulators and sets dp1 at the step start)."""
+        c, dt = dict(self.cfg.consts), self.cfg.dt_acoustic
+        yield ["u", "v", "w", "delp", "pt", "gz"]
+        self.call("c_grid", {**c, "dt2": 0.5 * dt})
+        yield ["uc", "vc"]
+        self.call("d_sw", {**c, "dt": dt})
+        self.call("nh_d", {**c, "dt": dt})
+        yield ["pef", "gz"]
+        self.call("p_grad_d", {**c, "dt": dt})
+
+    def substep(self, first: bool = True) -> None:
+        """One acoustic substep; ``first`` starts a timestep (accumulators
+        zeroed, dp1 = delp), as the device's first substep does."""
+        if first:
+            for n in ("cx", "cy", "xfa", "yfa", "mfx", "mfy"):
+                self.state[n][...] = 0.0
+            self.state["dp1"][...] = self.state["delp"]
+        for names in self.acoustic_phases():
+            self.halo(names)
 
     def step(self) -> None:
         for names in self.phases():

@@ -12,7 +12,7 @@ from pathlib import Path
 
 LIB_PATH = Path(os.environ.get("FV3B_LIB", Path(__file__).resolve().parent / "libfv3b.so"))
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 
 class Field(ctypes.Structure):
@@ -114,3 +114,53 @@ def enable_peer_access(peer: int) -> None:
     rc = fn(peer)
     if rc != 0:
         raise Fv3bError("fv3b_enable_peer_access", rc, lib().fv3b_last_error().decode())
+
+
+# launch-configuration knobs (include/fv3b.h FV3B_TUNE_*)
+TUNE = {
+    "kchunk": 0,
+    "kchunk_dsw_transport": 1,
+    "kchunk_dsw_momentum": 2,
+    "kchunk_csw": 3,
+    "kchunk_tracer": 4,
+    "kchunk_fv_tp_2d": 5,
+    "riem_cols": 6,
+}
+
+
+def tune_set(knob: str, value: int) -> None:
+    """``fv3b_tune_set``: process-wide override of a launch-configuration
+    knob (0 restores the automatic choice)."""
+    fn = lib().fv3b_tune_set
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.c_int, ctypes.c_int]
+    rc = fn(TUNE[knob], int(value))
+    if rc != 0:
+        raise Fv3bError("fv3b_tune_set", rc, lib().fv3b_last_error().decode())
+
+
+def tune_get(knob: str) -> int:
+    fn = lib().fv3b_tune_get
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.c_int]
+    return fn(TUNE[knob])
+
+
+class tuning:
+    """Context manager: ``with tuning(kchunk=3): ...`` sets knobs and
+    restores their previous values on exit."""
+
+    def __init__(self, **knobs: int):
+        self.knobs = knobs
+        self.saved: dict[str, int] = {}
+
+    def __enter__(self):
+        for k, v in self.knobs.items():
+            self.saved[k] = tune_get(k)
+            tune_set(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.saved.items():
+            tune_set(k, v)
+        return False

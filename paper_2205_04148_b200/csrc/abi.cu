@@ -61,7 +61,60 @@ int check_launch(const char* what) {
 
 }  // namespace fv3b
 
+// ---------------------------------------------------------------------------
+// Launch-configuration knobs, SM count, per-device shared-memory attributes.
+// ---------------------------------------------------------------------------
+#include <atomic>
+#include <mutex>
+#include <set>
+#include <utility>
+
+namespace fv3b {
+
+static std::atomic<int> g_tune[FV3B_TUNE_COUNT];
+
+int tune_get(int knob) { return (knob >= 0 && knob < FV3B_TUNE_COUNT) ? g_tune[knob].load() : 0; }
+
+int num_sms() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = cache[dev].load();
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev].store(n);
+  }
+  return n;
+}
+
+int ensure_smem(const void* fn, size_t bytes, const char* what) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({fn, dev})) return FV3B_OK;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return check_launch(what);
+  done.insert({fn, dev});
+  return FV3B_OK;
+}
+
+}  // namespace fv3b
+
 extern "C" int fv3b_abi_version(void) { return FV3B_ABI_VERSION; }
+
+extern "C" int fv3b_tune_set(int knob, int value) {
+  if (knob < 0 || knob >= FV3B_TUNE_COUNT || value < 0)
+    return fv3b::fail(FV3B_EINVAL, "fv3b_tune_set: unknown knob %d or negative value %d", knob, value);
+  fv3b::g_tune[knob].store(value);
+  return FV3B_OK;
+}
+
+extern "C" int fv3b_tune_get(int knob) {
+  return (knob >= 0 && knob < FV3B_TUNE_COUNT) ? fv3b::g_tune[knob].load() : -1;
+}
 
 extern "C" const char* fv3b_last_error(void) { return fv3b::g_err.c_str(); }
 

@@ -465,9 +465,7 @@ static int set_smem(const void* fn, size_t bytes) {
 // scheduler owns the same number of recurrences.
 static int cols_per_cta(size_t bytes_per_col, int64_t columns) {
   const size_t per_sm = 228 * 1024, reserved = 1024;
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = num_sms();
   const int64_t need = (columns + sms - 1) / sms;  // columns per SM for a single wave
   int best_cols = 1, best_total = 0;
   for (int m = 4; m <= 32; m += 4) {
@@ -486,7 +484,8 @@ static int cols_per_cta(size_t bytes_per_col, int64_t columns) {
 
 int launch_riem(const RiemArgs& a, cudaStream_t st) {
   const size_t per_col = (size_t)(a.nk + 1) * sizeof(double);
-  const int nc = cols_per_cta(per_col, (int64_t)a.ni_ext * a.nj_ext);
+  const int forced = tune_get(FV3B_TUNE_RIEM_COLS);
+  const int nc = forced > 0 ? (forced < NC_MAX ? forced : NC_MAX) : cols_per_cta(per_col, (int64_t)a.ni_ext * a.nj_ext);
   const size_t bytes = per_col * nc;
   FV3B_TRY(set_smem((const void*)riem_kernel, bytes));
   const int cols = a.ni_ext * a.nj_ext;

@@ -39,14 +39,27 @@ int check_launch(const char* what);
 
 inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
+// SM count of the current device (cached per device).
+int num_sms();
+
+// Launch-configuration knob (fv3b_tune_set); 0 = automatic.
+int tune_get(int knob);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `fn` once per
+// (kernel, device): the attribute is per device context, so a process that
+// launches on several GPUs sets it on each.
+int ensure_smem(const void* fn, size_t bytes, const char* what);
+
 // Levels per CTA of a level-marching tile kernel: a single wave when the
 // tiles fit the resident CTA slots (every CTA gets an equal chunk of levels,
-// no tail wave), otherwise one whole column of levels per CTA.
-inline int level_chunk(int tiles, int nk, int ctas_per_sm) {
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int slots = sms * ctas_per_sm;
+// no tail wave), otherwise one whole column of levels per CTA.  `knob` (and
+// FV3B_TUNE_KCHUNK) override the choice.
+inline int level_chunk(int knob, int tiles, int nk, int ctas_per_sm) {
+  if (nk <= 0 || tiles <= 0) return 1;
+  int forced = tune_get(knob);
+  if (forced <= 0) forced = tune_get(FV3B_TUNE_KCHUNK);
+  if (forced > 0) return forced < nk ? forced : nk;
+  const int slots = num_sms() * ctas_per_sm;
   int per_tile = tiles >= slots ? 1 : slots / tiles;
   if (per_tile > nk) per_tile = nk;
   return cdiv(nk, per_tile);

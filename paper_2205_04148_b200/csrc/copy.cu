@@ -53,16 +53,6 @@ __global__ void __launch_bounds__(256) copy_scalar_kernel(View in, View out, int
   }
 }
 
-static int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
 
 }  // namespace fv3b
 

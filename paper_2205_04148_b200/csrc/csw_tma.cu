@@ -233,20 +233,10 @@ int csw_maps(CswTmaArgs& a, const Geo& g, const fv3b_field* in5, const fv3b_fiel
 template <bool EXT>
 static int launch_t(const CswTmaArgs& a0, cudaStream_t st) {
   using L = CsLayout<CS_TI, CS_TJ>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(csw_kernel<CS_TI, CS_TJ, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)L::bytes) != cudaSuccess)
-      return check_launch("c_sw smem attribute");
-    attr = true;
-  }
+  FV3B_TRY(ensure_smem((const void*)csw_kernel<CS_TI, CS_TJ, EXT>, L::bytes, "c_sw smem attribute"));
   CswTmaArgs a = a0;
   const int tiles = cdiv(a.ni, CS_TI) * cdiv(a.nj, CS_TJ);
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  (void)sms;
-  a.kchunk = level_chunk(tiles, a.nk, 2);
+  a.kchunk = level_chunk(FV3B_TUNE_KCHUNK_CSW, tiles, a.nk, 2);
   dim3 grid(cdiv(a.ni, CS_TI), cdiv(a.nj, CS_TJ), cdiv(a.nk, a.kchunk));
   csw_kernel<CS_TI, CS_TJ, EXT><<<grid, CS_NT, L::bytes, st>>>(a);
   return check_launch("c_sw");

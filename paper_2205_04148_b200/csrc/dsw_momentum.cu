@@ -361,20 +361,10 @@ constexpr int MO_TI = 32, MO_TJ = 16;
 
 int launch_dsw_momentum(const DswMoArgs& a0, cudaStream_t st) {
   using L = MoLayout<MO_TI, MO_TJ>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(dsw_momentum_kernel<MO_TI, MO_TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)L::bytes) != cudaSuccess)
-      return check_launch("d_sw momentum smem attribute");
-    attr = true;
-  }
+  FV3B_TRY(ensure_smem((const void*)dsw_momentum_kernel<MO_TI, MO_TJ>, L::bytes, "d_sw momentum smem attribute"));
   DswMoArgs a = a0;
   const int tiles = cdiv(a.ni, MO_TI) * cdiv(a.nj, MO_TJ);
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  (void)sms;
-  a.kchunk = level_chunk(tiles, a.nk, cps_of<MO_TJ>());
+  a.kchunk = level_chunk(FV3B_TUNE_KCHUNK_DSW_MOMENTUM, tiles, a.nk, cps_of<MO_TJ>());
   dim3 grid(cdiv(a.ni, MO_TI), cdiv(a.nj, MO_TJ), cdiv(a.nk, a.kchunk));
   dsw_momentum_kernel<MO_TI, MO_TJ><<<grid, nt_of<MO_TJ>(), L::bytes, st>>>(a);
   return check_launch("d_sw momentum");

@@ -389,21 +389,10 @@ constexpr int DT_TI = 32, DT_TJ = 8;
 
 int launch_dsw_transport(const DswTpArgs& a0, cudaStream_t st) {
   using L = Dt2Layout<DT_TI, DT_TJ>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(dsw_transport2_kernel<DT_TI, DT_TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)L::bytes) != cudaSuccess)
-      return check_launch("d_sw transport smem attribute");
-    attr = true;
-  }
+  FV3B_TRY(ensure_smem((const void*)dsw_transport2_kernel<DT_TI, DT_TJ>, L::bytes, "d_sw transport smem attribute"));
   DswTpArgs a = a0;
   const int tiles = cdiv(a.ni, DT_TI) * cdiv(a.nj, DT_TJ);
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // ~4 waves of one CTA per SM, at least 2 levels per CTA so the prefetch overlaps
-  (void)sms;
-  a.kchunk = level_chunk(tiles, a.nk, cps_of<DT_TI, DT_TJ>());
+  a.kchunk = level_chunk(FV3B_TUNE_KCHUNK_DSW_TRANSPORT, tiles, a.nk, cps_of<DT_TI, DT_TJ>());
   dim3 grid(cdiv(a.ni, DT_TI), cdiv(a.nj, DT_TJ), cdiv(a.nk, a.kchunk));
   dsw_transport2_kernel<DT_TI, DT_TJ><<<grid, nt_of<DT_TI, DT_TJ>(), L::bytes, st>>>(a);
   return check_launch("d_sw transport");

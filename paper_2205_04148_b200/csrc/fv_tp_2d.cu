@@ -570,15 +570,9 @@ __global__ void __launch_bounds__(TI * TJ, 2) tracer2_kernel(const __grid_consta
 template <int TI, int TJ>
 static int launch_tracer2(const TpArgs& a0, cudaStream_t st) {
   using L = Tr2Layout<TI, TJ>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(tracer2_kernel<TI, TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes) !=
-        cudaSuccess)
-      return check_launch("tracer_2d smem attribute");
-    attr = true;
-  }
+  FV3B_TRY(ensure_smem((const void*)tracer2_kernel<TI, TJ>, L::bytes, "tracer_2d smem attribute"));
   TpArgs a = a0;
-  a.kchunk = level_chunk(cdiv(a.ni, TI) * cdiv(a.nj, TJ), a.nk, 2);
+  a.kchunk = level_chunk(FV3B_TUNE_KCHUNK_TRACER, cdiv(a.ni, TI) * cdiv(a.nj, TJ), a.nk, 2);
   dim3 grid(cdiv(a.ni, TI), cdiv(a.nj, TJ), cdiv(a.nk, a.kchunk));
   tracer2_kernel<TI, TJ><<<grid, TI * TJ, L::bytes, st>>>(a);
   return check_launch("tracer_2d");
@@ -587,24 +581,10 @@ static int launch_tracer2(const TpArgs& a0, cudaStream_t st) {
 template <int TI, int TJ>
 static int launch_tp(const TpArgs& a0, cudaStream_t st) {
   using L = TpLayout<TI, TJ, false>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(tp_kernel<TI, TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes) !=
-        cudaSuccess)
-      return check_launch("tp smem attribute");
-    attr = true;
-  }
+  FV3B_TRY(ensure_smem((const void*)tp_kernel<TI, TJ>, L::bytes, "tp smem attribute"));
   TpArgs a = a0;
   const int tiles = cdiv(a.ni, TI) * cdiv(a.nj, TJ);
-  int sms = 148;
-  {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  // ~4 waves of one CTA per SM; at least 2 levels per CTA so the pipeline overlaps
-  (void)sms;
-  a.kchunk = level_chunk(tiles, a.nk, cps_of<TJ>());
+  a.kchunk = level_chunk(FV3B_TUNE_KCHUNK_FV_TP_2D, tiles, a.nk, cps_of<TJ>());
   dim3 grid(cdiv(a.ni, TI), cdiv(a.nj, TJ), cdiv(a.nk, a.kchunk));
   tp_kernel<TI, TJ><<<grid, nt_of<TJ>(), L::bytes, st>>>(a);
   return check_launch("fv_tp_2d");

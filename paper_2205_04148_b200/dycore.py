@@ -426,18 +426,31 @@ class Dycore:
         # step start: the first d_sw reads the former as 0.0 (acc_reset) and
         # writes the latter (its delp input) instead of a fill and a copy
         for it in range(cfg.n_split):
-            yield ["u", "v", "w", "delp", "pt", "gz"]
-            self.c_grid()
-            yield ["uc", "vc"]
-            self.d_sw(first=it == 0)
-            self.nh_d()
-            yield ["pef", "gz"]
-            self.p_grad_d()
+            yield from self.acoustic_phases(first=it == 0)
         yield cfg.tracer_names() + list(ACCUM) + ["delp"]  # (delp: the winds' remapping thickness)
         self.tracer_2d()
         self.remap()
         self.remap_map()
         self.moist_pk()
+
+    def acoustic_phases(self, first: bool = False):
+        """One acoustic substep (BASELINE config C1: halo, c_sw +
+        riem_solver_c + p_grad_c, halo, d_sw, then the D-grid vertical solve
+        and pressure gradient), yielding its halo-update points like
+        ``phases``.  ``first``: the timestep's first substep (d_sw's
+        acc_reset and dp1 copy)."""
+        yield ["u", "v", "w", "delp", "pt", "gz"]
+        self.c_grid()
+        yield ["uc", "vc"]
+        self.d_sw(first=first)
+        self.nh_d()
+        yield ["pef", "gz"]
+        self.p_grad_d()
+
+    def substep(self, first: bool = False) -> None:
+        """Enqueue one acoustic substep on the current stream."""
+        for names in self.acoustic_phases(first):
+            self.halo.update(names)
 
     def step(self) -> None:
         """Enqueue one full timestep on the current stream."""

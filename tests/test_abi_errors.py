@@ -65,3 +65,15 @@ def test_wrong_rank_is_a_layout_error(lib):
     rc = _lib.entry("fv3b_copy")(fields, 2, None, 0, ctypes.byref(dom), None)
     assert rc == -2, rc  # FV3B_ELAYOUT
     assert "rank" in lib.fv3b_last_error().decode()
+
+
+def test_tuning_knobs_roundtrip(lib):
+    """fv3b_tune_set / fv3b_tune_get (host-only state, no device)."""
+    assert _lib.tune_get("kchunk") == 0
+    with _lib.tuning(kchunk=3, kchunk_csw=5):
+        assert _lib.tune_get("kchunk") == 3 and _lib.tune_get("kchunk_csw") == 5
+    assert _lib.tune_get("kchunk") == 0 and _lib.tune_get("kchunk_csw") == 0
+    assert lib.fv3b_tune_set(99, 1) < 0 and "unknown knob" in lib.fv3b_last_error().decode()
+    assert lib.fv3b_tune_set(0, -1) < 0
+    assert lib.fv3b_tune_get(99) == -1
+    assert set(_lib.TUNE.values()) == set(range(len(_lib.TUNE)))
