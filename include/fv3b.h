@@ -165,12 +165,14 @@ int fv3b_c_sw(const fv3b_field* f, int nf, const double* s, int ns,
 int fv3b_c_grid(const fv3b_field* f, int nf, const double* s, int ns,
                 const fv3b_domain* d, void* stream);
 
-/* K3  d_sw.stn — D-grid Lagrangian step (two fused kernels).  fields: u, v,
- *     w, delp, pt, uc, vc, cx, cy, xfa, yfa, mfx, mfy (3-D); dx, dy, dxc, dyc,
- *     rdx, rdy, rdxa, rdya, area, rarea, rarea_c, f0 (2-D); u, v, w, delp, pt,
- *     cx, cy, xfa, yfa, mfx, mfy outputs (3-D; accumulators may alias).
- *     [optional 37th: dp1_out, receives the input delp].  scalars: ppm_p1,
- *     ppm_p2, dt, dddmp, d2_bg, da_min, damp_w [, acc_reset: nonzero reads
+/* K3  d_sw.stn — D-grid Lagrangian step (two fused kernels), with del6 flux
+ *     damping (FV3 delnflux, nord = 2) of delp, pt, w and the vorticity.
+ *     fields: u, v, w, delp, pt, uc, vc, cx, cy, xfa, yfa, mfx, mfy (3-D);
+ *     dx, dy, dxc, dyc, rdx, rdy, rdxa, rdya, area, rarea, rarea_c, f0,
+ *     del6_u, del6_v (2-D); u, v, w, delp, pt, cx, cy, xfa, yfa, mfx, mfy
+ *     outputs (3-D; accumulators may alias).  [optional 39th: dp1_out,
+ *     receives the input delp].  scalars: ppm_p1, ppm_p2, dt, dddmp, d2_bg,
+ *     da_min, damp4, damp4h (= damp4 / 2), dampv [, acc_reset: nonzero reads
  *     the accumulator inputs as 0.0]. */
 int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns,
               const fv3b_domain* d, void* stream);

@@ -21,6 +21,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+from .programs.templates import DAMP4, DAMPV
+
 
 @dataclass(frozen=True)
 class RunConfig:
@@ -35,7 +37,9 @@ class RunConfig:
     # physical constants of the programs (templates.RIEM_CONSTS / D_CONSTS)
     consts: dict = field(default_factory=lambda: {
         "ptop": 300.0, "rdgas": 287.05, "grav": 9.80665, "gama": 1.4, "p_fac": 0.05,
-        "dddmp": 0.2, "d2_bg": 0.0, "da_min": 1.0e8, "damp_w": 0.02,
+        "dddmp": 0.2, "d2_bg": 0.0, "da_min": 1.0e8,
+        # del6 flux-damping coefficients of d_sw (templates.D_CONSTS: (c * da_min) ** 3)
+        "damp4": DAMP4, "damp4h": 0.5 * DAMP4, "dampv": DAMPV,
         "ppm_p1": 7.0 / 12.0, "ppm_p2": -1.0 / 12.0,
         # heat capacities of the post-remap diagnostics (FV3 constants; oracle/thermo.py)
         "cp_air": 1004.6, "rvgas": 461.50, "c_liq": 4185.5, "c_ice": 1972.0,
@@ -84,4 +88,4 @@ STATE_3D = ["u", "v", "w", "delp", "pt", "gz", "pef", "uc", "vc", "cx", "cy", "x
 # post-remap diagnostics (fv3b_moist_pk): interface pe, peln, pk; layer pkz, cvm
 DIAG_3D = ["pe", "peln", "pk", "pkz", "cvm"]
 METRICS_2D = ["dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxc", "rdyc", "rdxa", "rdya", "area", "rarea", "rarea_c",
-              "f0", "fc", "ws"]
+              "f0", "fc", "ws", "del6_u", "del6_v"]

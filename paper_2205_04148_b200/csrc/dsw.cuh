@@ -8,7 +8,11 @@ namespace fv3b {
 
 struct DswTpArgs {
   CUtensorMap qbox[5];  // delp, pt, w, uc, vc     (q-box: i in [-4, TI+6), j in [-3, TJ+3))
-  CUtensorMap met[5];   // dx, dy, rdxa, rdya, area (q-box, level 0)
+  CUtensorMap met[4];   // area, rarea, del6_u, del6_v (q-box, level 0)
+  const double* dx;     // courant metrics, interior origins (2-D, the 3-D fields' J stride)
+  const double* dy;
+  const double* rdxa;
+  const double* rdya;
   double* delpo;
   double* pto;
   double* wo;
@@ -20,11 +24,11 @@ struct DswTpArgs {
   int64_t sj, sk;
   int i0, j0;           // allocated column / row of the interior origin
   int ni, nj, nk, kchunk;
-  double p1, p2, dt, damp_w;
+  double p1, p2, dt, damp4, damp4h;  // del6 coefficient, half of it (mass-weighted chains)
 };
 
 int dsw_transport_maps(DswTpArgs& a, const Geo& g, const fv3b_field* qbox5, const fv3b_field* acc6,
-                       const fv3b_field* met5);
+                       const fv3b_field* met4);
 int launch_dsw_transport(const DswTpArgs& a, cudaStream_t st);
 
 }  // namespace fv3b
@@ -38,9 +42,11 @@ struct DswMoArgs {
   CUtensorMap met[12];       // dx (+1 row), dy, rdxa, rdya, area, f0, rarea, rdx, rdy, dxc, dyc, rarea_c
   double* uo;
   double* vo;
+  const double* del6_u;  // interior origins (2-D, the 3-D fields' J stride)
+  const double* del6_v;
   int64_t sj, sk;
   int i0, j0, ni, nj, nk, kchunk;
-  double p1, p2, dt, dddmp, d2_bg, da_min;
+  double p1, p2, dt, dddmp, d2_bg, da_min, dampv;
 };
 
 int dsw_momentum_maps(DswMoArgs& a, const Geo& g, const fv3b_field& u, const fv3b_field& v, const fv3b_field& uc,

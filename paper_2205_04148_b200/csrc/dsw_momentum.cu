@@ -14,6 +14,12 @@
 //   S3  (during the next level's S0) the u / v updates of the y-threads'
 //       cells.
 //
+// The vorticity flux carries its del6 damping (templates.delnflux on wk with
+// dampv, nord = 2): order 1 of the Laplacian chain (d2_v1, each cell forming
+// its four order-0 face fluxes from dampv * wk) runs in S1, order 2 (d2_v2)
+// in S2, and the y-threads add the last order's face fluxes to fxv / fyv in
+// their u / v updates.
+//
 // Every statement keeps the .stn operand order and association (ked is
 // 0.5 * (ub*uu + vb*vv) with both products rounded as in the interpreter),
 // so results are bitwise the reference's.
@@ -50,6 +56,8 @@ struct MoLayout {
   static constexpr int YW = TI + 8, YH = TJ + 1;   // y faces: i in [-4, TI+4), j in [0, TJ+1)
   static constexpr int JW = TI + 2;                // qj row width
   static constexpr int CW = TI + 2, CH = TJ + 1;   // corners: i in [0, TI+2), j in [0, TJ+1)
+  static constexpr int D1W = TI + 3, D1H = TJ + 3; // d2_v1: [-2, TI+1) x [-2, TJ+1)
+  static constexpr int D2W = TI + 1, D2H = TJ + 1; // d2_v2: [-1, TI) x [-1, TJ)
   static constexpr int n_q = a16(QW * QH), n_q1 = a16(QW * (QH + 1));
   static constexpr int n_x = a16(XW * XH), n_y = a16(YW * YH);
   static constexpr int n_mx = a16(XW * TJ), n_my = a16(TI * YH);
@@ -71,7 +79,9 @@ struct MoLayout {
   static constexpr int o_fx2 = o_qj + n_qj;
   static constexpr int o_fy2 = o_fx2 + n_mx;
   static constexpr int o_fx = o_fy2 + n_my;
-  static constexpr int total = o_fx + n_mx;
+  static constexpr int o_d1 = o_fx + n_mx;
+  static constexpr int o_d2 = o_d1 + a16(D1W * D1H);
+  static constexpr int total = o_d2 + a16(D2W * D2H);
   static constexpr size_t bytes = total * sizeof(double) + 64;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
   static_assert(TJ % SEG == 0 && TI % SEG == 0 && QW % 4 == 2 && XW % 4 == 2 && JW % 4 == 2, "tile shape");
@@ -139,6 +149,14 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
   double* sfx2 = smem + L::o_fx2;
   double* sfy2 = smem + L::o_fy2;
   double* sfx = smem + L::o_fx;
+  double* sd1 = smem + L::o_d1;
+  double* sd2 = smem + L::o_d2;
+  auto D1 = [&](int i, int j) { return sd1 + (j + 2) * L::D1W + (i + 2); };
+  auto D2 = [&](int i, int j) { return sd2 + (j + 1) * L::D2W + (i + 1); };
+  // del6 metrics straight from L1 / L2 (tile-local (i, j); 2-D, J stride sj)
+  const double* gd6u = a.del6_u + gi0 + (int64_t)gj0 * a.sj;
+  const double* gd6v = a.del6_v + gi0 + (int64_t)gj0 * a.sj;
+  const double dampv = a.dampv;
   auto QB = [&](auto* p, int i, int j) { return p + (j + 3) * L::QW + (i + 4); };
   auto CX = [&](auto* p, int i, int j) { return p + (j + 3) * L::XW + i; };
   auto CY = [&](auto* p, int i, int j) { return p + j * L::YW + (i + 4); };
@@ -168,9 +186,13 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
       if (gi2 < a.ni && gj < a.nj) {
         const int64_t off = gi2 + gj * sj + (int64_t)pend_k * sk;
         const double rdx = *QB(srdx, i, j), rdy = *QB(srdy, i, j);
-        a.uo[off] = (*QB(U, i, j) * *QB(sdx, i, j) + *CN(sked, i, j) - *CN(sked, i + 1, j) + fy[u]) * rdx +
+        const int64_t m = i + j * sj;
+        // fyv / fxv + their del6 increments dfy_v2 / dfx_v2
+        const double fyv = fy[u] + __ldg(gd6u + m) * (*D2(i, j) - *D2(i, j - 1));
+        const double fxv = sfx[j * L::XW + i] + __ldg(gd6v + m) * (*D2(i, j) - *D2(i - 1, j));
+        a.uo[off] = (*QB(U, i, j) * *QB(sdx, i, j) + *CN(sked, i, j) - *CN(sked, i + 1, j) + fyv) * rdx +
                     (*CN(sddv, i + 1, j) - *CN(sddv, i, j)) * rdx;
-        a.vo[off] = (*QB(V, i, j) * *QB(sdy, i, j) + *CN(sked, i, j) - *CN(sked, i, j + 1) - sfx[j * L::XW + i]) * rdy +
+        a.vo[off] = (*QB(V, i, j) * *QB(sdy, i, j) + *CN(sked, i, j) - *CN(sked, i, j + 1) - fxv) * rdy +
                     (*CN(sddv, i, j + 1) - *CN(sddv, i, j)) * rdy;
       }
     }
@@ -220,7 +242,20 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
       constexpr int NU = (TJ + 1) * NSEG;   // ub*uu rows j in [0, TJ+1), faces [0, TI+1)
       constexpr int NV = (TI + 1) * (TJ / SEG);  // vb*vv columns i in [0, TI+1), faces [0, TJ+1)
       constexpr int ND = (TI + 1) * (TJ + 1);    // ddv corners
-      for (int item = tid; item < NY + NX + NU + NV + ND; item += blockDim.x) {
+      constexpr int N1 = L::D1W * L::D1H;        // d2_v1 cells
+      for (int item = tid; item < NY + NX + NU + NV + ND + N1; item += blockDim.x) {
+        if (item >= NY + NX + NU + NV + ND) {
+          // d2_v0 = dampv * wk ; dfx_v0 = del6_v * (d2_v0[-1,0] - d2_v0) ; d2_v1 = div(dfx_v0, dfy_v0) * rarea
+          const int e = item - (NY + NX + NU + NV + ND);
+          const int i = e % L::D1W - 2, j = e / L::D1W - 2;
+          const int64_t m = i + j * sj;
+          const double v0 = __ldg(gd6v + m), v1 = __ldg(gd6v + m + 1), u0 = __ldg(gd6u + m), u1 = __ldg(gd6u + m + sj);
+          const double c = dampv * *QB(swk, i, j), wq = dampv * *QB(swk, i - 1, j), eq = dampv * *QB(swk, i + 1, j);
+          const double sq = dampv * *QB(swk, i, j - 1), nq = dampv * *QB(swk, i, j + 1);
+          const double fx0 = v0 * (wq - c), fx1 = v1 * (c - eq), fy0 = u0 * (sq - c), fy1 = u1 * (c - nq);
+          *D1(i, j) = (fx0 - fx1 + fy0 - fy1) * *QB(srarea, i, j);
+          continue;
+        }
         if (item < NY) {
           const int ci = item % NCY - 3, jb = (item / NCY) * SEG;
           double f[SEG + 1];
@@ -349,6 +384,16 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
         const int i = e % (TI + 1), j = e / (TI + 1);
         *CN(sked, i, j) = 0.5 * (*CN(sked, i, j) + *CN(svv, i, j));
       }
+    }
+    // d2_v2 = div(dfx_v1, dfy_v1) * rarea, dfx_v1 = del6_v * (d2_v1 - d2_v1[-1,0])
+    for (int e = tid; e < L::D2W * L::D2H; e += blockDim.x) {
+      const int i = e % L::D2W - 1, j = e / L::D2W - 1;
+      const int64_t m = i + j * sj;
+      const double v0 = __ldg(gd6v + m), v1 = __ldg(gd6v + m + 1), u0 = __ldg(gd6u + m), u1 = __ldg(gd6u + m + sj);
+      const double c = *D1(i, j);
+      const double fx0 = v0 * (c - *D1(i - 1, j)), fx1 = v1 * (*D1(i + 1, j) - c);
+      const double fy0 = u0 * (c - *D1(i, j - 1)), fy1 = u1 * (*D1(i, j + 1) - c);
+      *D2(i, j) = (fx0 - fx1 + fy0 - fy1) * *QB(srarea, i, j);
     }
     __syncthreads();
   }

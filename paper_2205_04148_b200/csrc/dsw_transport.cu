@@ -11,15 +11,21 @@
 //
 //   delp  weights xfx / yfx   -> fxm, fym (mass fluxes, kept in smem), delpn
 //   pt    weights fxm / fym   -> pt' = (pt*delp + div(gxp, gyp)*rarea) / delpn
-//   w     weights fxm / fym   -> w'  = (w*delp + div(hxw, hyw)*rarea) / delpn + damp_w*lap(w)
+//   w     weights fxm / fym   -> w'  = (w*delp + div(hxw, hyw)*rarea) / delpn
 //
 // exactly the tracer_2d update with dp1 = delp and (mfx, mfy) = (fxm, fym),
 // so the statement chain, association and operand order are the .stn's and
 // the results are bitwise the interpreter's.  Phase A evaluates yppm(q) ->
 // fy2, qi and xppm(q) -> fx2, qj over the tile halo (register sliding
 // windows, ppm.cuh); phase B the outer xppm(qi) / yppm(qj) and the weighted
-// fluxes.  Four barriers per level: courant | phase A of delp, pt, w |
-// phase B of delp | phase B of pt, w; then each thread updates its own cell.
+// fluxes.  Each flux carries its del6 damping increment (templates.delnflux,
+// FV3 deln_flux with nord = 2): the two Laplacian orders d2_1, d2_2 of every
+// quantity are cell passes riding in the courant and phase-A intervals (each
+// cell forms its four order-0/1 face fluxes itself: same operands, same
+// bits as the stored temporaries), and the last order's face fluxes are
+// formed by the phase-B items.  Five barriers per level: courant + d2_1 |
+// phase A + d2_2 + mass weights | phase B of delp | phase B of pt, w | cell
+// updates (d2_1 of the next level borrows the flux arrays they read).
 #include "common.cuh"
 #include "dsw.cuh"
 #include "fastdiv.cuh"
@@ -53,26 +59,33 @@ struct Dt2Layout {
   static constexpr int XW = TI + 2, XH = TJ + 6;
   static constexpr int YW = TI + 8, YH = TJ + 1;
   static constexpr int JW = TI + 2;
+  static constexpr int D1W = TI + 4, D1H = TJ + 4;  // d2 order 1: [-2, TI+2) x [-2, TJ+2)
+  static constexpr int D2W = TI + 2, D2H = TJ + 2;  // d2 order 2: [-1, TI+1) x [-1, TJ+1)
   static constexpr int n_q = a16(QW * QH);
   static constexpr int n_x = a16(XW * XH), n_y = a16(YW * YH);
   static constexpr int n_mx = a16(XW * TJ), n_my = a16(TI * YH);
   static constexpr int n_qi = a16(QW * TJ), n_qj = a16(JW * QH);
+  static constexpr int n_d1 = a16(D1W * D1H), n_d2 = a16(D2W * D2H);
   static constexpr int n_set = n_qi + n_qj + n_mx + n_my;  // qi, qj, fx2, fy2 of one quantity
   static constexpr int n_fl = n_mx + n_my;                 // x / y fluxes of one quantity
   static constexpr int o_stage = 0;                        // delp, pt, w, uc, vc
-  static constexpr int o_met = 5 * n_q;                    // dx, dy, rdxa, rdya, area
-  static constexpr int o_crx = o_met + 5 * n_q;
+  static constexpr int o_met = 5 * n_q;                    // area, rarea, del6_u, del6_v
+  static constexpr int o_crx = o_met + 4 * n_q;
   static constexpr int o_xfx = o_crx + n_x;
   static constexpr int o_cry = o_xfx + n_x;
   static constexpr int o_yfx = o_cry + n_y;
   static constexpr int o_set = o_yfx + n_y;
-  static constexpr int o_fl = o_set + 3 * n_set;
-  static constexpr int total = o_fl + 3 * n_fl;
+  static constexpr int o_fl = o_set + 3 * n_set;           // (d2_1 of the three quantities until phase B)
+  static constexpr int o_d2 = o_fl + 3 * n_fl;             // d2_2 of delp, pt, w
+  static constexpr int o_mw = o_d2 + 3 * n_d2;             // damp4h * (delp[-1] + delp): x faces, y faces
+  static constexpr int total = o_mw + n_mx + n_my;
   static constexpr size_t bytes = total * sizeof(double) + 64;
-  static_assert(bytes <= 227 * 1024, "shared memory budget");
+  static_assert(3 * n_d1 <= 3 * n_fl, "d2_1 fits the flux arrays it borrows");
+  // two CTAs per SM: 228 KB per SM, 1 KB reserved per CTA
+  static_assert(cps_of<TI, TJ>() * (bytes + 1024) <= 228 * 1024, "shared memory budget");
   static_assert(TJ % SEG == 0 && TI % SEG == 0 && QW % 4 == 2 && XW % 4 == 2 && JW % 4 == 2, "tile shape");
   static constexpr uint32_t tx_stage = 5 * QW * QH * 8;
-  static constexpr uint32_t tx_met = 5 * QW * QH * 8;
+  static constexpr uint32_t tx_met = 4 * QW * QH * 8;
 };
 
 template <int TI, int TJ>
@@ -104,17 +117,22 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
   if (tid == 0 && k1 > k0) {
     mbar_expect_tx(&bar[1], L::tx_met);
 #pragma unroll
-    for (int f = 0; f < 5; ++f) tma_load3(smem + L::o_met + f * L::n_q, &a.met[f], xq, yq, 0, &bar[1]);
+    for (int f = 0; f < 4; ++f) tma_load3(smem + L::o_met + f * L::n_q, &a.met[f], xq, yq, 0, &bar[1]);
     issue(k0);
   }
   const double* sdp = smem + L::o_stage;
   const double* suc = sdp + 3 * L::n_q;
   const double* svc = sdp + 4 * L::n_q;
-  const double* sdx = smem + L::o_met;
-  const double* sdy = sdx + L::n_q;
-  const double* srdxa = sdy + L::n_q;
-  const double* srdya = srdxa + L::n_q;
-  const double* sarea = srdya + L::n_q;
+  const double* sarea = smem + L::o_met;
+  const double* srarea = sarea + L::n_q;
+  const double* sd6u = srarea + L::n_q;
+  const double* sd6v = sd6u + L::n_q;
+  // courant-only metrics straight from L1 / L2 (tile-local (i, j); 2-D, J stride sj)
+  const int64_t moff = gi0 + (int64_t)gj0 * a.sj;
+  const double* gdx = a.dx + moff;
+  const double* gdy = a.dy + moff;
+  const double* grdxa = a.rdxa + moff;
+  const double* grdya = a.rdya + moff;
   double* scrx = smem + L::o_crx;  // XW, origin (0, -3)
   double* sxfx = smem + L::o_xfx;
   double* scry = smem + L::o_cry;  // YW, origin (-4, 0)
@@ -128,6 +146,11 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
   auto SFY2 = [&](int q) { return SFX2(q) + L::n_mx; };                            // TI, origin (0, 0)
   auto FLX = [&](int q) { return smem + L::o_fl + q * L::n_fl; };                  // XW, origin (0, 0)
   auto FLY = [&](int q) { return FLX(q) + L::n_mx; };                              // TI, origin (0, 0)
+  auto D1 = [&](int q, int i, int j) { return smem + L::o_fl + q * L::n_d1 + (j + 2) * L::D1W + (i + 2); };
+  auto D2 = [&](int q, int i, int j) { return smem + L::o_d2 + q * L::n_d2 + (j + 1) * L::D2W + (i + 1); };
+  double* smwx = smem + L::o_mw;  // XW, origin (0, 0)
+  double* smwy = smwx + L::n_mx;  // TI, origin (0, 0)
+  const double damp4 = a.damp4, damp4h = a.damp4h;
   if (k1 > k0) mbar_wait(&bar[1], 0);
 
   // this thread's update cell
@@ -135,7 +158,7 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
   const bool own = gi < a.ni && gj < a.nj;
   const int64_t sj = a.sj, sk = a.sk;
   const int64_t coff = gi + gj * sj;
-  const double ra = own ? a.rarea[coff] : 0.0;
+  const double ra = *QB(srarea, ci, cj);
 
   constexpr int NSEG = TI / SEG;
   constexpr int NCY = TI + 6, NSY = TJ / SEG;  // phase-A y items: columns [-3, TI+3)
@@ -263,6 +286,41 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
         for (int q = 0; q < 3; ++q) phase_a(q, it);
     }
   };
+  // del6 order 1 of delp, pt, w at cell (i, j) (templates.delnflux):
+  // d2_0 = damp4 * delp (delp) or q itself (pt, w: mass-weighted chains),
+  // dfx_0 = del6_v * (d2_0[-1,0] - d2_0), d2_1 = div(dfx_0, dfy_0) * rarea
+  auto deln1 = [&](int e) {
+    const int i = e % L::D1W - 2, j = e / L::D1W - 2;
+    const double v0 = *QB(sd6v, i, j), v1 = *QB(sd6v, i + 1, j);
+    const double u0 = *QB(sd6u, i, j), u1 = *QB(sd6u, i, j + 1), rr = *QB(srarea, i, j);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double* Q = sdp + q * L::n_q;
+      double c = *QB(Q, i, j), wq = *QB(Q, i - 1, j), eq = *QB(Q, i + 1, j), sq = *QB(Q, i, j - 1), nq = *QB(Q, i, j + 1);
+      if (q == 0) {
+        c = damp4 * c;
+        wq = damp4 * wq;
+        eq = damp4 * eq;
+        sq = damp4 * sq;
+        nq = damp4 * nq;
+      }
+      const double fx0 = v0 * (wq - c), fx1 = v1 * (c - eq), fy0 = u0 * (sq - c), fy1 = u1 * (c - nq);
+      *D1(q, i, j) = (fx0 - fx1 + fy0 - fy1) * rr;
+    }
+  };
+  // del6 order 2: dfx_1 = del6_v * (d2_1 - d2_1[-1,0]), d2_2 = div(dfx_1, dfy_1) * rarea
+  auto deln2 = [&](int e) {
+    const int i = e % L::D2W - 1, j = e / L::D2W - 1;
+    const double v0 = *QB(sd6v, i, j), v1 = *QB(sd6v, i + 1, j);
+    const double u0 = *QB(sd6u, i, j), u1 = *QB(sd6u, i, j + 1), rr = *QB(srarea, i, j);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double c = *D1(q, i, j);
+      const double fx0 = v0 * (c - *D1(q, i - 1, j)), fx1 = v1 * (*D1(q, i + 1, j) - c);
+      const double fy0 = u0 * (c - *D1(q, i, j - 1)), fy1 = u1 * (*D1(q, i, j + 1) - c);
+      *D2(q, i, j) = (fx0 - fx1 + fy0 - fy1) * rr;
+    }
+  };
   // phase B of quantity q, item `it` (0 <= it < NB): weighted fluxes into FLX/FLY(q)
   auto phase_b = [&](int q, int it) {
     if (it < NX2) {
@@ -277,7 +335,10 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
         if (u < nf) {
           const int i = ib + u;
           const double w = q == 0 ? *CX(sxfx, i, rj) : FLX(0)[rj * L::XW + i];
-          out[rj * L::XW + i] = 0.5 * (f[u] + fx2[rj * L::XW + i]) * w;
+          // + dfx_2 = del6_v * (d2_2 - d2_2[-1,0]) (x damp4h * (delp[-1,0] + delp) for pt, w)
+          const double dd = *QB(sd6v, i, rj) * (*D2(q, i, rj) - *D2(q, i - 1, rj));
+          const double dinc = q == 0 ? dd : smwx[rj * L::XW + i] * dd;
+          out[rj * L::XW + i] = 0.5 * (f[u] + fx2[rj * L::XW + i]) * w + dinc;
         }
       }
     } else {
@@ -293,7 +354,9 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
         if (u < nf) {
           const int j = jb + u;
           const double w = q == 0 ? *CY(syfx, c, j) : FLY(0)[j * TI + c];
-          out[j * TI + c] = 0.5 * (f[u] + fy2[j * TI + c]) * w;
+          const double dd = *QB(sd6u, c, j) * (*D2(q, c, j) - *D2(q, c, j - 1));
+          const double dinc = q == 0 ? dd : smwy[j * TI + c] * dd;
+          out[j * TI + c] = 0.5 * (f[u] + fy2[j * TI + c]) * w + dinc;
         }
       }
     }
@@ -309,26 +372,36 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
     for (int e = tid; e < L::XW * L::XH; e += NT) {
       const int i = e % L::XW, j = e / L::XW - 3;
       const double uc = *QB(suc, i, j);
-      *CX(sxfx, i, j) = dt * uc * *QB(sdy, i, j);
-      *CX(scrx, i, j) = uc > 0.0 ? dt * uc * *QB(srdxa, i - 1, j) : dt * uc * *QB(srdxa, i, j);
+      const int64_t m = i + j * sj;
+      *CX(sxfx, i, j) = dt * uc * __ldg(gdy + m);
+      *CX(scrx, i, j) = uc > 0.0 ? dt * uc * __ldg(grdxa + m - 1) : dt * uc * __ldg(grdxa + m);
     }
     for (int e = tid; e < L::YW * L::YH; e += NT) {
       const int i = e % L::YW - 4, j = e / L::YW;
       const double vc = *QB(svc, i, j);
-      *CY(syfx, i, j) = dt * vc * *QB(sdx, i, j);
-      *CY(scry, i, j) = vc > 0.0 ? dt * vc * *QB(srdya, i, j - 1) : dt * vc * *QB(srdya, i, j);
+      const int64_t m = i + j * sj;
+      *CY(syfx, i, j) = dt * vc * __ldg(gdx + m);
+      *CY(scry, i, j) = vc > 0.0 ? dt * vc * __ldg(grdya + m - sj) : dt * vc * __ldg(grdya + m);
     }
+    for (int e = tid; e < L::D1W * L::D1H; e += NT) deln1(e);
     __syncthreads();
-    // ---- S1: phase A of delp, pt, w ------------------------------------------
+    // ---- S1: phase A of delp, pt, w; del6 order 2; mass weights ---------------
     for (int e = tid; e < NA; e += NT) phase_a3(e);
+    for (int e = tid; e < L::D2W * L::D2H; e += NT) deln2(e);
+    for (int e = tid; e < (TI + 1) * TJ; e += NT) {
+      const int i = e % (TI + 1), j = e / (TI + 1);
+      smwx[j * L::XW + i] = damp4h * (*QB(sdp, i - 1, j) + *QB(sdp, i, j));
+    }
+    for (int e = tid; e < TI * (TJ + 1); e += NT) {
+      const int i = e % TI, j = e / TI;
+      smwy[j * TI + i] = damp4h * (*QB(sdp, i, j - 1) + *QB(sdp, i, j));
+    }
     __syncthreads();
     // ---- S2: phase B of delp (mass fluxes); stage values of the update cell ---
     if (tid < NB) phase_b(0, tid);
     const double* spt = sdp + L::n_q;
     const double* sww = sdp + 2 * L::n_q;
     const double dp = *QB(sdp, ci, cj), ptc = *QB(spt, ci, cj), wc = *QB(sww, ci, cj);
-    const double wl = *QB(sww, ci - 1, cj), wr = *QB(sww, ci + 1, cj);
-    const double wsth = *QB(sww, ci, cj - 1), wnth = *QB(sww, ci, cj + 1);
     const double crx = *CX(scrx, ci, cj), cry = *CY(scry, ci, cj);
     const double xfx = *CX(sxfx, ci, cj), yfx = *CY(syfx, ci, cj);
     __syncthreads();
@@ -370,7 +443,7 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
           wq = (wc * dp + divw) / dn;
         }
         a.pto[off] = ptn;
-        a.wo[off] = wq + a.damp_w * (wl + wr + wsth + wnth - 4.0 * wc);
+        a.wo[off] = wq;
         // cx += crx, cy += cry, xfa += xfx, yfa += yfx, mfx += fxm, mfy += fym
         a.acco[0][off] = acc[0] + crx;
         a.acco[1][off] = acc[1] + cry;
@@ -380,6 +453,8 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
         a.acco[5][off] = acc[5] + fym0;
       }
     }
+    // the next level's d2_1 reuses the flux arrays this level's updates read
+    if (k + 1 < k1) __syncthreads();
   }
 }
 
@@ -399,11 +474,11 @@ int launch_dsw_transport(const DswTpArgs& a0, cudaStream_t st) {
 }
 
 int dsw_transport_maps(DswTpArgs& a, const Geo& g, const fv3b_field* qbox5, const fv3b_field* acc6,
-                       const fv3b_field* met5) {
+                       const fv3b_field* met4) {
   (void)acc6;
   using L = Dt2Layout<DT_TI, DT_TJ>;
   for (int f = 0; f < 5; ++f) FV3B_TRY(tensor_map(qbox5[f].data, g.pitch, g.rows, g.levels, L::QW, L::QH, &a.qbox[f]));
-  for (int f = 0; f < 5; ++f) FV3B_TRY(tensor_map(met5[f].data, g.pitch, g.rows, 1, L::QW, L::QH, &a.met[f]));
+  for (int f = 0; f < 4; ++f) FV3B_TRY(tensor_map(met4[f].data, g.pitch, g.rows, 1, L::QW, L::QH, &a.met[f]));
   return FV3B_OK;
 }
 

@@ -25,7 +25,8 @@ from .config import DIAG_3D, METRICS_2D, STATE_3D, RunConfig
 from .device import Grid
 
 C_METRICS = ("dx", "dy", "dxc", "dyc", "rdxc", "rdyc", "rarea", "rarea_c", "fc")
-D_METRICS = ("dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxa", "rdya", "area", "rarea", "rarea_c", "f0")
+D_METRICS = ("dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxa", "rdya", "area", "rarea", "rarea_c", "f0", "del6_u",
+             "del6_v")
 PINGPONG = ("u", "v", "w", "delp", "pt")
 ACCUM = ("cx", "cy", "xfa", "yfa", "mfx", "mfy")
 
@@ -345,8 +346,8 @@ class Dycore:
         if first:
             fields.append(self.f("dp1"))  # the step's dp1 = delp at the step start
         self.launch("d_sw", "fv3b_d_sw", fields,
-                    [c["ppm_p1"], c["ppm_p2"], dt, c["dddmp"], c["d2_bg"], c["da_min"], c["damp_w"],
-                     1.0 if first else 0.0], self.dom_layers)
+                    [c["ppm_p1"], c["ppm_p2"], dt, c["dddmp"], c["d2_bg"], c["da_min"], c["damp4"], c["damp4h"],
+                     c["dampv"], 1.0 if first else 0.0], self.dom_layers)
         self.swap(*PINGPONG)
 
     def nh_d(self) -> None:

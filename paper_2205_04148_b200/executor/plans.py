@@ -172,7 +172,8 @@ class RemapPlan(Plan):
 
 
 C_METRICS = ("dx", "dy", "dxc", "dyc", "rdxc", "rdyc", "rarea", "rarea_c", "fc")
-D_METRICS = ("dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxa", "rdya", "area", "rarea", "rarea_c", "f0")
+D_METRICS = ("dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxa", "rdya", "area", "rarea", "rarea_c", "f0", "del6_u",
+             "del6_v")
 D_STATE = ("u", "v", "w", "delp", "pt", "uc", "vc", "cx", "cy", "xfa", "yfa", "mfx", "mfy")
 D_OUT = ("u", "v", "w", "delp", "pt", "cx", "cy", "xfa", "yfa", "mfx", "mfy")
 
@@ -211,7 +212,8 @@ class DswPlan(Plan):
         s = prog.scalars(prog.trace[0][1])
         fields = [ctx.f(n) for n in D_STATE] + [ctx.f(m, 2) for m in D_METRICS] + [ctx.o(n) for n in D_OUT]
         ctx.call("d_sw_courant_0", "fv3b_d_sw", fields,
-                 [s["ppm_p1"], s["ppm_p2"], s["dt"], s["dddmp"], s["d2_bg"], s["da_min"], s["damp_w"]])
+                 [s["ppm_p1"], s["ppm_p2"], s["dt"], s["dddmp"], s["d2_bg"], s["da_min"], s["damp4"], s["damp4h"],
+                  s["dampv"]])
 
 
 class NhDPlan(Plan):

@@ -37,6 +37,7 @@ _PHYSICAL = {
     "rdx": (0.95e-4, 1.05e-4), "rdy": (0.95e-4, 1.05e-4), "rdxc": (0.95e-4, 1.05e-4), "rdyc": (0.95e-4, 1.05e-4),
     "area": (0.9e8, 1.1e8), "rarea": (0.9e-8, 1.1e-8), "rarea_c": (0.9e-8, 1.1e-8),
     "fc": (0.9e-4, 1.1e-4), "f0": (0.9e-4, 1.1e-4),
+    "del6_u": (0.9, 1.1), "del6_v": (0.9, 1.1),
     "cx": (-1.0, 1.0), "cy": (-1.0, 1.0), "xfa": (-1.0, 1.0), "yfa": (-1.0, 1.0),
     "mfx": (-1.0, 1.0), "mfy": (-1.0, 1.0),
 }

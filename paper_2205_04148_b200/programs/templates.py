@@ -65,13 +65,59 @@ def ppm_flux(axis: str, q: str, c: str, out: str, tag: str, q2d: bool = False) -
     ]
 
 
+def delnflux(q: str, tag: str, nord: int, damp: str, mass: str | None = None,
+             damp2: str | None = None) -> tuple[list[str], str, str]:
+    """FV3 ``deln_flux``: the del-(2 nord + 2) diffusive fluxes of ``q``
+    (nord = 0: del2, 1: del4, 2: del6), to be added to a transport flux.
+
+    ``d2`` starts as ``damp * q`` (or ``q`` when the fluxes are mass
+    weighted); each order takes the flux-form divergence (``rarea``) of the
+    previous face fluxes ``del6_v * (d2[-1] - d2)`` / ``del6_u * ...`` and
+    flips the difference, so the operator stays diffusive.  Returns the
+    statements and the (x, y) increments: ``dfx`` / ``dfy`` of the last
+    order, times ``damp2 * (mass[-1] + mass)`` when mass weighted.  Each
+    order has its own temporaries (minimal extensions, extents.py:128-164).
+    Grid copy of corner halos at cube vertices (FV3 copy_corners) is not
+    applied (DESIGN.md).
+    """
+    lines = []
+    d2 = q if mass is not None else f"d2_{tag}0"
+    if mass is None:
+        lines.append(f"{d2} = {damp} * {q}")
+    fx2, fy2 = f"dfx_{tag}0", f"dfy_{tag}0"
+    lines.append(f"{fx2} = del6_v * ({d2}[-1, 0, 0] - {d2})")
+    lines.append(f"{fy2} = del6_u * ({d2}[0, -1, 0] - {d2})")
+    for n in range(1, nord + 1):
+        d2 = f"d2_{tag}{n}"
+        lines.append(f"{d2} = ({fx2} - {fx2}[1, 0, 0] + {fy2} - {fy2}[0, 1, 0]) * rarea")
+        fx2, fy2 = f"dfx_{tag}{n}", f"dfy_{tag}{n}"
+        lines.append(f"{fx2} = del6_v * ({d2} - {d2}[-1, 0, 0])")
+        lines.append(f"{fy2} = del6_u * ({d2} - {d2}[0, -1, 0])")
+    if mass is None:
+        return lines, fx2, fy2
+    return lines, f"{damp2} * ({mass}[-1, 0, 0] + {mass}) * {fx2}", f"{damp2} * ({mass}[0, -1, 0] + {mass}) * {fy2}"
+
+
+def deln_coefficient(c: float, da_min: float, nord: int) -> float:
+    """FV3's damping coefficient (c * da_min) ** (nord + 1), as repeated
+    products (no pow; the value is a program constant and a kernel scalar)."""
+    x = c * da_min
+    d = x
+    for _ in range(nord):
+        d = d * x
+    return d
+
+
 def fv_tp_2d(q: str, crx: str, cry: str, xfx: str, yfx: str, fx: str, fy: str, tag: str,
-             mfx: str | None = None, mfy: str | None = None) -> list[str]:
+             mfx: str | None = None, mfy: str | None = None,
+             damp: tuple[str, str] | None = None) -> list[str]:
     """FV3 ``fv_tp_2d``: 2-D transport fluxes of ``q`` with the inner
     (advective) updates in both directions (Lin & Rood 1996).
 
     Produces ``fx`` (west faces) and ``fy`` (south faces); they are area
-    (``xfx``/``yfx``) or mass (``mfx``/``mfy``) weighted.
+    (``xfx``/``yfx``) or mass (``mfx``/``mfy``) weighted.  ``damp``: the
+    (x, y) flux increments of a ``delnflux`` chain, added in the same
+    statement (fv_tp_2d's nord / damp_c arguments).
     """
     qi, qj = f"qi_{tag}", f"qj_{tag}"
     fx1, fx2, fy1, fy2 = f"fx1_{tag}", f"fx2_{tag}", f"fy1_{tag}", f"fy2_{tag}"
@@ -86,8 +132,9 @@ def fv_tp_2d(q: str, crx: str, cry: str, xfx: str, yfx: str, fx: str, fy: str, t
     lines.append(f"{qj} = ({q} * area + {fx2} * {xfx} - {fx2}[1, 0, 0] * {xfx}[1, 0, 0]) / "
                  f"(area + {xfx} - {xfx}[1, 0, 0])")
     lines += ppm_flux("y", qj, cry, fy1, f"{tag}y1")
-    lines.append(f"{fx} = 0.5 * ({fx1} + {fx2}) * {wx}")
-    lines.append(f"{fy} = 0.5 * ({fy1} + {fy2}) * {wy}")
+    dx_, dy_ = (f" + {damp[0]}", f" + {damp[1]}") if damp else ("", "")
+    lines.append(f"{fx} = 0.5 * ({fx1} + {fx2}) * {wx}{dx_}")
+    lines.append(f"{fy} = 0.5 * ({fy1} + {fy2}) * {wy}{dy_}")
     return lines
 
 
@@ -466,11 +513,20 @@ def c_grid_program() -> str:
 # fv_tp_2d of delp (mass fluxes) / pt / w (mass weighted), vorticity and
 # kinetic energy, vorticity transport, Smagorinsky-scaled divergence
 # damping (the paper's Smagorinsky listing with sqrt instead of **,
-# PAPER.md:532-537), u/v update, and the tracer-flux accumulators.
+# PAPER.md:532-537), del6 flux damping (FV3 delnflux) of delp, pt, w and the
+# vorticity, u/v update, and the tracer-flux accumulators.
 # ---------------------------------------------------------------------------
 
-D_METRICS = ["dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxa", "rdya", "area", "rarea", "rarea_c", "f0"]
-D_CONSTS = [("dt", "15.0"), ("dddmp", "0.2"), ("d2_bg", "0.0"), ("da_min", "1.0e8"), ("damp_w", "0.02")]
+D_METRICS = ["dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxa", "rdya", "area", "rarea", "rarea_c", "f0",
+             "del6_u", "del6_v"]
+# flux damping (FV3 d_sw / fv_tp_2d nord, damp_c): del6 (nord = 2) on the
+# delp, pt and w fluxes (d4_bg) and on the vorticity flux (vtdm4)
+NORD = 2
+D4_BG, VTDM4, DA_MIN = 0.12, 0.05, 1.0e8
+DAMP4 = deln_coefficient(D4_BG, DA_MIN, NORD)
+DAMPV = deln_coefficient(VTDM4, DA_MIN, NORD)
+D_CONSTS = [("dt", "15.0"), ("dddmp", "0.2"), ("d2_bg", "0.0"), ("da_min", repr(DA_MIN)),
+            ("damp4", repr(DAMP4)), ("damp4h", repr(0.5 * DAMP4)), ("dampv", repr(DAMPV))]
 
 
 def d_sw_stencils() -> list:
@@ -480,10 +536,15 @@ def d_sw_stencils() -> list:
         "yfx = dt * vc * dx",
         "cry = select(vc > 0.0, dt * vc * rdya[0, -1], dt * vc * rdya)",
     ]
-    mass = fv_tp_2d("delp", "crx", "cry", "xfx", "yfx", "fxm", "fym", "d")
+    dmass, dmx, dmy = delnflux("delp", "d", NORD, "damp4")
+    mass = dmass + fv_tp_2d("delp", "crx", "cry", "xfx", "yfx", "fxm", "fym", "d", damp=(dmx, dmy))
     mass += ["delpn = delp + (fxm - fxm[1, 0, 0] + fym - fym[0, 1, 0]) * rarea"]
-    heat = fv_tp_2d("pt", "crx", "cry", "xfx", "yfx", "gxp", "gyp", "p", mfx="fxm", mfy="fym")
-    vert = fv_tp_2d("w", "crx", "cry", "xfx", "yfx", "hxw", "hyw", "w", mfx="fxm", mfy="fym")
+    dheat, dpx, dpy = delnflux("pt", "p", NORD, "damp4", mass="delp", damp2="damp4h")
+    heat = dheat + fv_tp_2d("pt", "crx", "cry", "xfx", "yfx", "gxp", "gyp", "p", mfx="fxm", mfy="fym",
+                            damp=(dpx, dpy))
+    dvert, dwx, dwy = delnflux("w", "w", NORD, "damp4", mass="delp", damp2="damp4h")
+    vert = dvert + fv_tp_2d("w", "crx", "cry", "xfx", "yfx", "hxw", "hyw", "w", mfx="fxm", mfy="fym",
+                            damp=(dwx, dwy))
     ke = [
         "ub = 0.5 * dt * (uc[0, -1, 0] + uc)",
         "cub = select(ub > 0.0, ub * rdx[-1, 0], ub * rdx)",
@@ -494,7 +555,8 @@ def d_sw_stencils() -> list:
         "ked = 0.5 * (ub * uu + vb * vv)",
     ]
     vort = ["wk = f0 + rarea * (u * dx - u[0, 1, 0] * dx[0, 1] + v[1, 0, 0] * dy[1, 0] - v * dy)"]
-    vort += fv_tp_2d("wk", "crx", "cry", "xfx", "yfx", "fxv", "fyv", "v")
+    dvort, dvx, dvy = delnflux("wk", "v", NORD, "dampv")
+    vort += dvort + fv_tp_2d("wk", "crx", "cry", "xfx", "yfx", "fxv", "fyv", "v", damp=(dvx, dvy))
     damp = [
         "divg = rarea_c * (u * dyc - u[-1, 0, 0] * dyc[-1, 0] + v * dxc - v[0, -1, 0] * dxc[0, -1])",
         "tens = rarea_c * (u * dyc - u[-1, 0, 0] * dyc[-1, 0] - v * dxc + v[0, -1, 0] * dxc[0, -1])",
@@ -510,8 +572,7 @@ def d_sw_stencils() -> list:
         "mfx = mfx + fxm",
         "mfy = mfy + fym",
         "pt = (pt * delp + (gxp - gxp[1, 0, 0] + gyp - gyp[0, 1, 0]) * rarea) / delpn",
-        "w = (w * delp + (hxw - hxw[1, 0, 0] + hyw - hyw[0, 1, 0]) * rarea) / delpn + "
-        "damp_w * (w[-1, 0, 0] + w[1, 0, 0] + w[0, -1, 0] + w[0, 1, 0] - 4.0 * w)",
+        "w = (w * delp + (hxw - hxw[1, 0, 0] + hyw - hyw[0, 1, 0]) * rarea) / delpn",
         "delp = delpn",
         "u = (u * dx + ked - ked[1, 0, 0] + fyv) * rdx + (ddv[1, 0, 0] - ddv) * rdx",
         "v = (v * dy + ked - ked[0, 1, 0] - fxv) * rdy + (ddv[0, 1, 0] - ddv) * rdy",

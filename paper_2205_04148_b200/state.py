@@ -35,7 +35,8 @@ def initial_state(cfg: RunConfig) -> dict[str, np.ndarray]:
     L = nk + 1
     st: dict[str, np.ndarray] = {}
     # metrics (uniform, exact reciprocals)
-    for n, v in {"dx": DX, "dy": DX, "dxc": DX, "dyc": DX, "area": DX * DX, "f0": 1.0e-4, "fc": 1.0e-4}.items():
+    for n, v in {"dx": DX, "dy": DX, "dxc": DX, "dyc": DX, "area": DX * DX, "f0": 1.0e-4, "fc": 1.0e-4,
+                 "del6_u": 1.0, "del6_v": 1.0}.items():  # del6_u = sin_sg dx / dyc, del6_v = sin_sg dy / dxc
         st[n] = np.full((I, J), v)
     for n, v in {"rdx": 1.0 / DX, "rdy": 1.0 / DX, "rdxc": 1.0 / DX, "rdyc": 1.0 / DX, "rdxa": 1.0 / DX,
                  "rdya": 1.0 / DX, "rarea": 1.0 / (DX * DX), "rarea_c": 1.0 / (DX * DX), "ws": 0.0}.items():

@@ -41,6 +41,7 @@ CASES = [
     ("c_sw", "tile", (13, 14, 2), (True, True, True, True), 8),
     ("c_grid", "tile", (13, 12, 5), (True, True, True, True), 7),
     ("d_sw", "periodic", (17, 16, 2), (False, False, False, False), 7),
+    ("d_sw", "tile", (16, 17, 2), (True, True, True, True), 9),
     ("nh_d", "column", (5, 4, 17), (True, True, True, True), 7),
     ("p_grad_d", "periodic", (7, 6, 5), (False, False, False, False), 7),
 ]
