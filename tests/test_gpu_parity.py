@@ -126,5 +126,13 @@ def test_timing_api(engine):
 
 
 def test_measure_bandwidth(engine):
-    bw = engine.measure_bandwidth()
-    assert bw > 3.0e12, f"copy-stencil bandwidth {bw / 1e9:.0f} GB/s"
+    """SPEC.md:392-400 / the minimum-slice bar: the copy stencil at >= 0.9 of
+    the measured HBM copy peak (MEASURED_PEAKS.json, driver-written; else the
+    6544 GB/s measured on this pool)."""
+    import json
+    from pathlib import Path
+
+    peaks = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
+    peak = json.loads(peaks.read_text())["hbm_gbs"] * 1e9 if peaks.exists() else 6544e9
+    bw = max(engine.measure_bandwidth(1024 * 2**20) for _ in range(2))
+    assert bw >= 0.9 * peak, f"copy-stencil bandwidth {bw / 1e9:.0f} GB/s < 0.9 x {peak / 1e9:.0f} GB/s"
