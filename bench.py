@@ -289,6 +289,18 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     e2e_ms = e0.elapsed_time(e1) / args.steps
     io_bytes = sum(t.numel() * t.element_size() for t in h_in.values())
     assert all(bool(torch.isfinite(t).all()) for t in h_out.values()), "non-finite state after the e2e steps"
+    # chained integration: every step's input is the previous step's output,
+    # so a step's uploads wait for the previous downloads (no cross-step overlap)
+    h_a, h_b = h_in, h_out
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        done = d.step_host(h_a, h_b)
+        h_a, h_b = h_b, h_a
+    stream.wait_event(done)
+    e1.record(stream)
+    barrier()
+    e2e_chained_ms = e0.elapsed_time(e1) / args.steps
 
     # per-launch device times: the same K steps eagerly with events around
     # every libfv3b launch on the launching stream
@@ -311,6 +323,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
 
     ms = reduce_max(ms)
     e2e_ms = reduce_max(e2e_ms)
+    e2e_chained_ms = reduce_max(e2e_chained_ms)
     if rank != 0:
         return
 
@@ -374,18 +387,25 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                            ("peer-memory stores over CUDA IPC + device barriers" if args.halo == "peer" else "NCCL send/recv"),
                    "timing": ("CUDA-graph replay of whole timesteps" if graphs else "eager launches, NCCL halo exchange") + ", CUDA events, max over ranks"},
         "e2e": {"value": cells / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes},
+                "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
+                "mode": "pipelined: the same host input every step, so step n+1's uploads overlap step n",
+                "chained": {"value": cells / (e2e_chained_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_chained_ms,
+                            "mode": "each step's input is the previous step's output (uploads wait for the downloads)"}},
         "gpu_launches": kernels_per_step(cfg) * args.steps,
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "algo_bytes_per_launch": algo,
                      "mean_launch_s": mean_launch, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)",
                      "algo_bytes_source": by[top].source,
+                     "movement_model_bytes_per_launch": perf_model.movement_bytes(top, doms[top]),
                      "step_algo_bytes": step_bytes, "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak},
         "fp64_roofline": fp64,
         "report": {e.kernel: {"invocations_per_step": e.invocations // args.steps,
                               "measured_us": round(e.measured_time * 1e6, 2),
                               "bound_us": round(e.bound_time * 1e6, 2),
-                              "utilization": round(e.utilization, 4)} for e in report.entries},
+                              "utilization": round(e.utilization, 4),
+                              "first_touch_bytes": e.unique_bytes,
+                              "movement_model_bytes": perf_model.movement_bytes(e.kernel, doms[e.kernel])}
+                   for e in report.entries},
         "hotspots": perf_model.hotspot_list(report, 3),
         "kernels_ms_per_step": {n: round(v * 1e3 / args.steps, 4) for n, v in
                                 sorted(node_total.items(), key=lambda x: -x[1])},

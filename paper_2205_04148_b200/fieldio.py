@@ -6,7 +6,7 @@ array convention (axes in declared I, J, K order, C order) as raw binary,
 plus a ``<path>.json`` sidecar with the field name, element type, shape and
 the reference ``Layout`` (``scheduling.py:323-407``) of the field; text mode
 writes one value per line after a header.  Files written here load with the
-reference's ``load_field`` and vice versa (tests/test_fieldio.py).
+reference's ``load_field`` and vice versa (tests/test_perf_model.py).
 
 ``save_state`` / ``load_state`` checkpoint a :class:`~.dycore.Dycore` (every
 state field, one file each, plus ``run.json`` with the run configuration) —

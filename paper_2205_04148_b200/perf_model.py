@@ -58,6 +58,21 @@ def unique_bytes(program: str, domain) -> tuple[int, str]:
     return int(compulsory_bytes(program, tuple(domain))), "box model (upper bound)"
 
 
+def movement_bytes(program: str, domain) -> dict | None:
+    """The reference's per-node movement model of one launch (the paper's
+    method: ``trace_movement(lower(program))``, reference
+    ir/movement.py:64-74), committed in ``traffic_table.json`` by
+    tools/traffic_table.py: all containers (every stencil node an unfused
+    kernel) and the non-transient ones.  None when not tabulated."""
+    if not _TABLE.exists() or len(domain) != 3:
+        return None
+    row = json.loads(_TABLE.read_text()).get(f"{program}@{domain[0]}x{domain[1]}x{domain[2]}", {})
+    if "movement_model_bytes" not in row:
+        return None
+    return {"all_containers": int(row["movement_model_bytes"]),
+            "non_transient": int(row["movement_model_nontransient_bytes"])}
+
+
 @dataclass
 class KernelBound:
     kernel: str
