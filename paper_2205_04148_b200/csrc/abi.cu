@@ -65,8 +65,8 @@ int check_launch(const char* what) {
 // Launch-configuration knobs, SM count, per-device shared-memory attributes.
 // ---------------------------------------------------------------------------
 #include <atomic>
+#include <map>
 #include <mutex>
-#include <set>
 #include <utility>
 
 namespace fv3b {
@@ -89,15 +89,19 @@ int num_sms() {
 }
 
 int ensure_smem(const void* fn, size_t bytes, const char* what) {
+  // the largest size set so far per (kernel, device): a kernel whose dynamic
+  // shared memory depends on the call (the column solvers: levels) raises it
   static std::mutex mu;
-  static std::set<std::pair<const void*, int>> done;
+  static std::map<std::pair<const void*, int>, size_t> done;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
-  if (done.count({fn, dev})) return FV3B_OK;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+  auto it = done.find({fn, dev});
+  if (it != done.end() && it->second >= bytes) return FV3B_OK;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess ||
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
     return check_launch(what);
-  done.insert({fn, dev});
+  done[{fn, dev}] = bytes;
   return FV3B_OK;
 }
 
