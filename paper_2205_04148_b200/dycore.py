@@ -46,8 +46,14 @@ class PeriodicHalo:
 
 class Dycore:
     def __init__(self, cfg: RunConfig, state: dict[str, np.ndarray] | None = None, device: str = "cuda",
-                 placement=(False, False, False, False), halo=None):
+                 placement=(False, False, False, False), halo=None, tuned: bool = True):
+        """``tuned``: apply the launch configuration tools/tune.py recorded
+        for this device and shape (tuning.json), process-wide."""
         self.cfg = cfg
+        if tuned and device != "cpu" and torch.cuda.is_available():
+            from . import tuning
+
+            self.tuning = tuning.apply(torch.cuda.get_device_name(), (cfg.ni, cfg.nj, cfg.nk))
         self.device = device
         self.grid = Grid(cfg.ni, cfg.nj, cfg.nk, halo=cfg.halo)
         self.placement = placement

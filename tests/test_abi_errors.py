@@ -77,3 +77,18 @@ def test_tuning_knobs_roundtrip(lib):
     assert lib.fv3b_tune_set(0, -1) < 0
     assert lib.fv3b_tune_get(99) == -1
     assert set(_lib.TUNE.values()) == set(range(len(_lib.TUNE)))
+
+
+def test_tuning_table_roundtrip(tmp_path, monkeypatch, lib):
+    """tuning.record / apply: knobs of the matching (device, shape) entry only."""
+    from paper_2205_04148_b200 import tuning
+
+    monkeypatch.setattr(tuning, "PATH", tmp_path / "tuning.json")
+    tuning.record("GPU X", (192, 192, 80), {"knobs": {"kchunk_csw": 20}})
+    assert tuning.lookup("GPU X", (192, 192, 80)) == {"kchunk_csw": 20}
+    assert tuning.apply("GPU Y", (192, 192, 80)) == {}
+    try:
+        assert tuning.apply("GPU X", (192, 192, 80)) == {"kchunk_csw": 20}
+        assert _lib.tune_get("kchunk_csw") == 20
+    finally:
+        _lib.tune_set("kchunk_csw", 0)
