@@ -300,7 +300,9 @@ def _structure_fp(canon: dict) -> str:
     """Fingerprint of fields + stencil blocks, without stencil parameter
     lists (a lowered graph does not carry them)."""
     st = [{"name": s["name"], "blocks": s["blocks"]} for s in canon["stencils"]]
-    doc = json.dumps({"fields": canon["fields"], "stencils": st}, sort_keys=True)
+    # (field catalogue by name: graph documents list arrays sorted, serialize.py:171-186)
+    fields = sorted(canon["fields"], key=lambda f: f["name"])
+    doc = json.dumps({"fields": fields, "stencils": st}, sort_keys=True)
     return hashlib.sha256(doc.encode()).hexdigest()[:16]
 
 

@@ -136,3 +136,18 @@ def test_measure_bandwidth(engine):
     peak = json.loads(peaks.read_text())["hbm_gbs"] * 1e9 if peaks.exists() else 6544e9
     bw = max(engine.measure_bandwidth(1024 * 2**20) for _ in range(2))
     assert bw >= 0.9 * peak, f"copy-stencil bandwidth {bw / 1e9:.0f} GB/s < 0.9 x {peak / 1e9:.0f} GB/s"
+
+
+@pytest.mark.parametrize("name,domain", [("d_sw", (48, 40, 6)), ("c_grid", (37, 21, 9)), ("tracer_2d", (32, 32, 4))])
+def test_graph_document_runs_on_b200(engine, name, domain):
+    """A persisted graph document (graphio, the reference's stencilkit-graph
+    format) executes on the B200 engine bitwise like the program."""
+    from paper_2205_04148_b200 import graphio
+    from paper_2205_04148_b200.inputs import synthetic_inputs
+
+    placement = (False, True, False, True)
+    g = graphio.graph_from_json(graphio.graph_to_json(graphio.program_graph(name, domain, placement)))
+    inputs = synthetic_inputs(name, domain, 9)
+    got = engine.run_b200(g, inputs, domain, placement=placement)
+    ref = interp.run_program(name, inputs, domain, interp.Placement(*placement))
+    assert_outputs_equal(got, ref)
