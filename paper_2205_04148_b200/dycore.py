@@ -71,6 +71,7 @@ class Dycore:
         self.coord = {"ak": torch.from_numpy(ak).to(device), "bk": torch.from_numpy(bk).to(device)}
         self.halo = halo or PeriodicHalo(self)
         self.stream = None
+        self.overlap = False  # halo exchanges on their own stream (step_overlapped)
         self.launches = 0
         self.timer = None
         self._graphs: dict[tuple, tuple] = {}
@@ -460,9 +461,82 @@ class Dycore:
             self.halo.update(names)
 
     def step(self) -> None:
-        """Enqueue one full timestep on the current stream."""
+        """Enqueue one full timestep on the current stream (with
+        ``self.overlap``: halo exchanges on a second stream, see
+        :meth:`step_overlapped`)."""
+        if self.overlap:
+            self.step_overlapped()
+            return
         for names in self.phases():
             self.halo.update(names)
+
+    # -- halo exchanges overlapped with compute ----------------------------------
+
+    def _comm(self) -> torch.cuda.Stream:
+        if getattr(self, "_comm_stream", None) is None:
+            self._comm_stream = torch.cuda.Stream()
+        return self._comm_stream
+
+    def _start(self, names) -> torch.cuda.Event:
+        """Start the halo update of ``names`` on the exchange stream once the
+        compute stream has produced them; returns its completion event."""
+        comm = self._comm()
+        comm.wait_event(torch.cuda.current_stream().record_event())
+        with torch.cuda.stream(comm):
+            self.halo.update(list(names))
+        return comm.record_event()
+
+    @staticmethod
+    def _wait(*events) -> None:
+        for e in events:
+            if e is not None:
+                torch.cuda.current_stream().wait_event(e)
+
+    def step_overlapped(self) -> None:
+        """One timestep whose halo exchanges run on a second stream (SURVEY
+        8(e): the halo moves under compute).  Each field group's exchange
+        starts as soon as its producer has run and is waited for only by the
+        program that reads the halo, so a group whose next reader is not the
+        next program moves under the programs in between:
+
+        * the tracers (q*, unchanged by the acoustic substeps) from the step
+          start, under every substep, until tracer_2d;
+        * w, delp, pt (final after d_sw / nh_d) under p_grad_d, until the
+          next substep's c_grid; u, v after p_grad_d;
+        * the flux accumulators and delp after the last d_sw / nh_d, under
+          the last p_grad_d, until tracer_2d.
+        gz is refreshed with pef after nh_d (p_grad_d and the next c_grid
+        read it; nothing in between writes it), and every group is exchanged
+        exactly when the plain step's halo points would leave it fresh, so
+        the results are bitwise those of :meth:`step` (tests)."""
+        cfg = self.cfg
+        tracers = cfg.tracer_names()
+        dyn = [self._start(["u", "v", "w", "delp", "pt", "gz"])]
+        ev_trc = self._start(tracers) if tracers else None
+        ev_acc = None
+        for it in range(cfg.n_split):
+            last = it == cfg.n_split - 1
+            self._wait(*dyn)
+            self.c_grid()
+            self._wait(self._start(["uc", "vc"]))
+            self.d_sw(first=it == 0)
+            self.nh_d()
+            ev_p = self._start(["pef", "gz"])
+            if last:
+                ev_acc = self._start(list(ACCUM) + ["delp"])
+            else:
+                dyn = [self._start(["w", "delp", "pt"])]
+            self._wait(ev_p)
+            self.p_grad_d()
+            if not last:
+                dyn.append(self._start(["u", "v"]))
+        self._wait(ev_trc, ev_acc)
+        self.tracer_2d()
+        self.remap()
+        self.remap_map()
+        self.moist_pk()
+        # the exchange stream joins the compute stream (graph capture, next step)
+        self._wait(self._comm().record_event())
 
     # -- CUDA graphs ---------------------------------------------------------
 
