@@ -204,40 +204,114 @@ class LaunchTimer:
         return out
 
 
-def run_ours(args, rank: int, world: int, local: int) -> None:
-    import torch
-    import torch.distributed as dist
+class Setup:
+    """What one rank runs for a bench config: ``runner`` (step / capture /
+    replay: a Dycore, or a LoopbackCluster of cube tiles), its Dycores,
+    the job's cells per step and the line's config fields."""
 
-    from paper_2205_04148_b200 import _lib
+    def __init__(self, runner, dycores, cells_job, scaling, workload, decomposition, halo, graphs, sync=None):
+        self.runner, self.dycores, self.cells_job = runner, dycores, cells_job
+        self.scaling, self.workload, self.decomposition, self.halo = scaling, workload, decomposition, halo
+        self.graphs, self.sync = graphs, sync
+
+
+def setup_config(args, rank: int, world: int) -> Setup:
+    """C2 (default): 192x192x80 per rank, px x py weak scaling.  C4: the
+    768x768x80 domain split px x py (strong scaling: 768x384, 384x384,
+    384x192 blocks at 2, 4, 8 ranks).  C3: the C128 L80 cubed sphere, one
+    FULL_TILE tile per rank at 6 ranks, or all six tiles on one GPU
+    (LoopbackCluster).  Every block starts from the synthetic state of its
+    own shape (state.py): the same work per cell as the global field's
+    block."""
     from paper_2205_04148_b200.config import RunConfig
-    from paper_2205_04148_b200.dycore import Dycore, kernels_per_step
-    from paper_2205_04148_b200.parallel import DecomposedHalo, HaloPlan, IpcPeers, PeerHalo, grid_shape, new_flags
+    from paper_2205_04148_b200.dycore import Dycore
+    from paper_2205_04148_b200.parallel import (DecomposedHalo, HaloPlan, IpcPeers, LoopbackCluster, PeerHalo,
+                                                grid_shape, new_flags)
     from paper_2205_04148_b200.state import initial_state
-    from paper_2205_04148_b200 import perf_model
 
-    torch.cuda.set_device(local)
-    _lib.lib()  # no CPU fallback: fail loudly if the library is missing
-    cfg = RunConfig(ni=args.ni, nj=args.ni, nk=args.nk)
+    if args.config == "c3":
+        from paper_2205_04148_b200.cubesphere import CubeHalo, CubePeerHalo, topology
+
+        n, nk = args.c3_n, args.nk
+        cfg = RunConfig(ni=n, nj=n, nk=nk)
+        workload = f"C3 cubed sphere C{n} L{nk}, 6 FULL_TILE tiles, edge rotation + corner fill (n_split=6, nq=8)"
+        if world == 1:
+            tiles = [Dycore(cfg, initial_state(RunConfig(ni=n, nj=n, nk=nk, seed=2205 + t)), placement=(True,) * 4)
+                     for t in range(6)]
+            cl = LoopbackCluster(tiles, halos=[CubeHalo(d, t, transport=None) for t, d in enumerate(tiles)])
+            return Setup(cl, tiles, 6 * cfg.cells, "strong", workload, "6 tiles on 1 GPU",
+                         "cube rotation + corner fill, device copies (loopback)", True)
+        if world != 6:
+            raise SystemExit("--config c3 runs on 1 GPU (six tiles) or 6 ranks (one tile each)")
+        d = Dycore(cfg, initial_state(RunConfig(ni=n, nj=n, nk=nk, seed=2205 + rank)), placement=(True,) * 4)
+        sync = None
+        if args.halo == "peer":
+            nbrs = sorted({x.nb for x in topology()[rank].values()})
+            ipc = IpcPeers(d, None, neighbours=nbrs, rank=rank, flags=new_flags(world, "cuda"))
+            sync = ipc.flag_sync()
+            d.halo = CubePeerHalo(d, rank, ipc.tiles(), sync=sync)
+            halo = "cube rotation + corner fill by peer-memory stores (CUDA IPC) + device barriers"
+        else:
+            d.halo = CubeHalo(d, rank)
+            halo = "cube rotation + corner fill over NCCL send/recv"
+        return Setup(d, [d], 6 * cfg.cells, "strong", workload, "6 tiles on 6 GPUs", halo, args.halo == "peer", sync)
+
     px, py = grid_shape(world)
-    state = initial_state(cfg)
-    d = Dycore(cfg, state)
+    if args.config == "c4":
+        N = args.c4_n
+        if N % px or N % py:
+            raise SystemExit(f"--config c4: {N} does not split {px}x{py}")
+        cfg = RunConfig(ni=N // px, nj=N // py, nk=args.nk)
+        cells_job, scaling = N * N * args.nk, "strong"
+        workload = f"C4 doubly periodic {N}x{N}x{args.nk} fp64 dycore timestep split {px}x{py} (n_split=6, nq=8)"
+    else:
+        cfg = RunConfig(ni=args.ni, nj=args.ni, nk=args.nk)
+        cells_job, scaling = cfg.cells * world, "weak"
+        workload = (f"C2 doubly periodic {args.ni}x{args.ni}x{args.nk} fp64 dycore timestep per GPU "
+                    f"(n_split=6, nq=8)")
+    d = Dycore(cfg, initial_state(cfg))
+    sync = None
     if world > 1 and args.halo == "peer":
         # halos stored straight into the neighbours' buffers (CUDA IPC over
         # NVLink, fv3b_halo_peer_rects) behind device-side neighbour
         # barriers (fv3b_peer_barrier): no host sync, so whole steps replay
         # as CUDA graphs on every rank
         peers = IpcPeers(d, HaloPlan(cfg.ni, cfg.nj, cfg.halo, px, py, rank), flags=new_flags(world, "cuda"))
-        d.halo = PeerHalo(d, px, py, rank, peers, sync=peers.flag_sync())
+        sync = peers.flag_sync()
+        d.halo = PeerHalo(d, px, py, rank, peers, sync=sync)
+        halo = "peer-memory stores over CUDA IPC + device barriers"
     elif world > 1:
-        # every rank owns one 192x192x80 block of a (px*192) x (py*192)
-        # doubly periodic domain; halos move over NCCL (grouped send/recv)
+        # every rank owns one block of a (px ni) x (py nj) doubly periodic
+        # domain; halos move over NCCL (grouped send/recv)
         d.halo = DecomposedHalo(d, px, py, rank)
-    d.overlap = args.overlap == "on" or (args.overlap == "auto" and world > 1)
+        halo = "NCCL send/recv"
+    else:
+        halo = "periodic kernel"
+    return Setup(d, [d], cells_job, scaling, workload, f"{px}x{py}", halo, world == 1 or args.halo == "peer", sync)
+
+
+def run_ours(args, rank: int, world: int, local: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_04148_b200 import _lib
+    from paper_2205_04148_b200.dycore import kernels_per_step
+    from paper_2205_04148_b200 import perf_model
+
+    torch.cuda.set_device(local)
+    _lib.lib()  # no CPU fallback: fail loudly if the library is missing
+    su = setup_config(args, rank, world)
+    runner, dycores = su.runner, su.dycores
+    d = dycores[0]
+    cfg = d.cfg
+    overlap = args.overlap == "on" or (args.overlap == "auto" and world > 1)
+    for x in dycores:
+        x.overlap = overlap and len(dycores) == 1
     torch.cuda.synchronize()
-    # single rank and peer halos: whole timesteps replayed as CUDA graphs;
-    # NCCL halos: eager launches (the exchanges stay outside graph capture)
-    graphs = world == 1 or args.halo == "peer"
-    run_step = d.replay if graphs else d.step
+    # single rank, loopback clusters and peer halos: whole timesteps replayed
+    # as CUDA graphs; NCCL halos: eager launches (exchanges outside capture)
+    graphs = su.graphs
+    run_step = runner.replay if graphs else runner.step
 
     def barrier():
         if world > 1:
@@ -245,9 +319,9 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         torch.cuda.synchronize()
 
     # warm-up (eager, then capture and replay)
-    d.step()
+    runner.step()
     if graphs:
-        d.capture()
+        runner.capture()
     for _ in range(max(args.warmup, 3)):
         run_step()
     barrier()
@@ -264,39 +338,54 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         barrier()
     ms = t0.elapsed_time(t1) / args.steps
     clocks = clk.summary()
-    if world > 1 and args.halo == "peer":
-        d.halo.sync.check()  # a timed-out neighbour barrier voids the run instead of reporting it
+    if su.sync is not None:
+        su.sync.check()  # a timed-out neighbour barrier voids the run instead of reporting it
 
-    # end to end: pinned host state in, step, host state out (Dycore.step_host:
-    # uploads and downloads on their own streams, the tracers' uploads overlap
-    # the acoustic substeps, the dynamics fields' downloads overlap tracer
-    # advection and remapping, and successive steps pipeline: step n+1's
-    # uploads and step n-1's downloads run under step n's compute)
-    h_in = d.host_buffers()
-    h_out = d.host_buffers()
-    for n, t in h_in.items():
-        t.copy_(torch.from_numpy(state[n]))
-    d.step_host(h_in, h_out)
+    # end to end: pinned host state in, step, host state out.  One Dycore:
+    # Dycore.step_host (uploads and downloads on their own streams, the
+    # tracers' uploads overlap the acoustic substeps, the dynamics fields'
+    # downloads overlap tracer advection and remapping, successive steps
+    # pipeline).  A cube cluster: every tile's upload, the lockstep step,
+    # every tile's download, in stream order.
+    from paper_2205_04148_b200.state import initial_state as _init
+    h_in = [x.host_buffers() for x in dycores]
+    h_out = [x.host_buffers() for x in dycores]
+    for x, hb in zip(dycores, h_in):
+        st0 = _init(x.cfg)
+        for n, t in hb.items():
+            t.copy_(torch.from_numpy(st0[n]))
+
+    def e2e_step(hi, ho):
+        if len(dycores) == 1:
+            return dycores[0].step_host(hi[0], ho[0])
+        for x, hb in zip(dycores, hi):
+            x.load_host(hb)
+        runner.step()
+        for x, hb in zip(dycores, ho):
+            x.store_host(hb)
+        return torch.cuda.current_stream().record_event()
+
+    e2e_step(h_in, h_out)
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
     e0.record(stream)
     for _ in range(args.steps):
-        done = d.step_host(h_in, h_out)
+        done = e2e_step(h_in, h_out)
     stream.wait_event(done)  # the last step's downloads are inside the timed region
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1) / args.steps
-    io_bytes = sum(t.numel() * t.element_size() for t in h_in.values())
-    assert all(bool(torch.isfinite(t).all()) for t in h_out.values()), "non-finite state after the e2e steps"
+    io_bytes = sum(t.numel() * t.element_size() for hb in h_in for t in hb.values())
+    assert all(bool(torch.isfinite(t).all()) for hb in h_out for t in hb.values()), "non-finite state after e2e"
     # chained integration: every step's input is the previous step's output,
     # so a step's uploads wait for the previous downloads (no cross-step overlap)
     h_a, h_b = h_in, h_out
     barrier()
     e0.record(stream)
     for _ in range(args.steps):
-        done = d.step_host(h_a, h_b)
+        done = e2e_step(h_a, h_b)
         h_a, h_b = h_b, h_a
     stream.wait_event(done)
     e1.record(stream)
@@ -305,15 +394,19 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
 
     # per-launch device times: the same K steps eagerly with events around
     # every libfv3b launch on the launching stream
-    d.timer = LaunchTimer()
-    d.launches = 0
+    timer = LaunchTimer()
+    for x in dycores:
+        x.timer, x.launches = timer, 0
     barrier()
+    for x in dycores:
+        x.load(_init(x.cfg))
     for _ in range(args.steps):
-        d.step()
+        runner.step()
     barrier()
-    eager_launches = d.launches
-    per_node = d.timer.per_node()
-    d.timer = None
+    eager_launches = sum(x.launches for x in dycores)
+    per_node = timer.per_node()
+    for x in dycores:
+        x.timer = None
 
     def reduce_max(x: float) -> float:
         if world == 1:
@@ -328,7 +421,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     if rank != 0:
         return
 
-    cells = cfg.cells * world
+    cells = su.cells_job
     value = cells / (ms * 1e-3)
     node_total = {n: sum(v) for n, v in per_node.items()}
     # the Fig. 10 model-augmented report (perf_model): first-touch compulsory
@@ -373,27 +466,25 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                 "source": "ncu op counts (profiles/fp64.json) / CUDA-event launch time; peak: "
                           "tools/fp64_probe.cu DFMA issue (profiles/fp64_probe.txt)"}
     cpu = None
-    if not args.no_cpu and world == 1:
+    if not args.no_cpu and world == 1 and args.config == "c2":
         v, cores, sample = cpu_run(1)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": su.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded analytic state, state.py)",
-        "config": {"workload": "C2 doubly periodic 192x192x80 fp64 dycore timestep (n_split=6, nq=8)",
+        "config": {"workload": su.workload, "name": args.config,
                    "ni": cfg.ni, "nj": cfg.nj, "nk": cfg.nk, "n_split": cfg.n_split, "nq": cfg.nq,
-                   "decomposition": f"{px}x{py}", "l2": "state 1.3 GB/GPU > 126 MB L2 (no flush)",
-                   "halo": "periodic kernel" if world == 1 else
-                           ("peer-memory stores over CUDA IPC + device barriers" if args.halo == "peer" else "NCCL send/recv"),
-                   "halo_overlap": d.overlap,
+                   "decomposition": su.decomposition, "l2": "state > 126 MB L2 per GPU (no flush)",
+                   "halo": su.halo, "halo_overlap": overlap and len(dycores) == 1,
                    "timing": ("CUDA-graph replay of whole timesteps" if graphs else "eager launches, NCCL halo exchange") + ", CUDA events, max over ranks"},
         "e2e": {"value": cells / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
                 "mode": "pipelined: the same host input every step, so step n+1's uploads overlap step n",
                 "chained": {"value": cells / (e2e_chained_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_chained_ms,
                             "mode": "each step's input is the previous step's output (uploads wait for the downloads)"}},
-        "gpu_launches": kernels_per_step(cfg) * args.steps,
+        "gpu_launches": kernels_per_step(cfg) * args.steps * len(dycores),
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "algo_bytes_per_launch": algo,
                      "mean_launch_s": mean_launch, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)",
@@ -424,6 +515,11 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=("c2", "c3", "c4"), default="c2",
+                    help="c2: 192x192x80 per GPU (weak scaling, the BASELINE metric's workload); c3: the C128 L80 "
+                         "cubed sphere (1 GPU: six tiles; 6 GPUs: a tile each); c4: 768x768x80 split over the GPUs")
+    ap.add_argument("--c3-n", type=int, default=128)
+    ap.add_argument("--c4-n", type=int, default=768)
     ap.add_argument("--ni", type=int, default=192)
     ap.add_argument("--nk", type=int, default=80)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
