@@ -215,3 +215,81 @@ def test_ipc_peer_halo_two_ranks(px, py):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+# ---------------------------------------------------------------------------
+# a decomposed timestep across two gloo processes (the oracle programs on each
+# rank's block, DecomposedHalo + DistTransport at every halo point) against
+# the single-domain oracle step
+# ---------------------------------------------------------------------------
+
+class _NumpyGrid:
+    """What DecomposedHalo / TorchPacker need from a Grid, for (K, J, I)
+    views of the oracle's (I, J, K) state arrays (uniform halo, no pre-pad)."""
+
+    def __init__(self, ni, nj, h):
+        self.ni, self.nj, self.halo, self.i0 = ni, nj, h, h
+
+
+def _step_worker(rank, world, port, px, py, q):
+    import torch.distributed as dist
+
+    from oracle.dycore import OracleDycore
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.state import initial_state
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ni, nj, nk = 16, 16, 4
+        glob_cfg = RunConfig(ni=px * ni, nj=py * nj, nk=nk, n_split=2, dt_atmos=30.0)
+        glob = initial_state(glob_cfg)
+        h = glob_cfg.halo
+        ri, rj = rank % px, rank // px
+        local = {n: np.ascontiguousarray(_block(a, ri, rj, ni, nj, h)) if a.ndim == 3 else
+                 np.ascontiguousarray(_block(a[..., None], ri, rj, ni, nj, h)[..., 0]) for n, a in glob.items()}
+        cfg = RunConfig(ni=ni, nj=nj, nk=nk, n_split=2, dt_atmos=30.0)
+        od = OracleDycore(cfg, local)
+        stub = _Stub(_NumpyGrid(ni, nj, h), {})
+        halo = DecomposedHalo(stub, px, py, rank, transport=DistTransport(rank), packer=TorchPacker(stub.grid))
+        for _ in range(2):
+            for names in od.phases():
+                stub.cur = {n: torch.from_numpy(local[n]).permute(2, 1, 0) for n in names}
+                halo.update(names)
+        q.put((rank, {n: local[n][h:-h, h:-h] for n in ("u", "v", "w", "delp", "pt", "gz", "q0", "mfx")}))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("px,py", [(1, 2), (2, 1)])
+def test_gloo_two_rank_decomposed_timestep_equals_single_domain(px, py):
+    """Two timesteps of a 1x2 / 2x1 decomposition on two gloo processes
+    (DecomposedHalo, DistTransport, the message layouts of every halo point
+    of the step) == the single-domain oracle step on the whole domain."""
+    from oracle.dycore import OracleDycore
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.state import initial_state
+
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_step_worker, args=(r, 2, port, px, py, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    ni, nj, nk = 16, 16, 4
+    cfg = RunConfig(ni=px * ni, nj=py * nj, nk=nk, n_split=2, dt_atmos=30.0)
+    st = initial_state(cfg)
+    ref = OracleDycore(cfg, st)
+    for _ in range(2):
+        ref.step()
+    h = cfg.halo
+    for r in range(2):
+        ri, rj = r % px, r // px
+        for n, got in res[r].items():
+            top = nk + 1 if n == "gz" else nk
+            want = st[n][h + ri * ni: h + (ri + 1) * ni, h + rj * nj: h + (rj + 1) * nj, :top]
+            assert np.array_equal(got[..., :top], want), (r, n)
