@@ -254,7 +254,9 @@ int fv3b_halo_peer_idx(const fv3b_field* f, int nf, const double* s, int ns,
  *                       counter e, release-stores e into its word in every
  *                       neighbour's flag array, then acquire-spins until each
  *                       neighbour's word in its own array is >= e; after 10 s
- *                       it sets the error word instead.  fields: none.
+ *                       it sets the error word and traps (the stream fails
+ *                       loudly instead of storing into a halo a neighbour
+ *                       may still read).  fields: none.
  *                       scalars: [counter address bits, error-word address
  *                       bits, bump, npeer, then (remote word, local word)
  *                       address bits per neighbour], up to 8 neighbours.

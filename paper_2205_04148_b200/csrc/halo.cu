@@ -326,7 +326,8 @@ static int peer_idx_call(const fv3b_field* f, int ntot, const double* s, int ns,
 // No host synchronisation, so a PeerHalo update is three stream-ordered
 // launches (arrive barrier, peer stores, stored barrier) and can be captured
 // in a CUDA graph.  The spin is bounded (10 s of globaltimer): a neighbour
-// that never arrives sets *err instead of hanging the device.
+// that never arrives sets *err and traps (the context reports the failure)
+// instead of hanging the device or continuing on a torn halo.
 // ---------------------------------------------------------------------------
 struct SigArgs {
   unsigned long long* epoch;
@@ -356,8 +357,14 @@ __global__ void signal_wait_kernel(const SigArgs a) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.local[p]) : "memory");
       if (v >= e) break;
       if (global_ns() - t0 > 10000000000ull) {
+        // fail loudly: a neighbour never arrived, so the stores that follow
+        // this barrier could overwrite a halo it is still reading.  The
+        // error word records why; the trap aborts the stream (the host sees
+        // a launch failure at its next synchronisation) instead of letting
+        // the step continue on a torn halo.
         atomicExch(a.err, 1);
-        return;
+        __threadfence_system();
+        __trap();
       }
       __nanosleep(200);
     }

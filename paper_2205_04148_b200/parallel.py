@@ -215,14 +215,17 @@ class DecomposedHalo:
         self.plan = HaloPlan(g.ni, g.nj, g.halo, px, py, rank)
         self.transport = transport or DistTransport(rank)
         self.packer = packer or (DevicePacker(g) if dycore.device != "cpu" else TorchPacker(g))
-        self._bufs: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
+        self._bufs: dict[tuple[int, int, int], tuple[torch.Tensor, torch.Tensor]] = {}
 
-    def _buffers(self, nf: int, levels: int, device) -> tuple[torch.Tensor, torch.Tensor]:
-        if nf not in self._bufs:
+    def _buffers(self, chunk: int, nf: int, levels: int, device) -> tuple[torch.Tensor, torch.Tensor]:
+        """Send / receive buffers of chunk ``chunk`` of an update (one pair
+        per chunk: two equal-size chunks of one update must not share)."""
+        key = (chunk, nf, levels)
+        if key not in self._bufs:
             n = self.plan.total(nf, levels)
-            self._bufs[nf] = (torch.empty(n, dtype=torch.float64, device=device),
-                              torch.empty(n, dtype=torch.float64, device=device))
-        return self._bufs[nf]
+            self._bufs[key] = (torch.empty(n, dtype=torch.float64, device=device),
+                               torch.empty(n, dtype=torch.float64, device=device))
+        return self._bufs[key]
 
     def pack(self, names) -> list:
         """Pack every chunk of <= 32 fields; returns per-chunk state for
@@ -231,7 +234,7 @@ class DecomposedHalo:
         for c in range(0, len(names), MAX_FIELDS):
             tensors = [self.d.cur[n] for n in names[c : c + MAX_FIELDS]]
             L = tensors[0].shape[0]
-            sbuf, rbuf = self._buffers(len(tensors), L, tensors[0].device)
+            sbuf, rbuf = self._buffers(c // MAX_FIELDS, len(tensors), L, tensors[0].device)
             slay = self.plan.layout(len(tensors), L, recv=False)
             rlay = self.plan.layout(len(tensors), L, recv=True)
             self.packer.pack(tensors, [(r, off) for _, _, _, items in slay for _, r, off in items], sbuf)

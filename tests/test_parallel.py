@@ -293,3 +293,24 @@ def test_gloo_two_rank_decomposed_timestep_equals_single_domain(px, py):
             top = nk + 1 if n == "gz" else nk
             want = st[n][h + ri * ni: h + (ri + 1) * ni, h + rj * nj: h + (rj + 1) * nj, :top]
             assert np.array_equal(got[..., :top], want), (r, n)
+
+
+def test_loopback_halo_two_equal_chunks():
+    """One update of 64 fields = two chunks of 32 with equal message sizes:
+    each chunk has its own buffers (keyed by chunk, not size)."""
+    px, py = 2, 2
+    ni, nj, nk, h, nf = 6, 5, 1, 3, 64
+    grid = Grid(ni, nj, nk, halo=h)
+    glob = _global_fields(nf, px * ni, py * nj, grid.levels, h, seed=29)
+    stubs = []
+    for r in range(px * py):
+        ri, rj = r % px, r // px
+        fields = {f"f{t}": _local(grid, _block(glob[t], ri, rj, ni, nj, h), h, True) for t in range(nf)}
+        stubs.append(_Stub(grid, fields))
+    halos = [DecomposedHalo(s, px, py, r, transport=object(), packer=TorchPacker(grid)) for r, s in enumerate(stubs)]
+    _Loopback(halos).run([f"f{t}" for t in range(nf)])
+    for r, s in enumerate(stubs):
+        ri, rj = r % px, r // px
+        for t in range(nf):
+            got = grid.get(s.cur[f"f{t}"], ("I", "J", "K"), (h, h, 0), (ni + 2 * h, nj + 2 * h, grid.levels))
+            np.testing.assert_array_equal(got, _block(glob[t], ri, rj, ni, nj, h))
