@@ -65,6 +65,20 @@ inline int level_chunk(int knob, int tiles, int nk, int ctas_per_sm) {
   return cdiv(nk, per_tile);
 }
 
+// Global loads with an L1 policy: streaming operands read once per level
+// (no_allocate: they do not evict the tile's 2-D metrics) and the 2-D
+// metrics every level re-reads (evict_last).
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 // Tile-local shared-memory array covering [i0, i1) x [j0, j1) (tile coords).
 struct STile {
   double* p;

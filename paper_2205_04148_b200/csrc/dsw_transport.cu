@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
   constexpr int NRX = TJ + 6, NSX = TI / SEG;  // phase-A x items: rows [-3, TJ+3)
   constexpr int NY = NCY * NSY, NA = NY + NRX * NSX;
   constexpr int NX2 = TJ * NSEG, NB = NX2 + TI * (TJ / SEG);
+  static_assert(NA < NT, "one phase-A item per thread, spare threads for del6 order 2");
 
   // phase A of quantity q, item `it` (0 <= it < NA)
   auto phase_a = [&](int q, int it) {
@@ -232,12 +233,12 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
         const double* Q = sdp + q * L::n_q;
         double* sqi = SQI(q);
         double* sfy2 = SFY2(q);
-        double f[SEG + 1];
-        ppm_line<SEG + 1>(QB(Q, c, jb), L::QW, CY(scry, c, jb), L::YW, p1, p2, f);
+        double f[SEG + 1], qc[SEG];
+        ppm_line<SEG + 1, SEG>(QB(Q, c, jb), L::QW, CY(scry, c, jb), L::YW, p1, p2, f, qc);
 #pragma unroll
         for (int u = 0; u < SEG; ++u) {
           const int j = jb + u;
-          const double num = *QB(Q, c, j) * ar[u] + f[u] * y0[u] - f[u + 1] * y1[u];
+          const double num = qc[u] * ar[u] + f[u] * y0[u] - f[u + 1] * y1[u];
           double v = div_fast_r(num, den[u], rd[u], ok);
           sqi[j * L::QW + c + 4] = v;
         }
@@ -268,12 +269,12 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
         const double* Q = sdp + q * L::n_q;
         double* sqj = SQJ(q);
         double* sfx2 = SFX2(q);
-        double f[SEG + 1];
-        ppm_line<SEG + 1>(QB(Q, ib, rj), 1, CX(scrx, ib, rj), 1, p1, p2, f);
+        double f[SEG + 1], qc[SEG];
+        ppm_line<SEG + 1, SEG>(QB(Q, ib, rj), 1, CX(scrx, ib, rj), 1, p1, p2, f, qc);
 #pragma unroll
         for (int u = 0; u < SEG; ++u) {
           const int i = ib + u;
-          const double num = *QB(Q, i, rj) * ar[u] + f[u] * x0[u] - f[u + 1] * x1[u];
+          const double num = qc[u] * ar[u] + f[u] * x0[u] - f[u + 1] * x1[u];
           sqj[(rj + 3) * L::JW + i] = div_fast_r(num, den[u], rd[u], ok);
         }
         if (rj >= 0 && rj < TJ) {
@@ -286,42 +287,94 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
         for (int q = 0; q < 3; ++q) phase_a(q, it);
     }
   };
-  // del6 order 1 of delp, pt, w at cell (i, j) (templates.delnflux):
-  // d2_0 = damp4 * delp (delp) or q itself (pt, w: mass-weighted chains),
-  // dfx_0 = del6_v * (d2_0[-1,0] - d2_0), d2_1 = div(dfx_0, dfy_0) * rarea
+  // del6 order 1 of delp, pt, w (templates.delnflux): d2_0 = damp4 * delp
+  // (delp) or q itself (pt, w: mass-weighted chains), dfx_0 = del6_v *
+  // (d2_0[-1,0] - d2_0), d2_1 = div(dfx_0, dfy_0) * rarea.  An item is a
+  // vertical run of DR cells of one column for all three quantities: the
+  // metrics are loaded once for the three, and each y-face flux once for the
+  // two cells that share it (the same operands, so the same bits as each
+  // cell forming its four face fluxes).  Lanes run along i (conflict-free).
+  constexpr int DR = 2;
+  static_assert(L::D1H % DR == 0 && L::D2H % DR == 0, "del6 runs tile the rows");
   auto deln1 = [&](int e) {
-    const int i = e % L::D1W - 2, j = e / L::D1W - 2;
-    const double v0 = *QB(sd6v, i, j), v1 = *QB(sd6v, i + 1, j);
-    const double u0 = *QB(sd6u, i, j), u1 = *QB(sd6u, i, j + 1), rr = *QB(srarea, i, j);
+    const int i = e % L::D1W - 2, j0 = (e / L::D1W) * DR - 2;
+    double v0[DR], v1[DR], rr[DR], uf[DR + 1];
+#pragma unroll
+    for (int r = 0; r < DR; ++r) {
+      v0[r] = *QB(sd6v, i, j0 + r);
+      v1[r] = *QB(sd6v, i + 1, j0 + r);
+      rr[r] = *QB(srarea, i, j0 + r);
+    }
+#pragma unroll
+    for (int f = 0; f <= DR; ++f) uf[f] = *QB(sd6u, i, j0 + f);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       const double* Q = sdp + q * L::n_q;
-      double c = *QB(Q, i, j), wq = *QB(Q, i - 1, j), eq = *QB(Q, i + 1, j), sq = *QB(Q, i, j - 1), nq = *QB(Q, i, j + 1);
-      if (q == 0) {
-        c = damp4 * c;
-        wq = damp4 * wq;
-        eq = damp4 * eq;
-        sq = damp4 * sq;
-        nq = damp4 * nq;
+      double col[DR + 2], wq[DR], eq[DR];
+#pragma unroll
+      for (int d = 0; d < DR + 2; ++d) col[d] = *QB(Q, i, j0 - 1 + d);
+#pragma unroll
+      for (int r = 0; r < DR; ++r) {
+        wq[r] = *QB(Q, i - 1, j0 + r);
+        eq[r] = *QB(Q, i + 1, j0 + r);
       }
-      const double fx0 = v0 * (wq - c), fx1 = v1 * (c - eq), fy0 = u0 * (sq - c), fy1 = u1 * (c - nq);
-      *D1(q, i, j) = (fx0 - fx1 + fy0 - fy1) * rr;
+      if (q == 0) {
+#pragma unroll
+        for (int d = 0; d < DR + 2; ++d) col[d] = damp4 * col[d];
+#pragma unroll
+        for (int r = 0; r < DR; ++r) {
+          wq[r] = damp4 * wq[r];
+          eq[r] = damp4 * eq[r];
+        }
+      }
+      double fy[DR + 1];  // face j0 + f: del6_u * (d2[j-1] - d2[j])
+#pragma unroll
+      for (int f = 0; f <= DR; ++f) fy[f] = uf[f] * (col[f] - col[f + 1]);
+#pragma unroll
+      for (int r = 0; r < DR; ++r) {
+        const double c = col[r + 1];
+        const double fx0 = v0[r] * (wq[r] - c), fx1 = v1[r] * (c - eq[r]);
+        *D1(q, i, j0 + r) = (fx0 - fx1 + fy[r] - fy[r + 1]) * rr[r];
+      }
     }
   };
   // del6 order 2: dfx_1 = del6_v * (d2_1 - d2_1[-1,0]), d2_2 = div(dfx_1, dfy_1) * rarea
+  // (vertical runs like order 1)
   auto deln2 = [&](int e) {
-    const int i = e % L::D2W - 1, j = e / L::D2W - 1;
-    const double v0 = *QB(sd6v, i, j), v1 = *QB(sd6v, i + 1, j);
-    const double u0 = *QB(sd6u, i, j), u1 = *QB(sd6u, i, j + 1), rr = *QB(srarea, i, j);
+    const int i = e % L::D2W - 1, j0 = (e / L::D2W) * DR - 1;
+    double v0[DR], v1[DR], rr[DR], uf[DR + 1];
+#pragma unroll
+    for (int r = 0; r < DR; ++r) {
+      v0[r] = *QB(sd6v, i, j0 + r);
+      v1[r] = *QB(sd6v, i + 1, j0 + r);
+      rr[r] = *QB(srarea, i, j0 + r);
+    }
+#pragma unroll
+    for (int f = 0; f <= DR; ++f) uf[f] = *QB(sd6u, i, j0 + f);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const double c = *D1(q, i, j);
-      const double fx0 = v0 * (c - *D1(q, i - 1, j)), fx1 = v1 * (*D1(q, i + 1, j) - c);
-      const double fy0 = u0 * (c - *D1(q, i, j - 1)), fy1 = u1 * (*D1(q, i, j + 1) - c);
-      *D2(q, i, j) = (fx0 - fx1 + fy0 - fy1) * rr;
+      double col[DR + 2], wq[DR], eq[DR];
+#pragma unroll
+      for (int d = 0; d < DR + 2; ++d) col[d] = *D1(q, i, j0 - 1 + d);
+#pragma unroll
+      for (int r = 0; r < DR; ++r) {
+        wq[r] = *D1(q, i - 1, j0 + r);
+        eq[r] = *D1(q, i + 1, j0 + r);
+      }
+      double fy[DR + 1];  // face j0 + f: del6_u * (d2_1[j] - d2_1[j-1])
+#pragma unroll
+      for (int f = 0; f <= DR; ++f) fy[f] = uf[f] * (col[f + 1] - col[f]);
+#pragma unroll
+      for (int r = 0; r < DR; ++r) {
+        const double c = col[r + 1];
+        const double fx0 = v0[r] * (c - wq[r]), fx1 = v1[r] * (eq[r] - c);
+        *D2(q, i, j0 + r) = (fx0 - fx1 + fy[r] - fy[r + 1]) * rr[r];
+      }
     }
   };
-  // phase B of quantity q, item `it` (0 <= it < NB): weighted fluxes into FLX/FLY(q)
+  // phase B of quantity q, item `it` (0 <= it < NB): weighted fluxes into FLX/FLY(q).
+  // Every operand is loaded before the first store (the stores could alias
+  // them as far as the compiler knows, which would force reloads).
   auto phase_b = [&](int q, int it) {
     if (it < NX2) {
       const int rj = it % TJ, ib = (it / TJ) * SEG;
@@ -330,15 +383,24 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
       const int nf = (ib + SEG == TI) ? SEG + 1 : SEG;
       const double* fx2 = SFX2(q);
       double* out = FLX(q);
+      double wv[SEG + 1], f2[SEG + 1], d6[SEG + 1], mw[SEG + 1], dv[SEG + 2];
+#pragma unroll
+      for (int u = 0; u < SEG + 1; ++u) {
+        const int i = ib + u;  // <= TI: inside every face array
+        wv[u] = q == 0 ? *CX(sxfx, i, rj) : FLX(0)[rj * L::XW + i];
+        f2[u] = fx2[rj * L::XW + i];
+        d6[u] = *QB(sd6v, i, rj);
+        mw[u] = q == 0 ? 0.0 : smwx[rj * L::XW + i];
+      }
+#pragma unroll
+      for (int u = 0; u < SEG + 2; ++u) dv[u] = *D2(q, ib - 1 + u, rj);
 #pragma unroll
       for (int u = 0; u < SEG + 1; ++u) {
         if (u < nf) {
-          const int i = ib + u;
-          const double w = q == 0 ? *CX(sxfx, i, rj) : FLX(0)[rj * L::XW + i];
           // + dfx_2 = del6_v * (d2_2 - d2_2[-1,0]) (x damp4h * (delp[-1,0] + delp) for pt, w)
-          const double dd = *QB(sd6v, i, rj) * (*D2(q, i, rj) - *D2(q, i - 1, rj));
-          const double dinc = q == 0 ? dd : smwx[rj * L::XW + i] * dd;
-          out[rj * L::XW + i] = 0.5 * (f[u] + fx2[rj * L::XW + i]) * w + dinc;
+          const double dd = d6[u] * (dv[u + 1] - dv[u]);
+          const double dinc = q == 0 ? dd : mw[u] * dd;
+          out[rj * L::XW + ib + u] = 0.5 * (f[u] + f2[u]) * wv[u] + dinc;
         }
       }
     } else {
@@ -349,14 +411,23 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
       const int nf = (jb + SEG == TJ) ? SEG + 1 : SEG;
       const double* fy2 = SFY2(q);
       double* out = FLY(q);
+      double wv[SEG + 1], f2[SEG + 1], d6[SEG + 1], mw[SEG + 1], dv[SEG + 2];
+#pragma unroll
+      for (int u = 0; u < SEG + 1; ++u) {
+        const int j = jb + u;  // <= TJ: inside every face array
+        wv[u] = q == 0 ? *CY(syfx, c, j) : FLY(0)[j * TI + c];
+        f2[u] = fy2[j * TI + c];
+        d6[u] = *QB(sd6u, c, j);
+        mw[u] = q == 0 ? 0.0 : smwy[j * TI + c];
+      }
+#pragma unroll
+      for (int u = 0; u < SEG + 2; ++u) dv[u] = *D2(q, c, jb - 1 + u);
 #pragma unroll
       for (int u = 0; u < SEG + 1; ++u) {
         if (u < nf) {
-          const int j = jb + u;
-          const double w = q == 0 ? *CY(syfx, c, j) : FLY(0)[j * TI + c];
-          const double dd = *QB(sd6u, c, j) * (*D2(q, c, j) - *D2(q, c, j - 1));
-          const double dinc = q == 0 ? dd : smwy[j * TI + c] * dd;
-          out[j * TI + c] = 0.5 * (f[u] + fy2[j * TI + c]) * w + dinc;
+          const double dd = d6[u] * (dv[u + 1] - dv[u]);
+          const double dinc = q == 0 ? dd : mw[u] * dd;
+          out[(jb + u) * TI + c] = 0.5 * (f[u] + f2[u]) * wv[u] + dinc;
         }
       }
     }
@@ -366,35 +437,42 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
     // accumulator inputs of this thread's cell (consumed in S4)
     double acc[6];
 #pragma unroll
-    for (int f = 0; f < 6; ++f) acc[f] = (own && !a.acc_reset) ? a.acci[f][coff + (int64_t)k * sk] : 0.0;
+    for (int f = 0; f < 6; ++f) acc[f] = (own && !a.acc_reset) ? ld_stream(a.acci[f] + coff + (int64_t)k * sk) : 0.0;
     // ---- S0: courant -------------------------------------------------------
     mbar_wait(&bar[0], (k - k0) & 1);
     for (int e = tid; e < L::XW * L::XH; e += NT) {
       const int i = e % L::XW, j = e / L::XW - 3;
       const double uc = *QB(suc, i, j);
       const int64_t m = i + j * sj;
-      *CX(sxfx, i, j) = dt * uc * __ldg(gdy + m);
-      *CX(scrx, i, j) = uc > 0.0 ? dt * uc * __ldg(grdxa + m - 1) : dt * uc * __ldg(grdxa + m);
+      *CX(sxfx, i, j) = dt * uc * ld_keep(gdy + m);
+      *CX(scrx, i, j) = uc > 0.0 ? dt * uc * ld_keep(grdxa + m - 1) : dt * uc * ld_keep(grdxa + m);
     }
     for (int e = tid; e < L::YW * L::YH; e += NT) {
       const int i = e % L::YW - 4, j = e / L::YW;
       const double vc = *QB(svc, i, j);
       const int64_t m = i + j * sj;
-      *CY(syfx, i, j) = dt * vc * __ldg(gdx + m);
-      *CY(scry, i, j) = vc > 0.0 ? dt * vc * __ldg(grdya + m - sj) : dt * vc * __ldg(grdya + m);
+      *CY(syfx, i, j) = dt * vc * ld_keep(gdx + m);
+      *CY(scry, i, j) = vc > 0.0 ? dt * vc * ld_keep(grdya + m - sj) : dt * vc * ld_keep(grdya + m);
     }
-    for (int e = tid; e < L::D1W * L::D1H; e += NT) deln1(e);
+    for (int e = tid; e < L::D1W * (L::D1H / DR); e += NT) deln1(e);
     __syncthreads();
     // ---- S1: phase A of delp, pt, w; del6 order 2; mass weights ---------------
-    for (int e = tid; e < NA; e += NT) phase_a3(e);
-    for (int e = tid; e < L::D2W * L::D2H; e += NT) deln2(e);
-    for (int e = tid; e < (TI + 1) * TJ; e += NT) {
-      const int i = e % (TI + 1), j = e / (TI + 1);
-      smwx[j * L::XW + i] = damp4h * (*QB(sdp, i - 1, j) + *QB(sdp, i, j));
-    }
-    for (int e = tid; e < TI * (TJ + 1); e += NT) {
-      const int i = e % TI, j = e / TI;
-      smwy[j * TI + i] = damp4h * (*QB(sdp, i, j - 1) + *QB(sdp, i, j));
+    // (the phase-A items are the heavy ones: one per thread of the first NA;
+    // the remaining threads take del6 order 2 and the mass weights)
+    if (tid < NA) {
+      phase_a3(tid);
+    } else {
+      const int t = tid - NA;
+      constexpr int NR = NT - NA;
+      for (int e = t; e < L::D2W * (L::D2H / DR); e += NR) deln2(e);
+      for (int e = t; e < (TI + 1) * TJ; e += NR) {
+        const int i = e % (TI + 1), j = e / (TI + 1);
+        smwx[j * L::XW + i] = damp4h * (*QB(sdp, i - 1, j) + *QB(sdp, i, j));
+      }
+      for (int e = t; e < TI * (TJ + 1); e += NR) {
+        const int i = e % TI, j = e / TI;
+        smwy[j * TI + i] = damp4h * (*QB(sdp, i, j - 1) + *QB(sdp, i, j));
+      }
     }
     __syncthreads();
     // ---- S2: phase B of delp (mass fluxes); stage values of the update cell ---

@@ -13,17 +13,24 @@
 //                        Q    + select(sm[-1] + sm > 0.0, (1.0 + C) * (bl + C * b0), 0.0))
 //
 // `q` points at cell 0 (q[d * s] is cell d, needs d in [-3, NF+2)), `c` at
-// the Courant number of face 0 (c[f * cs]).
+// the Courant number of face 0 (c[f * cs]).  With NC > 0 the cell values
+// 0 .. NC-1 of the window are also returned in `qc` (the inner-update
+// numerators reuse them instead of reloading shared memory).
 #pragma once
 
 namespace fv3b {
 
-template <int NF>
+template <int NF, int NC = 0>
 __device__ __forceinline__ void ppm_line(const double* q, int s, const double* c, int cs, double p1, double p2,
-                                         double* out) {
+                                         double* out, double* qc = nullptr) {
+  static_assert(NC <= NF + 2, "centre values lie in the window");
   double qv[NF + 5];  // cells -3 .. NF+1
 #pragma unroll
   for (int d = 0; d < NF + 5; ++d) qv[d] = q[(d - 3) * s];
+  if constexpr (NC > 0) {
+#pragma unroll
+    for (int u = 0; u < NC; ++u) qc[u] = qv[u + 3];
+  }
   double al[NF + 2];  // cells -1 .. NF
 #pragma unroll
   for (int m = 0; m < NF + 2; ++m) {
