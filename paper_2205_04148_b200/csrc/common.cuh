@@ -67,7 +67,9 @@ inline int level_chunk(int knob, int tiles, int nk, int ctas_per_sm) {
 
 // Global loads with an L1 policy: streaming operands read once per level
 // (no_allocate: they do not evict the tile's 2-D metrics) and the 2-D
-// metrics every level re-reads (evict_last).
+// metrics every level re-reads (evict_last).  The asm is a pure expression
+// to the compiler, which may evaluate it outside the guard of its call site:
+// callers pass addresses that are valid whether or not the value is used.
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
   asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));

@@ -437,22 +437,50 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
     // accumulator inputs of this thread's cell (consumed in S4)
     double acc[6];
 #pragma unroll
-    for (int f = 0; f < 6; ++f) acc[f] = (own && !a.acc_reset) ? ld_stream(a.acci[f] + coff + (int64_t)k * sk) : 0.0;
+    for (int f = 0; f < 6; ++f) acc[f] = (own && !a.acc_reset) ? ld_stream(a.acci[f] + (own ? coff : 0) + (int64_t)k * sk) : 0.0;
     // ---- S0: courant -------------------------------------------------------
-    mbar_wait(&bar[0], (k - k0) & 1);
-    for (int e = tid; e < L::XW * L::XH; e += NT) {
+    // (this thread's courant metrics are loaded before the stage wait, so
+    // their L1 / L2 latency hides behind it; nothing else is live here)
+    constexpr int NCX = (L::XW * L::XH + NT - 1) / NT, NCYI = (L::YW * L::YH + NT - 1) / NT;
+    double mxd[NCX], mxl[NCX], mxr[NCX], myd[NCYI], myl[NCYI], myr[NCYI];
+#pragma unroll
+    for (int u = 0; u < NCX; ++u) {  // (spare items load the last item's metrics: always in bounds)
+      const int e = min(tid + u * NT, L::XW * L::XH - 1);
       const int i = e % L::XW, j = e / L::XW - 3;
-      const double uc = *QB(suc, i, j);
       const int64_t m = i + j * sj;
-      *CX(sxfx, i, j) = dt * uc * ld_keep(gdy + m);
-      *CX(scrx, i, j) = uc > 0.0 ? dt * uc * ld_keep(grdxa + m - 1) : dt * uc * ld_keep(grdxa + m);
+      mxd[u] = ld_keep(gdy + m);
+      mxl[u] = ld_keep(grdxa + m - 1);
+      mxr[u] = ld_keep(grdxa + m);
     }
-    for (int e = tid; e < L::YW * L::YH; e += NT) {
+#pragma unroll
+    for (int u = 0; u < NCYI; ++u) {
+      const int e = min(tid + u * NT, L::YW * L::YH - 1);
       const int i = e % L::YW - 4, j = e / L::YW;
-      const double vc = *QB(svc, i, j);
       const int64_t m = i + j * sj;
-      *CY(syfx, i, j) = dt * vc * ld_keep(gdx + m);
-      *CY(scry, i, j) = vc > 0.0 ? dt * vc * ld_keep(grdya + m - sj) : dt * vc * ld_keep(grdya + m);
+      myd[u] = ld_keep(gdx + m);
+      myl[u] = ld_keep(grdya + m - sj);
+      myr[u] = ld_keep(grdya + m);
+    }
+    mbar_wait(&bar[0], (k - k0) & 1);
+#pragma unroll
+    for (int u = 0; u < NCX; ++u) {
+      const int e = tid + u * NT;
+      if (e < L::XW * L::XH) {
+        const int i = e % L::XW, j = e / L::XW - 3;
+        const double uc = *QB(suc, i, j);
+        *CX(sxfx, i, j) = dt * uc * mxd[u];
+        *CX(scrx, i, j) = uc > 0.0 ? dt * uc * mxl[u] : dt * uc * mxr[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NCYI; ++u) {
+      const int e = tid + u * NT;
+      if (e < L::YW * L::YH) {
+        const int i = e % L::YW - 4, j = e / L::YW;
+        const double vc = *QB(svc, i, j);
+        *CY(syfx, i, j) = dt * vc * myd[u];
+        *CY(scry, i, j) = vc > 0.0 ? dt * vc * myl[u] : dt * vc * myr[u];
+      }
     }
     for (int e = tid; e < L::D1W * (L::D1H / DR); e += NT) deln1(e);
     __syncthreads();
