@@ -64,6 +64,83 @@ struct D1 { double x; };
 struct D2 { double x, y; };
 struct D3 { double x, y, z; };
 
+// Level streaming through a per-thread shared-memory ring filled by
+// cp.async (LDGSTS): the operands of the next RD levels are in flight
+// without holding registers, so the sweeps' loads run far ahead of the
+// recurrence at the 8 warps per SM the column count allows.  A Stream
+// gives the NF operand addresses of step 0 and their per-step element
+// deltas (negative for the backward sweeps); use(s, T) runs strictly in step
+// order.  The thread's slot (l, f) is ring[(l * NF + f) * 32] (stride of a
+// full warp of columns: consecutive threads, consecutive banks).  Steps are
+// consumed in batches of RU (one wait per batch; the batch's independent
+// work interleaves like pipelined()'s).
+#ifndef FV3B_RD
+#define FV3B_RD 8
+#endif
+#ifndef FV3B_RU
+#define FV3B_RU 2
+#endif
+constexpr int RD = FV3B_RD, RU = FV3B_RU;
+constexpr int RING = RD * 3 * NC_MAX;  // doubles of one CTA's operand ring
+static_assert(RD % RU == 0 && RD > RU, "ring depth is a multiple of the batch");
+
+template <int NF>
+struct Stream {
+  const double* p[NF];
+  int64_t d[NF];
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int NF, class T, class UseF>
+__device__ __forceinline__ void staged(double* ring, int n, Stream<NF> st, UseF use) {
+  constexpr int SS = NF * NC_MAX;  // doubles per slot
+  double* const last = ring + (RD - 1) * SS;
+  double* wr = ring;  // next slot to fill
+  auto fill = [&]() {
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      cp_async8(wr + f * NC_MAX, st.p[f]);
+      st.p[f] += st.d[f];
+    }
+    wr = wr == last ? ring : wr + SS;
+  };
+#pragma unroll
+  for (int s = 0; s < RD; ++s) {
+    if (s < n) fill();
+    cp_async_commit();
+  }
+  const double* rp = ring;  // next slot to read
+#pragma unroll 1
+  for (int s0 = 0; s0 < n; s0 += RU) {
+    cp_async_wait<RD - RU>();  // the batch's RU groups have landed
+    T v[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      if constexpr (NF == 1) v[u] = T{rp[0]};
+      else if constexpr (NF == 2) v[u] = T{rp[0], rp[NC_MAX]};
+      else v[u] = T{rp[0], rp[NC_MAX], rp[2 * NC_MAX]};
+      rp = rp == last ? ring : rp + SS;
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      if (s0 + u < n) use(s0 + u, v[u]);
+      if (s0 + u + RD < n) fill();  // into a slot this batch has read
+      cp_async_commit();
+    }
+  }
+  cp_async_wait<0>();
+}
+
 #ifndef FV3B_PF  // (overridable for tuning sweeps, tools/build_variant.py)
 #define FV3B_PF 4
 #define FV3B_PFS 12
@@ -92,7 +169,11 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   ColArith<FAST> ar;
   const int nk = a.nk, L = nk + 1;
   double* S0 = sm + c;  // pp -> w2 -> pe2 (shifted one level down)
+#ifdef FV3B_RIEM_REGRING
   (void)L;
+#else
+  double* ring = sm - RING + c;  // staged() operand ring (RD levels x 3) below S0
+#endif
 #define AT(S, k) (S)[(k) * NC]
   const double dt = a.dt, ptop = a.ptop, rdgas = a.rdgas, grav = a.grav, gama = a.gama;
   const double* __restrict__ dm = a.dm.ptr(i, j, 0);
@@ -152,12 +233,17 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
     using T_ = std::true_type;
     using F_ = std::false_type;
     level(0, D3{__ldg(dm + sk), __ldg(gz + sk), __ldg(pt)}, T_{}, F_{});
+#ifdef FV3B_RIEM_REGRING
     pipelined<PF, D3>(
         nk - 2,
         [&](int s) {  // k = s + 1: dm(k+1), gz(k+1), pt(k)
           return D3{__ldg(dm + (s + 2) * sk), __ldg(gz + (s + 2) * sk), __ldg(pt + (s + 1) * sk)};
         },
         [&](int s, const D3& v) { level(s + 1, v, F_{}, F_{}); });
+#else
+    staged<3, D3>(ring, nk - 2, Stream<3>{{dm + 2 * sk, gz + 2 * sk, pt + sk}, {sk, sk, sk}},
+                  [&](int s, const D3& v) { level(s + 1, v, F_{}, F_{}); });
+#endif
     level(nk - 1, D3{0.0, __ldg(gz + nk * sk), __ldg(pt + (nk - 1) * sk)}, F_{}, T_{});
     // interface nk: pp = (dd[nk-1] - pp[nk-1]) / bet[nk-1], dd[nk-1] = 3*pe[nk-1]
     const double dd_prev = 3.0 * pe_prev;
@@ -172,11 +258,16 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
     const double rgrav = ar.rcp(grav);
     double dz_n = ar.div_r(__ldg(gz + nk * sk) - gzn, grav, rgrav);  // dz(nk-1)
     S1[nk * s1] = ar.div(t1g, dz_n) * (pf[nk * sp] + ppn);   // aa(nk)
+#ifdef FV3B_RIEM_REGRING
     pipelined<PFS, D3>(
         nk - 1,
         [&](int s) {  // gz(k-1), pem(k), gam(k)
           return D3{__ldg(gz + (nk - 2 - s) * sk), pf[(nk - 1 - s) * sp], S1[(nk - 1 - s) * s1]};
         },
+#else
+    staged<3, D3>(  // gz(k-1), pem(k), gam(k) for k = nk-1-s
+        ring, nk - 1, Stream<3>{{gz + (nk - 2) * sk, pf + (nk - 1) * sp, S1 + (nk - 1) * s1}, {-sk, -sp, -s1}},
+#endif
         [&](int s, const D3& v) {
           const int k = nk - 1 - s;
           const double ppk = AT(S0, k) - v.z * ppn;
@@ -220,7 +311,12 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
     using F_ = std::false_type;
     auto ld = [&](int l) { return D3{__ldg(dm + l * sk), __ldg(w + l * sk), S1[(l + 1) * s1]}; };
     level(0, ld(0), T_{}, F_{});
+#ifdef FV3B_RIEM_REGRING
     pipelined<PF, D3>(nk - 2, [&](int s) { return ld(s + 1); }, [&](int s, const D3& v) { level(s + 1, v, F_{}, F_{}); });
+#else
+    staged<3, D3>(ring, nk - 2, Stream<3>{{dm + sk, w + sk, S1 + 2 * s1}, {sk, sk, s1}},
+                  [&](int s, const D3& v) { level(s + 1, v, F_{}, F_{}); });
+#endif
     level(nk - 1, ld(nk - 1), F_{}, T_{});
   }
 
@@ -230,8 +326,12 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
     double* wo = a.has_wout ? a.wout.ptr(i, j, 0) : nullptr;
     const int64_t so = a.wout.sk;
     if (wo) wo[(nk - 1) * so] = w2n;
+#ifdef FV3B_RIEM_REGRING
     pipelined<PFS, D1>(
         nk - 1, [&](int s) { return D1{S1[(nk - 1 - s) * s1]}; },  // l = nk-2-s: gw(l+1)
+#else
+    staged<1, D1>(ring, nk - 1, Stream<1>{{S1 + (nk - 1) * s1}, {-s1}},  // gw(l+1), l = nk-2-s
+#endif
         [&](int s, const D1& v) {
           const int l = nk - 2 - s;
           const double w2l = AT(S0, l) - v.x * w2n;
@@ -246,8 +346,12 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
     double pe2 = 0.0, pem = ptop;
     const double rdt = ar.rcp(dt);
     pf[0] = pe2 + pem;
+#ifdef FV3B_RIEM_REGRING
     pipelined<PFS, D2>(
         nk, [&](int s) { return D2{__ldg(dm + s * sk), __ldg(w + s * sk)}; },  // k = s+1: layer k-1
+#else
+    staged<2, D2>(ring, nk, Stream<2>{{dm, w}, {sk, sk}},  // k = s+1: layer k-1
+#endif
         [&](int s, const D2& v) {
           const int k = s + 1;
           pe2 = pe2 + ar.div_r(v.x * (AT(S0, k - 1) - v.y), dt, rdt);
@@ -261,12 +365,16 @@ __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int
   {
     double gzn = __ldg(gz + nk * sk);
     go[nk * sg] = gzn;
+#ifdef FV3B_RIEM_REGRING
     pipelined<PFS, D3>(
         nk,
         [&](int s) {
           const int l = nk - 1 - s;
           return D3{__ldg(dm + l * sk), __ldg(pt + l * sk), go[l * sg]};
         },
+#else
+    staged<3, D3>(ring, nk, Stream<3>{{dm + (nk - 1) * sk, pt + (nk - 1) * sk, go + (nk - 1) * sg}, {-sk, -sk, -sg}},
+#endif
         [&](int s, const D3& v) {
           const int l = nk - 1 - s;
           const double dml = v.x, pm = v.z;
@@ -287,7 +395,12 @@ __device__ __noinline__ void riem_exact(const RiemArgs& a, int i, int j, int c, 
 #endif
 
 __global__ void __launch_bounds__(NC_MAX) riem_kernel(const RiemArgs a) {
-  extern __shared__ double sm[];
+  extern __shared__ double sm_[];
+#ifdef FV3B_RIEM_REGRING
+  double* sm = sm_;
+#else
+  double* sm = sm_ + RING;  // [operand ring | S0]
+#endif
   const int c = threadIdx.x, NC = blockDim.x;
   const int cidx = blockIdx.x * NC + c;
   if (cidx >= a.ni_ext * a.nj_ext) return;
@@ -483,10 +596,18 @@ static int cols_per_cta(size_t bytes_per_col, int64_t columns) {
 }
 
 int launch_riem(const RiemArgs& a, cudaStream_t st) {
+#ifdef FV3B_RIEM_REGRING
   const size_t per_col = (size_t)(a.nk + 1) * sizeof(double);
+#else
+  const size_t per_col = (size_t)(a.nk + 1 + 3 * RD) * sizeof(double);  // S0 + the operand ring
+#endif
   const int forced = tune_get(FV3B_TUNE_RIEM_COLS);
   const int nc = forced > 0 ? (forced < NC_MAX ? forced : NC_MAX) : cols_per_cta(per_col, (int64_t)a.ni_ext * a.nj_ext);
+#ifdef FV3B_RIEM_REGRING
   const size_t bytes = per_col * nc;
+#else
+  const size_t bytes = (size_t)(a.nk + 1) * sizeof(double) * nc + RING * sizeof(double);
+#endif
   FV3B_TRY(set_smem((const void*)riem_kernel, bytes));
   const int cols = a.ni_ext * a.nj_ext;
   riem_kernel<<<cdiv(cols, nc), nc, bytes, st>>>(a);
