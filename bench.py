@@ -465,6 +465,28 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                 "peak": fp64_peak / 1e12, "unit": "Top/s", "frac": ops / mean_launch / fp64_peak,
                 "source": "ncu op counts (profiles/fp64.json) / CUDA-event launch time; peak: "
                           "tools/fp64_probe.cu DFMA issue (profiles/fp64_probe.txt)"}
+        # the program's own arithmetic (tools/opcount.py: each .stn operation
+        # once per point, a division counted once), beside the executed count
+        tab = json.loads((ROOT / "paper_2205_04148_b200" / "traffic_table.json").read_text())
+        alg = tab.get(f"{top}@{doms[top][0]}x{doms[top][1]}x{doms[top][2]}", {}).get("algorithmic_ops")
+        if alg:
+            fp64.update({"algorithmic_ops_per_launch": alg["fp64_ops"], "algorithmic_divisions": alg.get("div", 0),
+                         "algorithmic_frac": alg["fp64_ops"] / mean_launch / fp64_peak,
+                         "executed_over_algorithmic": ops / alg["fp64_ops"]})
+    # per program: the fraction of each roof (HBM: first-touch bytes; fp64
+    # issue: ncu-executed DADD + DMUL + DFMA per launch, profiles/fp64.json)
+    # and the binding one (the larger fraction)
+    executed = json.loads(ff.read_text()) if ff.exists() else {}
+    fp64_pk = FP64_PEAK_OPS * torch.cuda.get_device_properties(0).multi_processor_count / 148
+
+    def binding_roof(kernel, t, hbm_frac):
+        ops = executed.get(kernel)
+        if not isinstance(ops, (int, float)) or t <= 0:
+            return {}
+        f = ops / t / fp64_pk
+        return {"fp64_executed_frac": round(f, 4), "binding": "fp64 issue" if f > hbm_frac else "hbm",
+                "binding_frac": round(max(f, hbm_frac), 4)}
+
     cpu = None
     if not args.no_cpu and world == 1 and args.config == "c2":
         v, cores, sample = cpu_run(1)
@@ -496,6 +518,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                               "measured_us": round(e.measured_time * 1e6, 2),
                               "bound_us": round(e.bound_time * 1e6, 2),
                               "utilization": round(e.utilization, 4),
+                              **binding_roof(e.kernel, e.measured_time, e.utilization),
                               "first_touch_bytes": e.unique_bytes,
                               "movement_model_bytes": perf_model.movement_bytes(e.kernel, doms[e.kernel])}
                    for e in report.entries},

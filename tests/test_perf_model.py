@@ -92,3 +92,26 @@ def test_field_io_interoperates_with_reference(tmp_path):
     name, layout, b = ref_load(tmp_path / "pt.bin")
     assert name == "pt" and np.array_equal(a, b)
     assert layout.to_json() == reference_layout(("I", "J", "K"), (14, 12, 6), (3, 3, 0))
+
+
+def test_algorithmic_op_counts():
+    """tools/opcount.py: the copy stencil has no arithmetic; the committed
+    C2 counts are what the counter gives; d_sw's executed fp64 count (ncu,
+    profiles/fp64.json) exceeds its algorithmic count (tile-halo recompute,
+    reciprocal refinement) but by less than 2x."""
+    import json
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root / "tools"))
+    import opcount
+
+    assert opcount.program_ops("copy", (8, 8, 4))["fp64_ops"] == 0
+    tab = json.loads((root / "paper_2205_04148_b200" / "traffic_table.json").read_text())
+    for name, k in opcount.PROGS:
+        key = f"{name}@192x192x{k}"
+        assert tab[key]["algorithmic_ops"] == opcount.program_ops(name, (192, 192, k)), name
+    executed = json.loads((root / "profiles" / "fp64.json").read_text())["d_sw"]
+    alg = tab["d_sw@192x192x80"]["algorithmic_ops"]["fp64_ops"]
+    assert alg < executed < 2 * alg
