@@ -24,6 +24,11 @@
  *  - Every 3-D field passed to one call must share strides; 2-D fields share
  *    the J stride.  Output fields must not alias inputs (the reference
  *    materialises every right-hand side before its store, reference.py:10-12).
+ *  - Device buffers that are not fields (halo message buffers, index lists,
+ *    barrier flag words) are passed as BUFFER FIELDS: rank 1, `data` = the
+ *    buffer's address, shape[0] = its capacity in elements of its type
+ *    (doubles, int32 or 64-bit words as the entry states), stride[0] = 1.
+ *    Entries check the capacity they need; no address travels in a scalar.
  *  - Status 0 = OK.  Negative = error; fv3b_last_error() has the message.
  *    No exceptions or aborts cross the ABI; no implicit synchronisation:
  *    work is enqueued on `stream` (a cudaStream_t, NULL = legacy default).
@@ -38,7 +43,7 @@
 extern "C" {
 #endif
 
-#define FV3B_ABI_VERSION 4
+#define FV3B_ABI_VERSION 5
 
 enum {
   FV3B_OK = 0,
@@ -195,8 +200,9 @@ int fv3b_p_grad_d(const fv3b_field* f, int nf, const double* s, int ns,
  *                       periodic single-rank domain.  scalars: [halo width].
  *   fv3b_halo_pack / fv3b_halo_unpack  copy an edge strip (all levels) of up
  *                       to 32 fields to / from one contiguous buffer for the
- *                       NCCL neighbour exchange.  scalars: [i0, j0, w, h,
- *                       buffer address as the bits of a double]. */
+ *                       NCCL neighbour exchange.  fields: the fields, then
+ *                       the message buffer (buffer field, doubles).
+ *                       scalars: [i0, j0, w, h]. */
 int fv3b_halo_periodic(const fv3b_field* f, int nf, const double* s, int ns,
                        const fv3b_domain* d, void* stream);
 int fv3b_halo_pack(const fv3b_field* f, int nf, const double* s, int ns,
@@ -208,9 +214,10 @@ int fv3b_halo_unpack(const fv3b_field* f, int nf, const double* s, int ns,
  *                       strip of one decomposed-domain halo update (up to 8
  *                       rectangles, all levels, up to 32 fields sharing one
  *                       level count) to / from one message buffer in one
- *                       launch.  scalars: [buffer address as the bits of a
- *                       double, nrect, then (i0, j0, w, h, element offset)
- *                       per rectangle, interior-relative].  Rectangle r of
+ *                       launch.  fields: the fields, then the message
+ *                       buffer (buffer field, doubles).  scalars: [nrect,
+ *                       then (i0, j0, w, h, element offset) per rectangle,
+ *                       interior-relative].  Rectangle r of
  *                       field t, level k is at offset_r + (t*levels + k)*w*h,
  *                       row-major.  Replaces the paper's Python halo updater
  *                       pack/unpack. */
@@ -241,9 +248,10 @@ int fv3b_halo_peer_rects(const fv3b_field* f, int nf, const double* s, int ns,
  *                       (source slot, source offset, destination slot,
  *                       destination offset, sign +/-1), offsets
  *                       interior-relative; all levels.  fields: nf sources,
- *                       then set r's destination of slot t at nf + r*nf + t.
- *                       scalars: [nf, nset, then (list address bits, n) per
- *                       set].  Up to 32 fields sharing one level count. */
+ *                       then set r's destination of slot t at nf + r*nf + t,
+ *                       then set r's list (buffer field, int32, 5 per
+ *                       entry) at nf*(1+nset) + r.  scalars: [nf, nset].
+ *                       Up to 32 fields sharing one level count. */
 int fv3b_halo_peer_idx(const fv3b_field* f, int nf, const double* s, int ns,
                        const fv3b_domain* d, void* stream);
 
@@ -256,19 +264,20 @@ int fv3b_halo_peer_idx(const fv3b_field* f, int nf, const double* s, int ns,
  *                       neighbour's word in its own array is >= e; after 10 s
  *                       it sets the error word and traps (the stream fails
  *                       loudly instead of storing into a halo a neighbour
- *                       may still read).  fields: none.
- *                       scalars: [counter address bits, error-word address
- *                       bits, bump, npeer, then (remote word, local word)
- *                       address bits per neighbour], up to 8 neighbours.
- *                       d may be NULL. */
+ *                       may still read).  fields (buffer fields of one
+ *                       element): the counter (u64), the error word
+ *                       (int32), then (remote word, local word) per
+ *                       neighbour, up to 8 neighbours.  scalars: [bump,
+ *                       npeer].  d may be NULL. */
 int fv3b_peer_barrier(const fv3b_field* f, int nf, const double* s, int ns,
                       const fv3b_domain* d, void* stream);
 
 /*   fv3b_halo_gather / fv3b_halo_scatter  index-list halo movement for the
  *                       cubed-sphere update (edge strips arrive rotated and,
  *                       for vector pairs, component-swapped with a sign;
- *                       corner fill).  scalars: [buffer address bits, device
- *                       int32 index-list address bits, n].  Gather entries
+ *                       corner fill).  fields: the fields, then the
+ *                       message buffer (buffer field, doubles) and the index
+ *                       list (buffer field, int32).  scalars: [n].  Gather entries
  *                       are (field slot, interior-relative cell offset);
  *                       scatter entries (field slot, offset, sign +/-1).
  *                       Level k of entry s is buf[k*n + s]; all levels of up

@@ -12,7 +12,7 @@ from pathlib import Path
 
 LIB_PATH = Path(os.environ.get("FV3B_LIB", Path(__file__).resolve().parent / "libfv3b.so"))
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 class Field(ctypes.Structure):
@@ -75,6 +75,24 @@ def entry(name: str):
     fn.restype = ctypes.c_int
     fn.argtypes = _ENTRY_SIG
     return fn
+
+
+def buffer_field(addr: int, n: int) -> Field:
+    """A device buffer as an ABI buffer field (include/fv3b.h): rank 1, data
+    = its address, shape[0] = its capacity in elements of its type."""
+    f = Field()
+    f.data = addr
+    f.stride[:] = [1, 0, 0]
+    f.shape[:] = [n, 1, 1]
+    f.halo_lo[:] = [0, 0, 0]
+    f.rank = 1
+    return f
+
+
+def tensor_buffer(t) -> Field:
+    """``buffer_field`` of a contiguous device tensor (capacity: its numel)."""
+    assert t.is_contiguous()
+    return buffer_field(t.data_ptr(), t.numel())
 
 
 def call(name: str, fields: list[Field], scalars: list[float], domain: Domain, stream: int) -> None:

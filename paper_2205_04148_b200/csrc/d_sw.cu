@@ -115,6 +115,8 @@ extern "C" int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns, c
     t.sk = a.u.sk;
     t.i0 = g.i0;
     t.j0 = g.j0;
+    t.mlo = -(g.i0 + g.j0 * t.sj);
+    t.mhi = g.rows * t.sj + t.mlo - 1;
     t.ni = d->ni; t.nj = d->nj; t.nk = d->nk;
     t.p1 = a.p1; t.p2 = a.p2; t.dt = a.dt; t.damp4 = a.damp4; t.damp4h = a.damp4h;
     t.acc_reset = ns == 10 && s[9] != 0.0;
@@ -138,6 +140,8 @@ extern "C" int fv3b_d_sw(const fv3b_field* f, int nf, const double* s, int ns, c
     FV3B_TRY(dsw_momentum_maps(mo, g, f[0], f[1], f[5], f[6], mt));
     mo.i0 = g.i0;
     mo.j0 = g.j0;
+    mo.mlo = -(g.i0 + g.j0 * a.u.sj);
+    mo.mhi = g.rows * a.u.sj + mo.mlo - 1;
   }
   mo.uo = a.uo.o;
   mo.vo = a.vo.o;

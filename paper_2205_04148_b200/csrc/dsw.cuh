@@ -22,6 +22,7 @@ struct DswTpArgs {
   double* acco[6];        // and of their outputs (may alias the inputs)
   const double* rarea;  // interior origin (2-D)
   int64_t sj, sk;
+  int64_t mlo, mhi;     // offsets (from the interior origin) of a 2-D metric's first / last allocated element
   int i0, j0;           // allocated column / row of the interior origin
   int ni, nj, nk, kchunk;
   double p1, p2, dt, damp4, damp4h;  // del6 coefficient, half of it (mass-weighted chains)
@@ -45,6 +46,7 @@ struct DswMoArgs {
   const double* del6_u;  // interior origins (2-D, the 3-D fields' J stride)
   const double* del6_v;
   int64_t sj, sk;
+  int64_t mlo, mhi;  // offsets (from the interior origin) of a 2-D metric's first / last allocated element
   int i0, j0, ni, nj, nk, kchunk;
   double p1, p2, dt, dddmp, d2_bg, da_min, dampv;
 };

@@ -156,6 +156,9 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
   // del6 metrics straight from L1 / L2 (tile-local (i, j); 2-D, J stride sj)
   const double* gd6u = a.del6_u + gi0 + (int64_t)gj0 * a.sj;
   const double* gd6v = a.del6_v + gi0 + (int64_t)gj0 * a.sj;
+  // del6 order 1 / 2 loads of a ragged edge tile are clamped into the
+  // allocation (the cells beyond it are outside every owned cell's stencil)
+  const int64_t mlo = a.mlo - (gi0 + (int64_t)gj0 * a.sj), mhi = a.mhi - (gi0 + (int64_t)gj0 * a.sj) - a.sj;
   const double dampv = a.dampv;
   auto QB = [&](auto* p, int i, int j) { return p + (j + 3) * L::QW + (i + 4); };
   auto CX = [&](auto* p, int i, int j) { return p + (j + 3) * L::XW + i; };
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
           // d2_v0 = dampv * wk ; dfx_v0 = del6_v * (d2_v0[-1,0] - d2_v0) ; d2_v1 = div(dfx_v0, dfy_v0) * rarea
           const int e = item - (NY + NX + NU + NV + ND);
           const int i = e % L::D1W - 2, j = e / L::D1W - 2;
-          const int64_t m = i + j * sj;
+          const int64_t m = min(max(i + j * sj, mlo), mhi);
           const double v0 = __ldg(gd6v + m), v1 = __ldg(gd6v + m + 1), u0 = __ldg(gd6u + m), u1 = __ldg(gd6u + m + sj);
           const double c = dampv * *QB(swk, i, j), wq = dampv * *QB(swk, i - 1, j), eq = dampv * *QB(swk, i + 1, j);
           const double sq = dampv * *QB(swk, i, j - 1), nq = dampv * *QB(swk, i, j + 1);
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
     // d2_v2 = div(dfx_v1, dfy_v1) * rarea, dfx_v1 = del6_v * (d2_v1 - d2_v1[-1,0])
     for (int e = tid; e < L::D2W * L::D2H; e += blockDim.x) {
       const int i = e % L::D2W - 1, j = e / L::D2W - 1;
-      const int64_t m = i + j * sj;
+      const int64_t m = min(max(i + j * sj, mlo), mhi);
       const double v0 = __ldg(gd6v + m), v1 = __ldg(gd6v + m + 1), u0 = __ldg(gd6u + m), u1 = __ldg(gd6u + m + sj);
       const double c = *D1(i, j);
       const double fx0 = v0 * (c - *D1(i - 1, j)), fx1 = v1 * (*D1(i + 1, j) - c);

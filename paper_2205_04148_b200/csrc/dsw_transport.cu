@@ -133,6 +133,11 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
   const double* gdy = a.dy + moff;
   const double* grdxa = a.rdxa + moff;
   const double* grdya = a.rdya + moff;
+  // a ragged edge tile's box reaches past the allocated halo: its metric
+  // loads are clamped into the allocation (those cells lie outside the
+  // domain plus the 3-cell halo every owned cell reads, so no owned result
+  // sees the clamped values)
+  const int64_t mlo = a.mlo - moff, mhi = a.mhi - moff;
   double* scrx = smem + L::o_crx;  // XW, origin (0, -3)
   double* sxfx = smem + L::o_xfx;
   double* scry = smem + L::o_cry;  // YW, origin (-4, 0)
@@ -447,7 +452,7 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
     for (int u = 0; u < NCX; ++u) {  // (spare items load the last item's metrics: always in bounds)
       const int e = min(tid + u * NT, L::XW * L::XH - 1);
       const int i = e % L::XW, j = e / L::XW - 3;
-      const int64_t m = i + j * sj;
+      const int64_t m = min(max(i + j * sj, mlo + 1), mhi);
       mxd[u] = ld_keep(gdy + m);
       mxl[u] = ld_keep(grdxa + m - 1);
       mxr[u] = ld_keep(grdxa + m);
@@ -456,7 +461,7 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
     for (int u = 0; u < NCYI; ++u) {
       const int e = min(tid + u * NT, L::YW * L::YH - 1);
       const int i = e % L::YW - 4, j = e / L::YW;
-      const int64_t m = i + j * sj;
+      const int64_t m = min(max(i + j * sj, mlo + sj), mhi);
       myd[u] = ld_keep(gdx + m);
       myl[u] = ld_keep(grdya + m - sj);
       myr[u] = ld_keep(grdya + m);

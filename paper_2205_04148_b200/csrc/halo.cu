@@ -113,6 +113,18 @@ static int collect(const fv3b_field* f, int nf, const fv3b_domain* d, int h, dou
 }
 
 
+// A device buffer passed as a rank-1 field: data = its address, shape[0] =
+// its capacity in elements of its type (doubles for message buffers, int32
+// for index lists, 64-bit words for barrier flags).
+static int buffer_of(const fv3b_field& f, int64_t need, const char* what, void** out) {
+  if (f.rank != 1 || f.data == nullptr)
+    return fail(FV3B_EINVAL, "%s: expects a rank-1 buffer field with a non-null address", what);
+  if ((int64_t)f.shape[0] < need)
+    return fail(FV3B_EINVAL, "%s: buffer holds %d elements, the call needs %lld", what, f.shape[0], (long long)need);
+  *out = f.data;
+  return FV3B_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Multi-rectangle pack / unpack: every edge / corner strip of a halo update
 // for a batch of fields in one launch (the decomposed-domain exchange,
@@ -148,15 +160,15 @@ __global__ void rects_kernel(const RectArgs a) {
 
 static int rects_call(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d, void* stream,
                       bool unpack) {
-  // scalars: [buffer address bits, nrect, (i0, j0, w, h, offset) x nrect]
-  if (f == nullptr || d == nullptr || s == nullptr || ns < 2) return fail(FV3B_EINVAL, "halo rects: bad arguments");
+  // fields: the halo fields, then the message buffer (a buffer field);
+  // scalars: [nrect, (i0, j0, w, h, offset) x nrect]
+  if (f == nullptr || d == nullptr || s == nullptr || ns < 1 || nf < 2)
+    return fail(FV3B_EINVAL, "halo rects: bad arguments");
   RectArgs a;
-  uint64_t bits;
-  memcpy(&bits, &s[0], sizeof bits);
-  a.buf = reinterpret_cast<double*>(bits);
-  a.nrect = (int)s[1];
-  if (a.buf == nullptr || a.nrect < 1 || a.nrect > RECT_MAX || ns != 2 + 5 * a.nrect)
-    return fail(FV3B_EINVAL, "halo rects: 1..%d rectangles, 2 + 5*n scalars, non-null buffer", RECT_MAX);
+  a.nrect = (int)s[0];
+  if (a.nrect < 1 || a.nrect > RECT_MAX || ns != 1 + 5 * a.nrect)
+    return fail(FV3B_EINVAL, "halo rects: 1..%d rectangles, 1 + 5*n scalars", RECT_MAX);
+  --nf;
   int levels[HALO_MAXF];
   FV3B_TRY(collect(f, nf, d, 0, a.o, levels, &a.sj, &a.sk));
   for (int t = 1; t < nf; ++t)
@@ -165,16 +177,22 @@ static int rects_call(const fv3b_field* f, int nf, const double* s, int ns, cons
   a.nf = nf;
   a.unpack = unpack;
   int maxn = 1;
+  int64_t need = 0;
   for (int r = 0; r < a.nrect; ++r) {
-    const double* q = s + 2 + 5 * r;
+    const double* q = s + 1 + 5 * r;
     a.i0[r] = (int)q[0];
     a.j0[r] = (int)q[1];
     a.w[r] = (int)q[2];
     a.h[r] = (int)q[3];
     a.off[r] = (int64_t)q[4];
-    if (a.w[r] <= 0 || a.h[r] <= 0) return fail(FV3B_EINVAL, "halo rects: empty rectangle %d", r);
+    if (a.w[r] <= 0 || a.h[r] <= 0 || a.off[r] < 0) return fail(FV3B_EINVAL, "halo rects: empty rectangle %d", r);
     maxn = a.w[r] * a.h[r] > maxn ? a.w[r] * a.h[r] : maxn;
+    const int64_t end = a.off[r] + (int64_t)nf * a.levels * a.w[r] * a.h[r];
+    need = end > need ? end : need;
   }
+  void* buf;
+  FV3B_TRY(buffer_of(f[nf], need, "halo rects", &buf));
+  a.buf = static_cast<double*>(buf);
   dim3 grid(cdiv(maxn, 256) < 16 ? cdiv(maxn, 256) : 16, a.levels, a.nrect * nf);
   rects_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
   return check_launch(unpack ? "fv3b_halo_unpack_rects" : "fv3b_halo_pack_rects");
@@ -280,15 +298,15 @@ __global__ void peer_idx_kernel(const PeerIdxArgs a) {
 
 static int peer_idx_call(const fv3b_field* f, int ntot, const double* s, int ns, const fv3b_domain* d,
                          void* stream) {
-  // scalars: [nf, nset, (index-list address bits, n) x nset]; fields: nf
-  // sources, then set r's destination of slot t at nf + r*nf + t
-  if (f == nullptr || d == nullptr || s == nullptr || ns < 2) return fail(FV3B_EINVAL, "halo peer idx: bad arguments");
+  // scalars: [nf, nset]; fields: nf sources, then set r's destination of
+  // slot t at nf + r*nf + t, then set r's index list (an int32 buffer
+  // field of 5 entries per cell) at nf*(1+nset) + r
+  if (f == nullptr || d == nullptr || s == nullptr || ns != 2) return fail(FV3B_EINVAL, "halo peer idx: bad arguments");
   PeerIdxArgs a;
   const int nf = (int)s[0];
   a.nset = (int)s[1];
-  if (nf < 1 || nf > PEER_MAXF || a.nset < 1 || a.nset > RECT_MAX || ns != 2 + 2 * a.nset ||
-      ntot != nf * (1 + a.nset))
-    return fail(FV3B_EINVAL, "halo peer idx: 1..%d fields, 1..%d sets, 2 + 2*nset scalars, nf*(1+nset) fields",
+  if (nf < 1 || nf > PEER_MAXF || a.nset < 1 || a.nset > RECT_MAX || ntot != nf * (1 + a.nset) + a.nset)
+    return fail(FV3B_EINVAL, "halo peer idx: 1..%d fields, 1..%d sets, nf*(1+nset) fields + nset lists",
                 PEER_MAXF, RECT_MAX);
   int levels[PEER_MAXF], lv[PEER_MAXF];
   double* o[PEER_MAXF];
@@ -304,11 +322,15 @@ static int peer_idx_call(const fv3b_field* f, int ntot, const double* s, int ns,
     int64_t sj2, sk2;
     FV3B_TRY(collect(f + nf * (1 + r), nf, d, 0, a.dst[r], lv, &sj2, &sk2));
     if (sj2 != sj || sk2 != sk) return fail(FV3B_ELAYOUT, "halo peer idx: destinations must share the sources' strides");
-    uint64_t bits;
-    memcpy(&bits, &s[2 + 2 * r], sizeof bits);
-    a.idx[r] = reinterpret_cast<const int*>(bits);
-    a.n[r] = (int)s[3 + 2 * r];
-    if (a.n[r] < 0 || (a.n[r] > 0 && a.idx[r] == nullptr)) return fail(FV3B_EINVAL, "halo peer idx: bad list %d", r);
+    const fv3b_field& lf = f[nf * (1 + a.nset) + r];
+    a.n[r] = lf.rank == 1 ? lf.shape[0] / 5 : -1;
+    a.idx[r] = nullptr;
+    if (a.n[r] < 0 || lf.shape[0] % 5 != 0) return fail(FV3B_EINVAL, "halo peer idx: list %d is not 5 int32 per entry", r);
+    if (a.n[r] > 0) {
+      void* p;
+      FV3B_TRY(buffer_of(lf, 5 * (int64_t)a.n[r], "halo peer idx list", &p));
+      a.idx[r] = static_cast<const int*>(p);
+    }
     maxn = a.n[r] > maxn ? a.n[r] : maxn;
   }
   if (maxn == 0) return FV3B_OK;
@@ -372,25 +394,26 @@ __global__ void signal_wait_kernel(const SigArgs a) {
   __threadfence_system();
 }
 
-static int signal_call(const double* s, int ns, void* stream) {
-  // scalars: [epoch addr bits, error-word addr bits, bump, npeer, (remote, local addr bits) x npeer]
-  if (s == nullptr || ns < 4) return fail(FV3B_EINVAL, "peer barrier: bad arguments");
+static int signal_call(const fv3b_field* f, int nf, const double* s, int ns, void* stream) {
+  // fields (buffer fields of one element each): the counter (u64), the
+  // error word (int32), then (remote, local) flag words per neighbour;
+  // scalars: [bump, npeer]
+  if (f == nullptr || s == nullptr || ns != 2) return fail(FV3B_EINVAL, "peer barrier: bad arguments");
   SigArgs a;
-  auto ptr = [&](int i) {
-    uint64_t b;
-    memcpy(&b, &s[i], sizeof b);
-    return b;
-  };
-  a.epoch = reinterpret_cast<unsigned long long*>(ptr(0));
-  a.err = reinterpret_cast<int*>(ptr(1));
-  a.bump = s[2] != 0.0;
-  a.npeer = (int)s[3];
-  if (a.epoch == nullptr || a.err == nullptr || a.npeer < 0 || a.npeer > RECT_MAX || ns != 4 + 2 * a.npeer)
-    return fail(FV3B_EINVAL, "peer barrier: 0..%d neighbours, 4 + 2*n scalars, non-null counter", RECT_MAX);
-  for (int p = 0; p < a.npeer; ++p) {
-    a.remote[p] = reinterpret_cast<unsigned long long*>(ptr(4 + 2 * p));
-    a.local[p] = reinterpret_cast<unsigned long long*>(ptr(5 + 2 * p));
-    if (a.remote[p] == nullptr || a.local[p] == nullptr) return fail(FV3B_EINVAL, "peer barrier: null flag word");
+  a.bump = s[0] != 0.0;
+  a.npeer = (int)s[1];
+  if (a.npeer < 0 || a.npeer > RECT_MAX || nf != 2 + 2 * a.npeer)
+    return fail(FV3B_EINVAL, "peer barrier: 0..%d neighbours, 2 + 2*n buffer fields", RECT_MAX);
+  void* p;
+  FV3B_TRY(buffer_of(f[0], 1, "peer barrier counter", &p));
+  a.epoch = static_cast<unsigned long long*>(p);
+  FV3B_TRY(buffer_of(f[1], 1, "peer barrier error word", &p));
+  a.err = static_cast<int*>(p);
+  for (int q = 0; q < a.npeer; ++q) {
+    FV3B_TRY(buffer_of(f[2 + 2 * q], 1, "peer barrier remote flag", &p));
+    a.remote[q] = static_cast<unsigned long long*>(p);
+    FV3B_TRY(buffer_of(f[3 + 2 * q], 1, "peer barrier local flag", &p));
+    a.local[q] = static_cast<unsigned long long*>(p);
   }
   signal_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(a);
   return check_launch("fv3b_peer_barrier");
@@ -429,23 +452,27 @@ __global__ void idx_kernel(const IdxArgs a) {
 
 static int idx_call(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d, void* stream,
                     bool scatter) {
-  // scalars: [buffer address bits, index-list address bits, n]
-  if (f == nullptr || d == nullptr || s == nullptr || ns != 3) return fail(FV3B_EINVAL, "halo gather/scatter: 3 scalars");
+  // fields: the halo fields, then the message buffer (doubles) and the
+  // index list (int32, 2 per entry to gather, 3 to scatter) as buffer
+  // fields; scalars: [n entries]
+  if (f == nullptr || d == nullptr || s == nullptr || ns != 1 || nf < 3)
+    return fail(FV3B_EINVAL, "halo gather/scatter: fields + buffer + list, 1 scalar");
   IdxArgs a;
-  uint64_t bits;
-  memcpy(&bits, &s[0], sizeof bits);
-  a.buf = reinterpret_cast<double*>(bits);
-  memcpy(&bits, &s[1], sizeof bits);
-  a.idx = reinterpret_cast<const int*>(bits);
-  a.n = (int)s[2];
+  a.n = (int)s[0];
   a.scatter = scatter;
-  if (a.buf == nullptr || a.idx == nullptr || a.n < 0) return fail(FV3B_EINVAL, "halo gather/scatter: null buffer or index list");
+  if (a.n < 0) return fail(FV3B_EINVAL, "halo gather/scatter: negative entry count");
+  nf -= 2;
   int levels[HALO_MAXF];
   int64_t sj;
   FV3B_TRY(collect(f, nf, d, 0, a.o, levels, &sj, &a.sk));
   for (int t = 1; t < nf; ++t)
     if (levels[t] != levels[0]) return fail(FV3B_EINVAL, "halo gather/scatter: fields must share their level count");
   a.levels = levels[0];
+  void* p;
+  FV3B_TRY(buffer_of(f[nf], (int64_t)a.n * a.levels, "halo gather/scatter buffer", &p));
+  a.buf = static_cast<double*>(p);
+  FV3B_TRY(buffer_of(f[nf + 1], (int64_t)a.n * (scatter ? 3 : 2), "halo gather/scatter list", &p));
+  a.idx = static_cast<const int*>(p);
   if (a.n == 0) return FV3B_OK;
   dim3 grid(cdiv(a.n, 256) < 32 ? cdiv(a.n, 256) : 32, a.levels);
   idx_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
@@ -478,18 +505,17 @@ extern "C" int fv3b_halo_periodic(const fv3b_field* f, int nf, const double* s, 
 
 static int strip_call(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d, void* stream,
                       bool unpack) {
-  // scalars: i0, j0, w, h (strip rectangle, interior-relative), buffer
-  // pointer passed as the bit pattern of s[4] (uint64 in a double slot).
-  if (f == nullptr || d == nullptr || s == nullptr || ns != 5) return fail(FV3B_EINVAL, "halo strip: 5 scalars");
+  // fields: the halo fields, then the message buffer (a buffer field);
+  // scalars: i0, j0, w, h (strip rectangle, interior-relative)
+  if (f == nullptr || d == nullptr || s == nullptr || ns != 4 || nf < 2)
+    return fail(FV3B_EINVAL, "halo strip: fields + buffer, 4 scalars");
   StripArgs a;
   a.i0 = (int)s[0];
   a.j0 = (int)s[1];
   a.w = (int)s[2];
   a.h = (int)s[3];
-  uint64_t bits;
-  memcpy(&bits, &s[4], sizeof bits);
-  a.buf = reinterpret_cast<double*>(bits);
-  if (a.buf == nullptr || a.w <= 0 || a.h <= 0) return fail(FV3B_EINVAL, "halo strip: empty strip or null buffer");
+  if (a.w <= 0 || a.h <= 0) return fail(FV3B_EINVAL, "halo strip: empty strip");
+  --nf;
   FV3B_TRY(collect(f, nf, d, 0, a.o, a.levels, &a.sj, &a.sk));
   a.nf = nf;
   a.unpack = unpack;
@@ -500,6 +526,9 @@ static int strip_call(const fv3b_field* f, int nf, const double* s, int ns, cons
     off += (int64_t)a.levels[t] * a.w * a.h;
     maxl = a.levels[t] > maxl ? a.levels[t] : maxl;
   }
+  void* buf;
+  FV3B_TRY(buffer_of(f[nf], off, "halo strip", &buf));
+  a.buf = static_cast<double*>(buf);
   dim3 grid(cdiv(a.w * a.h, 256) < 16 ? cdiv(a.w * a.h, 256) : 16, maxl, nf);
   strip_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
   return check_launch(unpack ? "fv3b_halo_unpack" : "fv3b_halo_pack");
@@ -537,10 +566,8 @@ extern "C" int fv3b_halo_peer_idx(const fv3b_field* f, int nf, const double* s, 
 
 extern "C" int fv3b_peer_barrier(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                                  void* stream) {
-  (void)f;
-  (void)nf;
   (void)d;
-  return signal_call(s, ns, stream);
+  return signal_call(f, nf, s, ns, stream);
 }
 
 extern "C" int fv3b_halo_gather(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,

@@ -275,16 +275,13 @@ class CubeHalo:
         return plan
 
     def _call(self, entry, tensors, buf, idx, n):
-        import struct
-
         import torch
 
         from . import _lib
 
-        bits = lambda t: struct.unpack("d", struct.pack("Q", t.data_ptr()))[0]
         g = self.d.grid
-        _lib.call(entry, [g.abi(t) for t in tensors], [bits(buf), bits(idx), float(n)], g.domain(),
-                  torch.cuda.current_stream().cuda_stream)
+        fields = [g.abi(t) for t in tensors] + [_lib.tensor_buffer(buf), _lib.tensor_buffer(idx)]
+        _lib.call(entry, fields, [float(n)], g.domain(), torch.cuda.current_stream().cuda_stream)
 
     def pack(self, names) -> list:
         names = tuple(names)
@@ -370,17 +367,14 @@ class CubePeerHalo:
         return self._plans[names]
 
     def _call(self, names, dst_sets, lists) -> None:
-        import struct
-
         import torch
 
         from . import _lib
 
         g = self.d.grid
         fields = [g.abi(self.d.cur[n]) for n in names] + [g.abi(t) for row in dst_sets for t in row]
+        fields += [_lib.tensor_buffer(idx) for idx in lists]  # int32, 5 per entry
         s = [float(len(names)), float(len(lists))]
-        for idx in lists:
-            s += [struct.unpack("d", struct.pack("Q", idx.data_ptr()))[0], float(idx.numel() // 5)]
         _lib.call("fv3b_halo_peer_idx", fields, s, g.domain(), torch.cuda.current_stream().cuda_stream)
 
     def push(self, names) -> None:

@@ -156,3 +156,28 @@ class Grid:
         else:
             raise ValueError(f"unsupported field dims {dims}")
         return np.ascontiguousarray(v.cpu().numpy())
+
+
+class capture_guard:
+    """Around a CUDA-graph capture: collect garbage first and keep the
+    collector off until the capture ends.  A collection during a capture can
+    free device tensors of dead objects whose blocks carry cross-stream
+    events, and the allocator's event queries then invalidate the capture
+    (torch.cuda.graph does not collect by default)."""
+
+    def __enter__(self):
+        import gc
+
+        gc.collect()
+        torch.cuda.synchronize()
+        self._was = gc.isenabled()
+        gc.disable()
+        return self
+
+    def __exit__(self, *exc):
+        import gc
+
+        if self._was:
+            gc.enable()
+        return False
+

@@ -22,7 +22,7 @@ import torch
 
 from . import _lib
 from .config import DIAG_3D, METRICS_2D, STATE_3D, RunConfig
-from .device import Grid
+from .device import Grid, capture_guard
 
 C_METRICS = ("dx", "dy", "dxc", "dyc", "rdxc", "rdyc", "rarea", "rarea_c", "fc")
 D_METRICS = ("dx", "dy", "dxc", "dyc", "rdx", "rdy", "rdxa", "rdya", "area", "rarea", "rarea_c", "f0", "del6_u",
@@ -549,15 +549,15 @@ class Dycore:
         times at present, so one graph suffices); the captures follow the
         assignments until they cycle.  Capture executes nothing, so the
         state is unchanged; the bookkeeping is restored afterwards."""
-        torch.cuda.synchronize()
         start = (dict(self.cur), dict(self.alt))
         self._graphs = {}
-        while self._assignment() not in self._graphs:
-            key = self._assignment()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self.step()
-            self._graphs[key] = (g, dict(self.cur), dict(self.alt))
+        with capture_guard():
+            while self._assignment() not in self._graphs:
+                key = self._assignment()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self.step()
+                self._graphs[key] = (g, dict(self.cur), dict(self.alt))
         self.cur, self.alt = start
         torch.cuda.synchronize()
 

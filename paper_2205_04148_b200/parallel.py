@@ -37,7 +37,6 @@ computes bitwise what the single domain computes on its cells.
 
 from __future__ import annotations
 
-import struct
 from dataclasses import dataclass
 
 import torch
@@ -158,11 +157,10 @@ class DevicePacker:
         self.dom = grid.domain(placement)
 
     def _call(self, entry, tensors, rects, buf):
-        bits = struct.unpack("d", struct.pack("Q", buf.data_ptr()))[0]
-        s = [bits, float(len(rects))]
+        s = [float(len(rects))]
         for r, off in rects:
             s += [float(r.i0), float(r.j0), float(r.w), float(r.h), float(off)]
-        fields = [self.grid.abi(t) for t in tensors]
+        fields = [self.grid.abi(t) for t in tensors] + [self._lib.tensor_buffer(buf)]
         self._lib.call(entry, fields, s, self.dom, torch.cuda.current_stream().cuda_stream)
 
     def pack(self, tensors, rects, buf):
@@ -463,10 +461,6 @@ def ipc_sync(group=None, device: bool = True):
     return sync
 
 
-def _bits(addr: int) -> float:
-    return struct.unpack("d", struct.pack("Q", addr))[0]
-
-
 class FlagSync:
     """Stream-ordered barrier of one rank with its neighbours for
     :class:`PeerHalo` (``fv3b_peer_barrier``): every rank owns an int64
@@ -490,12 +484,12 @@ class FlagSync:
         self.dom = _lib.Domain()
         self._args = []
         for phase in (0, 1):
-            sc = [_bits(self.epoch.data_ptr()), _bits(self.err.data_ptr()), 1.0 - phase, float(len(nb))]
+            words = [_lib.tensor_buffer(self.epoch), _lib.tensor_buffer(self.err)]
             for p in nb:
                 remote = peer_flags[p].data_ptr() + 8 * (phase * world + rank)
                 local = flags.data_ptr() + 8 * (phase * world + p)
-                sc += [_bits(remote), _bits(local)]
-            self._args.append(_lib.prepare([], sc))
+                words += [_lib.buffer_field(remote, 1), _lib.buffer_field(local, 1)]
+            self._args.append(_lib.prepare(words, [1.0 - phase, float(len(nb))]))
 
     def __call__(self, phase: int) -> None:
         self._lib.call_prepared("fv3b_peer_barrier", self._args[phase], self.dom,
@@ -585,15 +579,17 @@ class LoopbackCluster:
         bookkeeping is restored afterwards."""
         import torch
 
-        torch.cuda.synchronize()
+        from .device import capture_guard
+
         start = [(dict(d.cur), dict(d.alt)) for d in self.d]
         self._graphs = {}
-        while self._assignment() not in self._graphs:
-            key = self._assignment()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self.step()
-            self._graphs[key] = (g, [(dict(d.cur), dict(d.alt)) for d in self.d])
+        with capture_guard():
+            while self._assignment() not in self._graphs:
+                key = self._assignment()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self.step()
+                self._graphs[key] = (g, [(dict(d.cur), dict(d.alt)) for d in self.d])
         for d, (cur, alt) in zip(self.d, start):
             d.cur, d.alt = cur, alt
         torch.cuda.synchronize()

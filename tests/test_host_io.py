@@ -64,23 +64,22 @@ def test_flag_sync_needs_peer_halos():
 
 
 def test_flag_sync_word_addresses():
-    """FlagSync's scalars: rank r release-stores into column r of each
+    """FlagSync's buffer fields: rank r release-stores into column r of each
     neighbour's flag array and waits on the neighbours' columns of its own;
     phase 0 bumps the counter, phase 1 reuses it; self-neighbours are skipped."""
-    import struct
-
     from paper_2205_04148_b200.parallel import FlagSync, new_flags
 
     world, rank = 4, 1
     flags = [new_flags(world, "cpu") for _ in range(world)]
     fs = FlagSync(rank, [0, 2, 1, 2], flags[rank], dict(enumerate(flags)))
-    bits = lambda v: struct.unpack("Q", struct.pack("d", v))[0]
     for phase in (0, 1):
-        _, _, sarr, ns = fs._args[phase]
-        s = [sarr[i] for i in range(ns)]
-        assert bits(s[0]) == fs.epoch.data_ptr() and bits(s[1]) == fs.err.data_ptr()
-        assert s[2] == (1.0 if phase == 0 else 0.0) and s[3] == 2.0  # neighbours 0 and 2
+        farr, nf, sarr, ns = fs._args[phase]
+        f = [farr[i] for i in range(nf)]
+        assert all(x.rank == 1 and x.shape[0] >= 1 for x in f)
+        assert f[0].data == fs.epoch.data_ptr() and f[1].data == fs.err.data_ptr()
+        assert ns == 2 and sarr[0] == (1.0 if phase == 0 else 0.0) and sarr[1] == 2.0  # neighbours 0 and 2
+        assert nf == 2 + 2 * 2
         for q, p in enumerate([0, 2]):
-            remote, local = bits(s[4 + 2 * q]), bits(s[5 + 2 * q])
+            remote, local = f[2 + 2 * q].data, f[3 + 2 * q].data
             assert remote == flags[p].data_ptr() + 8 * (phase * world + rank)
             assert local == flags[rank].data_ptr() + 8 * (phase * world + p)
