@@ -10,17 +10,27 @@ from paper_2205_04148_b200.config import RunConfig
 from paper_2205_04148_b200.dycore import Dycore
 from paper_2205_04148_b200.state import initial_state
 
+from paper_2205_04148_b200 import _lib
+
 cfg = RunConfig(ni=40, nj=24, nk=6, n_split=1, dt_atmos=20.0)
 d = Dycore(cfg, initial_state(cfg))
 d.step()
 torch.cuda.synchronize()
 print("step done")
+# the level-marching tile kernels with multi-level chunks, the last one
+# ragged (6 = 4 + 2 levels): the TMA refill of the next level, the mbarrier
+# phase flip and tracer_2d's level-boundary restaging (the C2 launch shapes)
+with _lib.tuning(kchunk=4):
+    d.step()
+torch.cuda.synchronize()
+print("kchunk=4 step done")
 # the program-level kernels the step does not launch (run_b200, ragged domains,
 # full-tile placement: edge regions fire)
 from paper_2205_04148_b200.executor import run_b200
 from paper_2205_04148_b200.inputs import synthetic_inputs
 
 for name, dom, place in (("fv_tp_2d", (37, 21, 4), (False,) * 4), ("c_sw", (37, 21, 3), (True,) * 4),
+                         ("d_sw", (37, 21, 3), (True,) * 4), ("d_sw", (35, 17, 5), (False,) * 4),
                          ("riem_solver_c", (33, 7, 9), (False,) * 4), ("remap_profile", (33, 7, 9), (False,) * 4),
                          ("copy", (33, 17, 5), (False,) * 4)):
     run_b200(name, synthetic_inputs(name, dom, 1), dom, placement=place)
