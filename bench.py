@@ -434,9 +434,9 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     # the remapping: the profile launch covers the scalars and the winds, the
     # mapping runs as the scalars' and the winds' launches
     if "remap_map" in doms:
-        doms["remap_map"] = (cfg.ni, cfg.nj, cfg.nk + 1, len(cfg.remapped()))
-    if "remap_map_winds" in doms:
-        doms["remap_map_winds"] = (cfg.ni, cfg.nj, cfg.nk + 1, 2)
+        doms["remap_map"] = (cfg.ni, cfg.nj, cfg.nk + 1, len(cfg.remap_linear()))
+    if "remap_map_winds" in doms:  # u, v (and pt in log pressure)
+        doms["remap_map_winds"] = (cfg.ni, cfg.nj, cfg.nk + 1, 2 + int(cfg.pt_logp))
     if "moist_pk" in doms:
         doms["moist_pk"] = (cfg.ni, cfg.nj, cfg.nk + 1, len(cfg.moist_names()))
     if "remap_tracers" in doms:

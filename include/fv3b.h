@@ -138,9 +138,22 @@ int fv3b_remap_profile(const fv3b_field* f, int nf, const double* s, int ns,
  *     q_out (q_out must not alias any other field).  scalars: none.
  *     Grouped form: scalars s[g] = fields in group g; fields ak, bk, then
  *     per group its thickness (rewritten with its pe2 differences) and 5
- *     per member. */
+ *     per member.  s[g] < 0: group g (of -s[g] fields) maps in log pressure
+ *     (FV3 pt, kord_tm < 0): its thickness slot holds log(pe1) and is
+ *     followed by log(pe2) (interfaces, fv3b_log_thickness), nothing is
+ *     rewritten, and its profiles were formed at the log-pressure thickness. */
 int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int ns,
                    const fv3b_domain* d, void* stream);
+
+/* K5d log-pressure coordinate: pe1[0] = ak[0], pe1[k+1] = pe1[k] +
+ *     delp[k], ps = pe1[nk], pe2 = (pe1[0], ak + bk * ps, ps); lnpe1 =
+ *     det_log(pe1), lnpe2 = det_log(pe2), dlnp[k] = lnpe1[k+1] - lnpe1[k]
+ *     (the thickness remap_profile takes for a field remapped in log
+ *     pressure, and the interfaces fv3b_remap_map's log group maps between).
+ *     fields: delp (3-D), ak, bk (K), dlnp (3-D layers), lnpe1, lnpe2 (3-D
+ *     interfaces).  No scalars.  Domain nk = layers. */
+int fv3b_log_thickness(const fv3b_field* f, int nf, const double* s, int ns,
+                       const fv3b_domain* d, void* stream);
 
 /* K5c pressure / heat-capacity diagnostics of the remapped state (FV3
  *     fv_mapz pe, pk, pkz and moist_cv; oracle/thermo.py):

@@ -114,17 +114,28 @@ class OracleDycore:
         yield cfg.tracer_names() + ["cx", "cy", "xfa", "yfa", "mfx", "mfy", "delp"]
         self.call("tracer_2d", c)
         self.call("remap_tracers", c)
+        ak, bk = cfg.target_coordinate()
+        # pt in log pressure (FV3 kord_tm < 0): its profile at the log-pressure thickness
+        if cfg.pt_logp:
+            st["dlnp"] = np.zeros_like(st["delp"])
+            sl = (slice(self._h, -self._h), slice(self._h, -self._h))
+            st["dlnp"][sl + (slice(0, cfg.nk),)] = remap_map.log_thickness(st["delp"][sl], ak, cfg.nk)
         for n in ("pt", "w"):  # the remap_profile program on each thermodynamic field
-            self.call("remap_profile", c, bind={"q": n, "a4_2": f"{n}_a2", "a4_3": f"{n}_a3", "a4_4": f"{n}_a4"})
+            bind = {"q": n, "a4_2": f"{n}_a2", "a4_3": f"{n}_a3", "a4_4": f"{n}_a4"}
+            if n == "pt" and cfg.pt_logp:
+                bind["delp"] = "dlnp"
+            self.call("remap_profile", c, bind=bind)
         # the D-grid winds at their own thickness (remap_profile program, map1_ppm)
         st["du"], st["dv"] = remap_map.face_thickness(st["delp"], cfg.nk, self._h)
         for w, dw in (("u", "du"), ("v", "dv")):
             self.call("remap_profile", c,
                       bind={"q": w, "delp": dw, "a4_2": f"{w}_a2", "a4_3": f"{w}_a3", "a4_4": f"{w}_a4"})
-        ak, bk = cfg.target_coordinate()
-        remap_map.remap_map(st, cfg.remapped(), ak, bk, cfg.nk, self._h)
+        # (delp's rewrite comes last: the log-pressure mapping of pt reads it)
+        if cfg.pt_logp:
+            remap_map.remap_map(st, ["pt"], ak, bk, cfg.nk, self._h, log=True)
         for w, dw in (("u", "du"), ("v", "dv")):
             remap_map.remap_map(st, [w], ak, bk, cfg.nk, self._h, delp_key=dw)
+        remap_map.remap_map(st, cfg.remap_linear(), ak, bk, cfg.nk, self._h)
         thermo.apply(st, cfg.tracer_names()[:thermo.SPECIES], cfg.nk, self._h, thermo.constants(c))
 
     def acoustic_phases(self):

@@ -27,6 +27,8 @@ from __future__ import annotations
 
 import numpy as np
 
+from .detmath import det_log
+
 R3 = 1.0 / 3.0
 R23 = 2.0 / 3.0
 
@@ -142,16 +144,37 @@ def face_thickness(delp: np.ndarray, nk: int, h: int) -> tuple[np.ndarray, np.nd
     return du, dv
 
 
-def remap_map(state: dict, names: list[str], ak, bk, nk: int, h: int, delp_key: str = "delp") -> None:
+def log_edges(pe1: np.ndarray, pe2: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """The interfaces in the log-pressure mapping coordinate (FV3 maps pt in
+    log(p) when kord_tm < 0: ``peln`` and ``log(pe2)`` in fv_mapz), through
+    the deterministic det_log (the device's)."""
+    return det_log(pe1), det_log(pe2)
+
+
+def log_thickness(delp: np.ndarray, ak, nk: int) -> np.ndarray:
+    """dlnp[k] = log(pe1[k+1]) - log(pe1[k]) (..., nk): the layer thickness
+    remap_profile takes for a field remapped in log pressure
+    (fv3b_log_thickness)."""
+    pe1, _ = pe_edges(delp, ak, np.zeros(nk + 1), nk)
+    ln1 = det_log(pe1)
+    return ln1[..., 1:] - ln1[..., :-1]
+
+
+def remap_map(state: dict, names: list[str], ak, bk, nk: int, h: int, delp_key: str = "delp",
+              log: bool = False) -> None:
     """In place on the interior columns of reference-convention arrays:
     every field q in ``names`` <- its profile (q_a2, q_a3, q_a4) mapped onto
     the target layers of the thickness ``state[delp_key]``; then that
-    thickness <- pe2 differences."""
+    thickness <- pe2 differences.  ``log``: the mapping coordinate is
+    log(p) (the profiles were formed at log_thickness) and the thickness is
+    left as it is."""
     sl = (slice(h, -h or None), slice(h, -h or None))
     delp = state[delp_key][sl]
     pe1, pe2 = pe_edges(delp, ak, bk, nk)
+    x1, x2 = log_edges(pe1, pe2) if log else (pe1, pe2)
     for n in names:
         q = state[n][sl]
-        q2 = map_columns(pe1, pe2, q, state[f"{n}_a2"][sl], state[f"{n}_a3"][sl], state[f"{n}_a4"][sl], nk)
+        q2 = map_columns(x1, x2, q, state[f"{n}_a2"][sl], state[f"{n}_a3"][sl], state[f"{n}_a4"][sl], nk)
         q[..., :nk] = q2
-    delp[..., :nk] = pe2[..., 1:] - pe2[..., :-1]
+    if not log:  # (a log-pressure mapping only reads the thickness)
+        delp[..., :nk] = pe2[..., 1:] - pe2[..., :-1]

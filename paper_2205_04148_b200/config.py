@@ -13,8 +13,11 @@ One dycore timestep (k_split = 1):
         p_grad_d                                      -> u, v
     halo_update(q*, cx, cy, xfa, yfa, mfx, mfy)
     tracer_2d (nq tracers)                            -> q*
-    remap_tracers (remap_profile of q*, pt, w)        -> *_a2, *_a3, *_a4
-    remap_map (Lagrangian -> Eulerian, map1_ppm)      -> q*, pt, w, delp
+    log_thickness (pt_logp)                           -> dlnp
+    remap_tracers (remap_profile of q*, w at delp,
+                   pt at dlnp, u / v at their faces)  -> *_a2, *_a3, *_a4
+    remap_map (Lagrangian -> Eulerian, map1_ppm;
+               pt in log pressure)                    -> q*, pt, w, u, v, delp
 """
 
 from __future__ import annotations
@@ -34,6 +37,9 @@ class RunConfig:
     dt_atmos: float = 90.0
     halo: int = 4
     seed: int = 2205
+    # remap pt in log pressure (FV3 fv_mapz with kord_tm < 0): its profile at
+    # the log-pressure thickness, its mapping on log(pe1) -> log(pe2)
+    pt_logp: bool = True
     # physical constants of the programs (templates.RIEM_CONSTS / D_CONSTS)
     consts: dict = field(default_factory=lambda: {
         "ptop": 300.0, "rdgas": 287.05, "grav": 9.80665, "gama": 1.4, "p_fac": 0.05,
@@ -55,6 +61,11 @@ class RunConfig:
 
     def tracer_names(self) -> list[str]:
         return [f"q{n}" for n in range(self.nq)]
+
+    def remap_linear(self) -> list[str]:
+        """The remapped fields mapped in pressure at delp (pt is mapped in log
+        pressure when ``pt_logp``)."""
+        return self.tracer_names() + (["w"] if self.pt_logp else ["pt", "w"])
 
     def remapped(self) -> list[str]:
         """Fields the vertical remapping maps onto the target layers: the

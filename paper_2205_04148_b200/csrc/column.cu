@@ -745,6 +745,8 @@ struct RemapMapArgs {
   View delp, ak, bk;           // delp: the first group's thickness (strides shared)
   double* thick[16];           // per group: its thickness (rewritten with the pe2 differences)
   int gfirst[17];              // group g maps fields gfirst[g] .. gfirst[g+1]-1
+  bool glog[16];               // group g maps in log pressure: thick[g] = log(pe1), lnpe2[g] = log(pe2)
+  const double* lnpe2[16];
   int ngroup;
   int ncb;                     // blocks of 32 columns per CTA
   const double* q[16];
@@ -762,7 +764,85 @@ struct RemapMapArgs {
 constexpr int MP_COLS = 32, MP_TY = 16;  // blockDim.y = min(ceil(nq / MP_F), MP_TY)
 constexpr double MP_R3 = 1.0 / 3.0, MP_R23 = 2.0 / 3.0;  // the oracle's R3, R23 (same roundings)
 
-template <int MP_F>
+// map1_ppm in log pressure for one field per thread (a log group, FV3's pt
+// with kord_tm < 0): the source and target interfaces are the precomputed
+// log(pe1), log(pe2) (fv3b_log_thickness), read per level; the cursor walk
+// and every expression are remap_map_kernel's (oracle/remap_map.py
+// map_columns on log_edges).
+__device__ __forceinline__ void map_log_column(const double* __restrict__ l1, const double* __restrict__ l2,
+                                               const double* __restrict__ q, const double* __restrict__ a2,
+                                               const double* __restrict__ a3, const double* __restrict__ a4,
+                                               double* qo, int nk, int64_t sk) {
+  // the next source interface, the next target interface and the next
+  // layer's coefficients are loaded one step ahead, so the cursor walk never
+  // waits on a load (the linear kernel's running-sum prefetch)
+  int k1 = 0;
+  double pk = __ldg(l1), pn = __ldg(l1 + sk), pnn = __ldg(l1 + min(2, nk) * sk);
+  double top = __ldg(l2), bot = __ldg(l2 + sk);
+  double b2 = __ldg(a2), b3 = __ldg(a3), b4 = __ldg(a4);
+  const int k1n = nk > 1 ? 1 : 0;
+  double n2 = __ldg(a2 + k1n * sk), n3 = __ldg(a3 + k1n * sk), n4 = __ldg(a4 + k1n * sk);
+  auto advance_to = [&](int m, double pm, double pm1) {  // the cursor moves to source layer m
+    k1 = m;
+    pk = pm;
+    pn = pm1;
+    pnn = __ldg(l1 + min(m + 2, nk) * sk);
+    b2 = __ldg(a2 + m * sk);
+    b3 = __ldg(a3 + m * sk);
+    b4 = __ldg(a4 + m * sk);
+    const int mn = m + 1 < nk ? m + 1 : m;
+    n2 = __ldg(a2 + mn * sk);
+    n3 = __ldg(a3 + mn * sk);
+    n4 = __ldg(a4 + mn * sk);
+  };
+  for (int k2 = 0; k2 < nk; ++k2) {
+    const double botn = __ldg(l2 + min(k2 + 2, nk) * sk);
+    while (top > pn && k1 < nk - 1) {
+      ++k1;
+      pk = pn;
+      pn = pnn;
+      pnn = __ldg(l1 + min(k1 + 2, nk) * sk);
+      b2 = n2;
+      b3 = n3;
+      b4 = n4;
+      const int mn = k1 + 1 < nk ? k1 + 1 : k1;
+      n2 = __ldg(a2 + mn * sk);
+      n3 = __ldg(a3 + mn * sk);
+      n4 = __ldg(a4 + mn * sk);
+    }
+    const double d = pn - pk;
+    const double pl = (top - pk) / d;
+    if (bot <= pn) {
+      const double pr = (bot - pk) / d;
+      qo[k2 * sk] = b2 + 0.5 * (b4 + b3 - b2) * (pr + pl) - b4 * MP_R3 * (pr * (pr + pl) + pl * pl);
+    } else {
+      double qsum = (pn - top) * (b2 + 0.5 * (b4 + b3 - b2) * (1.0 + pl) - b4 * (MP_R3 * (1.0 + pl * (1.0 + pl))));
+      double pm = pn;
+      for (int m = k1 + 1; m < nk; ++m) {
+        const double pm1 = m == k1 + 1 ? pnn : __ldg(l1 + (m + 1) * sk);
+        const double dm = pm1 - pm;
+        if (bot > pm1) {
+          qsum = qsum + dm * __ldg(q + m * sk);
+          pm = pm1;
+        } else {
+          const double dp = bot - pm;
+          const double esl = dp / dm;
+          const double c2 = __ldg(a2 + m * sk);
+          qsum = qsum + dp * (c2 + 0.5 * esl * (__ldg(a3 + m * sk) - c2 + __ldg(a4 + m * sk) * (1.0 - MP_R23 * esl)));
+          advance_to(m, pm, pm1);
+          break;
+        }
+      }
+      qo[k2 * sk] = qsum / (bot - top);
+    }
+    top = bot;
+    bot = botn;
+  }
+}
+
+// LG: the launch has log-pressure groups (their CTAs take map_log_column;
+// kept out of the other instantiations, whose registers it would raise)
+template <int MP_F, bool LG>
 __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapMapArgs a) {
   // map1_ppm's walk over the source layers only moves downwards, so the
   // Lagrangian interfaces pe1 are produced by a running sum as it advances
@@ -779,6 +859,14 @@ __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapM
   const int i = live ? cidx % a.ni : 0, j = live ? cidx / a.ni : 0;
   const int64_t off = i + (int64_t)j * a.sj, sk = a.sk;
   const int grp = blockIdx.y;
+  if (LG && a.glog[grp]) {  // a log-pressure group: its interface pair, one field per thread, nothing rewritten
+    const double* l1 = a.thick[grp] + off;
+    const double* l2 = a.lnpe2[grp] + off;
+    if (live)
+      for (int t = a.gfirst[grp] + threadIdx.y % (blockDim.y / a.ncb); t < a.gfirst[grp + 1]; t += blockDim.y / a.ncb)
+        map_log_column(l1, l2, a.q[t] + off, a.a2[t] + off, a.a3[t] + off, a.a4[t] + off, a.qo[t] + off, a.nk, a.sk);
+    return;
+  }
   double* thick = a.thick[grp] + off;
   double* AK = sm;
   double* BK = sm + (nk + 1);
@@ -913,7 +1001,10 @@ __global__ void __launch_bounds__(MP_COLS * MP_TY) remap_map_kernel(const RemapM
 
 // fields: delp (3-D, rewritten in place), ak, bk (K, nk+1 target
 // coefficients), then per tracer t: q_t, a4_2_t, a4_3_t, a4_4_t (remap_profile
-// outputs), q_out_t.  Domain nk = interface levels.  No scalars.
+// outputs), q_out_t.  Domain nk = interface levels.  Grouped form: s[g] =
+// fields in group g, negative for a group mapped in log pressure, whose
+// thickness slot holds log(pe1) followed by log(pe2) (interfaces,
+// fv3b_log_thickness; nothing is rewritten).
 extern "C" int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
                               void* stream) {
   // ns == 0: delp, ak, bk, then 5 fields per tracer (one group).  ns >= 1:
@@ -927,13 +1018,20 @@ extern "C" int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int 
     cnt[0] = (nf - 3) / 5;
   } else {
     for (int g = 0; g < ng; ++g) {
-      cnt[g] = (int)s[g];
-      if (cnt[g] < 1 || (double)cnt[g] != s[g]) return fail(FV3B_EINVAL, "fv3b_remap_map: bad group size %g", s[g]);
+      cnt[g] = (int)(s[g] < 0 ? -s[g] : s[g]);  // negative: a log-pressure group
+      if (cnt[g] < 1 || (double)cnt[g] != (s[g] < 0 ? -s[g] : s[g]))
+        return fail(FV3B_EINVAL, "fv3b_remap_map: bad group size %g", s[g]);
     }
   }
-  for (int g = 0; g < ng; ++g) total += cnt[g];
-  if (total > 16 || nf != 2 + ng + 5 * total)
-    return fail(FV3B_EINVAL, "fv3b_remap_map: expects the thickness(es), ak, bk and 5 per field (<= 16 fields)");
+  int nlog = 0;
+  for (int g = 0; g < ng; ++g) {
+    total += cnt[g];
+    nlog += ns > 0 && s[g] < 0;
+  }
+  if (total > 16 || nf != 2 + ng + nlog + 5 * total)
+    return fail(FV3B_EINVAL,
+                "fv3b_remap_map: expects ak, bk, per group its thickness (log groups: log(pe1), log(pe2)) and 5 per "
+                "field (<= 16 fields)");
   if (d->nk < 2 || d->nk > 4096)
     return fail(FV3B_EDOMAIN, "fv3b_remap_map: program domain nk=%d outside [2, 4096]", d->nk);
   // field-list positions: thickness of group g, ak, bk, field t's five
@@ -949,6 +1047,7 @@ extern "C" int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int 
     xbk = 1;
     for (int g = 0, x = 2, t = 0; g < ng; ++g) {
       xthick[g] = x++;
+      if (s[g] < 0) ++x;  // log(pe2) follows log(pe1)
       for (int m = 0; m < cnt[g]; ++m, ++t, x += 5) xfield[t] = x;
     }
   }
@@ -959,6 +1058,16 @@ extern "C" int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int 
   FV3B_TRY(view_of(f[xbk], 1, *d, h0, "bk", &a.bk));
   a.nq = total;
   a.ngroup = ng;
+  for (int g = 0; g < ng; ++g) {
+    a.glog[g] = ns > 0 && s[g] < 0;
+    a.lnpe2[g] = nullptr;
+    if (a.glog[g]) {
+      View v;
+      FV3B_TRY(view_of(f[xthick[g] + 1], 3, *d, h0, "log(pe2)", &v));
+      if (v.sj != a.delp.sj || v.sk != a.delp.sk) return fail(FV3B_ELAYOUT, "fv3b_remap_map: strides differ");
+      a.lnpe2[g] = v.o;
+    }
+  }
   for (int g = 0, t = 0; g < ng; ++g) {
     View v;
     FV3B_TRY(view_of(f[xthick[g]], 3, *d, h0, "thickness", &v));
@@ -996,13 +1105,20 @@ extern "C" int fv3b_remap_map(const fv3b_field* f, int nf, const double* s, int 
   const int ty = cdiv(maxc, F) < MP_TY ? cdiv(maxc, F) : MP_TY;
   a.ncb = ty >= 4 ? 1 : 4 / ty;  // at least 4 warps per CTA
   const size_t bytes = (size_t)2 * (a.nk + 1) * sizeof(double);
-  const void* kern = F == 4 ? (const void*)remap_map_kernel<4> : (const void*)remap_map_kernel<2>;
+  bool anylog = false;
+  for (int g = 0; g < ng; ++g) anylog = anylog || a.glog[g];
+  const void* kern = F == 4 ? (anylog ? (const void*)remap_map_kernel<4, true> : (const void*)remap_map_kernel<4, false>)
+                            : (anylog ? (const void*)remap_map_kernel<2, true> : (const void*)remap_map_kernel<2, false>);
   if (bytes > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
     return check_launch("remap_map smem attribute");
   dim3 grid(cdiv(a.ni * a.nj, MP_COLS * a.ncb), ng), block(MP_COLS, ty * a.ncb);
-  if (F == 4)
-    remap_map_kernel<4><<<grid, block, bytes, (cudaStream_t)stream>>>(a);
+  if (F == 4 && anylog)
+    remap_map_kernel<4, true><<<grid, block, bytes, (cudaStream_t)stream>>>(a);
+  else if (F == 4)
+    remap_map_kernel<4, false><<<grid, block, bytes, (cudaStream_t)stream>>>(a);
+  else if (anylog)
+    remap_map_kernel<2, true><<<grid, block, bytes, (cudaStream_t)stream>>>(a);
   else
-    remap_map_kernel<2><<<grid, block, bytes, (cudaStream_t)stream>>>(a);
+    remap_map_kernel<2, false><<<grid, block, bytes, (cudaStream_t)stream>>>(a);
   return check_launch("remap_map");
 }

@@ -16,6 +16,7 @@
 // HBM-bound: delp + the moist tracers in, five fields out.
 #include "common.cuh"
 #include "detmath.cuh"
+#include "fastdiv.cuh"
 
 namespace fv3b {
 
@@ -116,4 +117,81 @@ extern "C" int fv3b_moist_pk(const fv3b_field* f, int nf, const double* s, int n
     return check_launch("moist_pk smem attribute");
   moist_pk_kernel<<<cdiv(d->ni * d->nj, MK_COLS), dim3(MK_COLS, MK_TY), bytes, (cudaStream_t)stream>>>(a);
   return check_launch("fv3b_moist_pk");
+}
+
+// ---------------------------------------------------------------------------
+// Log-pressure coordinate for remapping pt in log(p) (FV3 fv_mapz with
+// kord_tm < 0: pt is profiled and mapped in the log-pressure coordinate):
+//   pe1[0] = ak[0] (ptop), pe1[k+1] = pe1[k] + delp[k],  ps = pe1[nk]
+//   pe2 = pe1[0] | ak[k] + bk[k] * ps | ps       (the mapping's target)
+//   lnpe1 = log(pe1), lnpe2 = log(pe2),  dlnp[k] = lnpe1[k+1] - lnpe1[k]
+// with the deterministic det_log; oracle/remap_map.py log_thickness /
+// log_edges, bitwise.  dlnp is the thickness remap_profile takes for pt,
+// lnpe1 / lnpe2 the interfaces fv3b_remap_map's log group maps between.
+// One thread per column; the logs of consecutive levels are independent.
+// ---------------------------------------------------------------------------
+namespace fv3b {
+// FAST: det_log_fast (branch-free, fastdiv.cuh) with a validity flag; a
+// column whose flag fails is redone with det_log.  Inputs are never written.
+template <bool FAST>
+__device__ __forceinline__ bool log_column(const double* d, int64_t sd, double* o, int64_t so, double* x1, int64_t s1,
+                                           double* x2, int64_t s2, const double* ak, const double* bk, int64_t skk,
+                                           int nk) {
+  ColArith<FAST> ar;
+  double pe = __ldg(ak), lp = ar.log(pe);
+  x1[0] = lp;
+  x2[0] = lp;
+#pragma unroll 4
+  for (int k = 0; k < nk; ++k) {
+    pe = pe + __ldg(d + k * sd);
+    const double ln = ar.log(pe);
+    o[k * so] = ln - lp;
+    x1[(k + 1) * s1] = ln;
+    lp = ln;
+  }
+  const double ps = pe;
+  x2[nk * s2] = lp;  // log(ps)
+#pragma unroll 4
+  for (int k = 1; k < nk; ++k) x2[k * s2] = ar.log(__ldg(ak + k * skk) + __ldg(bk + k * skk) * ps);
+  return ar.ok;
+}
+
+__global__ void __launch_bounds__(128) log_thickness_kernel(View dp, View dl, View l1, View l2, const double* ak,
+                                                            const double* bk, int64_t skk, int ni, int nj, int nk) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= ni * nj) return;
+  const int i = col % ni, j = col / ni;
+  const double* d = dp.ptr(i, j, 0);
+  double *o = dl.ptr(i, j, 0), *x1 = l1.ptr(i, j, 0), *x2 = l2.ptr(i, j, 0);
+  if (!log_column<true>(d, dp.sk, o, dl.sk, x1, l1.sk, x2, l2.sk, ak, bk, skk, nk))
+    log_column<false>(d, dp.sk, o, dl.sk, x1, l1.sk, x2, l2.sk, ak, bk, skk, nk);
+}
+}  // namespace fv3b
+
+// fields: delp (3-D), ak, bk (K, nk+1), dlnp (3-D layers), lnpe1, lnpe2 (3-D
+// interfaces) outputs.  No scalars.  Domain nk = layers.
+extern "C" int fv3b_log_thickness(const fv3b_field* f, int nf, const double* s, int ns, const fv3b_domain* d,
+                                  void* stream) {
+  using namespace fv3b;
+  (void)s;
+  if (f == nullptr || d == nullptr || nf != 6 || ns != 0)
+    return fail(FV3B_EINVAL, "fv3b_log_thickness: expects delp, ak, bk, dlnp, lnpe1, lnpe2; no scalars");
+  View dp, ak, bk, dl, l1, l2;
+  const Halo h0 = {0, 0, 0, 0, 0, 0};
+  fv3b_domain di = *d;
+  di.nk = d->nk + 1;  // (interfaces)
+  FV3B_TRY(view_of(f[0], 3, *d, h0, "delp", &dp));
+  FV3B_TRY(view_of(f[1], 1, di, h0, "ak", &ak));
+  FV3B_TRY(view_of(f[2], 1, di, h0, "bk", &bk));
+  FV3B_TRY(view_of(f[3], 3, *d, h0, "dlnp", &dl));
+  FV3B_TRY(view_of(f[4], 3, di, h0, "lnpe1", &l1));
+  FV3B_TRY(view_of(f[5], 3, di, h0, "lnpe2", &l2));
+  for (int x = 3; x < 6; ++x)
+    for (int y = 0; y < 6; ++y)
+      if (x != y && f[x].data == f[y].data) return fail(FV3B_EINVAL, "fv3b_log_thickness: output %d aliases field %d", x, y);
+  if (d->ni <= 0 || d->nj <= 0 || d->nk <= 0) return FV3B_OK;
+  const int cols = d->ni * d->nj;
+  log_thickness_kernel<<<cdiv(cols, 128), 128, 0, (cudaStream_t)stream>>>(dp, dl, l1, l2, ak.o, bk.o, ak.sk, d->ni,
+                                                                          d->nj, d->nk);
+  return check_launch("fv3b_log_thickness");
 }

@@ -65,7 +65,8 @@ class Dycore:
         self.cur: dict[str, torch.Tensor] = {n: g.new3(device) for n in names3}
         self.cur.update({n: g.new2(device) for n in METRICS_2D})
         self.alt: dict[str, torch.Tensor] = {n: g.new3(device) for n in list(PINGPONG) + ["gz"] + cfg.tracer_names()}
-        self.scratch = {n: g.new3(device) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc", "riem_scr", "du", "dv")}
+        self.scratch = {n: g.new3(device) for n in ("delpcc", "ptcc", "wcc", "pkc", "gzc", "riem_scr", "du", "dv",
+                                                     "dlnp", "lnpe1", "lnpe2")}
         # target coordinate of the vertical remapping (pe2 = ak + bk * ps)
         ak, bk = cfg.target_coordinate()
         self.coord = {"ak": torch.from_numpy(ak).to(device), "bk": torch.from_numpy(bk).to(device)}
@@ -385,6 +386,11 @@ class Dycore:
         point).  One launch per kernel, the field groups sharing it."""
         self.launch("remap_faces", "fv3b_face_thickness", [self.f("delp"), self.s("du"), self.s("dv")], [],
                     self.dom_layers)
+        if self.cfg.pt_logp:  # pt is profiled at the log-pressure thickness
+            coord = [self.grid.abi(self.coord[n], rank=1) for n in ("ak", "bk")]
+            self.launch("remap_logp", "fv3b_log_thickness",
+                        [self.f("delp")] + coord + [self.s(n) for n in ("dlnp", "lnpe1", "lnpe2")], [],
+                        self.dom_layers)
         fields, counts = [], []
         for thick, names in self._remap_groups():
             counts.append(float(len(names)))
@@ -394,7 +400,24 @@ class Dycore:
         self.launch("remap_tracers", "fv3b_remap_profile", fields, counts, self.dom_ifaces)
 
     def _remap_groups(self):
-        return [(self.f("delp"), self.cfg.remapped()), (self.s("du"), ["u"]), (self.s("dv"), ["v"])]
+        """(thickness, fields) of the profile launch: the tracers and w (and
+        pt unless pt_logp) at delp, pt at its log-pressure thickness, the
+        winds at their face thickness."""
+        cfg = self.cfg
+        groups = [(self.f("delp"), cfg.remap_linear())]
+        if cfg.pt_logp:
+            groups.append((self.s("dlnp"), ["pt"]))
+        return groups + [(self.s("du"), ["u"]), (self.s("dv"), ["v"])]
+
+    def _map_launches(self):
+        """(node, [(thickness fields, fields, sign)]) of the mapping launches:
+        the fields at delp (which rewrites delp), then the winds at their
+        face thickness and pt in log pressure (sign -1: between the log
+        interfaces of fv3b_log_thickness)."""
+        side = [([self.s("du")], ["u"], 1.0), ([self.s("dv")], ["v"], 1.0)]
+        if self.cfg.pt_logp:
+            side.append(([self.s("lnpe1"), self.s("lnpe2")], ["pt"], -1.0))
+        return [("remap_map", [([self.f("delp")], self.cfg.remap_linear(), 1.0)]), ("remap_map_winds", side)]
 
     def moist_pk(self) -> None:
         """Pressure and heat-capacity diagnostics of the remapped state: pe,
@@ -409,15 +432,14 @@ class Dycore:
         over the target layers (pe2 = ak + bk * ps of its thickness), each
         thickness <- its pe2 differences (delp; the winds' are scratch)."""
         coord = [self.grid.abi(self.coord[n], rank=1) for n in ("ak", "bk")]
-        groups = self._remap_groups()
         swapped = []
-        # the scalars' group (10 fields) and the winds' single-field groups in
-        # separate launches (measured: one launch of all three is slower)
-        for node, launch in (("remap_map", groups[:1]), ("remap_map_winds", groups[1:])):
+        # the scalars' group (9 or 10 fields) and the single-field groups in
+        # separate launches (measured: one launch of all of them is slower)
+        for node, launch in self._map_launches():
             fields, counts = list(coord), []
-            for thick, names in launch:
-                counts.append(float(len(names)))
-                fields.append(thick)
+            for thick, names, sign in launch:
+                counts.append(sign * len(names))
+                fields += thick
                 for q in names:
                     fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4"), self.a(q)]
                     swapped.append(q)
@@ -574,4 +596,5 @@ KERNELS = {"fv3b_c_grid": 3, "fv3b_d_sw": 2}
 
 def kernels_per_step(cfg: RunConfig) -> int:
     per_sub = 3 + KERNELS["fv3b_c_grid"] + KERNELS["fv3b_d_sw"] + 1 + 1
-    return cfg.n_split * per_sub + 1 + 1 + 2 + 2 + 1  # tracer halo, tracer_2d, face thickness + profiles, maps, moist_pk
+    # tracer halo, tracer_2d, face thickness (+ log thickness) + profiles, maps, moist_pk
+    return cfg.n_split * per_sub + 1 + 1 + 2 + int(cfg.pt_logp) + 2 + 1

@@ -35,6 +35,9 @@ def unique_bytes(program: str, domain) -> tuple[int, str]:
     if program == "remap_faces":  # fv3b_face_thickness: delp read, du / dv written
         ni, nj, nk = domain[:3]
         return 8 * 3 * ni * nj * nk, "analytic (each operand level once)"
+    if program == "remap_logp":  # fv3b_log_thickness: delp read; dlnp, lnpe1, lnpe2 written
+        ni, nj, nk = domain[:3]
+        return 8 * ni * nj * (2 * nk + 2 * (nk + 1)), "analytic (each operand level once)"
     if program == "moist_pk":  # delp + moist tracers read; pe, peln, pk (interfaces), pkz, cvm written
         ni, nj, nki, nw = domain
         return 8 * ni * nj * ((1 + nw) * (nki - 1) + 3 * nki + 2 * (nki - 1)), "analytic (each operand level once)"

@@ -113,3 +113,107 @@ def test_transpose_round_trip_bitwise():
     d._transpose(d._window(d.cur["pt"]), back)
     torch.cuda.synchronize()
     assert torch.equal(back, src)
+
+
+def _grid_fields(ni, nj, nk):
+    from paper_2205_04148_b200.device import Grid
+
+    return Grid(ni, nj, nk, halo=3)
+
+
+def _log_coordinate(g, td, ak, bk, nk):
+    """fv3b_log_thickness on device delp ``td``: (dlnp, lnpe1, lnpe2) tensors."""
+    import torch
+
+    from paper_2205_04148_b200 import _lib
+
+    out = [g.new3("cuda") for _ in range(3)]
+    coord = [torch.from_numpy(x).cuda() for x in (ak, bk)]
+    _lib.call("fv3b_log_thickness", [g.abi(td)] + [g.abi(c, rank=1) for c in coord] + [g.abi(t) for t in out], [],
+              g.domain(nk=nk), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("ni,nj,nk,seed", [(32, 8, 16, 1), (37, 5, 80, 2), (1, 1, 3, 3)])
+def test_log_thickness_bitwise_vs_oracle(ni, nj, nk, seed):
+    """fv3b_log_thickness: log(pe1), log(pe2) of the running-sum interfaces
+    and the target coordinate, and dlnp their layer differences
+    (oracle/remap_map.py log_edges / log_thickness)."""
+    import torch
+
+    from paper_2205_04148_b200.config import RunConfig
+
+    delp, _ = _case(ni, nj, nk, 0, seed, 0.6)
+    ak, bk = RunConfig(ni=ni, nj=nj, nk=nk).target_coordinate()
+    g = _grid_fields(ni, nj, nk)
+    td = g.new3("cuda")
+    g.interior(td, nk)[...] = torch.from_numpy(np.ascontiguousarray(delp.transpose(2, 1, 0)))
+    tl, t1, t2 = _log_coordinate(g, td, ak, bk, nk)
+    down = lambda t, n: g.interior(t, n).cpu().numpy().transpose(2, 1, 0)
+    pe1, pe2 = rm.pe_edges(delp, ak, bk, nk)
+    l1, l2 = rm.log_edges(pe1, pe2)
+    assert np.array_equal(down(tl, nk), rm.log_thickness(delp, ak, nk))
+    assert np.array_equal(down(t1, nk + 1), l1)
+    assert np.array_equal(down(t2, nk + 1), l2)
+
+
+@pytest.mark.parametrize("ni,nj,nk,nq,spread,seed", [(32, 8, 16, 1, 0.3, 1), (37, 5, 24, 2, 0.9, 2),
+                                                     (48, 48, 80, 1, 0.5, 3)])
+def test_remap_map_log_group_bitwise_vs_oracle(ni, nj, nk, nq, spread, seed):
+    """A log-pressure group (negative group size: FV3's pt with kord_tm < 0,
+    its slot holding log(pe1) then log(pe2)) beside a linear group: the log
+    group maps on log(pe1) -> log(pe2) and rewrites nothing; the linear
+    group maps and rewrites its thickness."""
+    import torch
+
+    from paper_2205_04148_b200 import _lib
+    from paper_2205_04148_b200.config import RunConfig
+
+    delp, qs = _case(ni, nj, nk, nq, seed, spread)
+    other, qo = _case(ni, nj, nk, 1, seed + 10, spread)
+    ak, bk = RunConfig(ni=ni, nj=nj, nk=nk).target_coordinate()
+    g = _grid_fields(ni, nj, nk)
+
+    def up(a):
+        t = g.new3("cuda")
+        g.interior(t, nk)[...] = torch.from_numpy(np.ascontiguousarray(a.transpose(2, 1, 0)))
+        return t
+
+    td, tother = up(delp), up(other)
+    _, t1, t2 = _log_coordinate(g, td, ak, bk, nk)
+    tq = [[up(x) for x in qq] for qq in qs]
+    tqo = [up(x) for x in qo[0]]
+    tout = [g.new3("cuda") for _ in qs]
+    tout2 = g.new3("cuda")
+    coord = [torch.from_numpy(x).cuda() for x in (ak, bk)]
+    fields = [g.abi(c, rank=1) for c in coord] + [g.abi(t1), g.abi(t2)]
+    for qq, o in zip(tq, tout):
+        fields += [g.abi(x) for x in qq] + [g.abi(o)]
+    fields.append(g.abi(tother))
+    fields += [g.abi(x) for x in tqo] + [g.abi(tout2)]
+    _lib.call("fv3b_remap_map", fields, [-float(nq), 1.0], g.domain(nk=nk + 1), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    down = lambda t, n=nk: g.interior(t, n).cpu().numpy().transpose(2, 1, 0)
+    pe1, pe2 = rm.pe_edges(delp, ak, bk, nk)
+    l1, l2 = rm.log_edges(pe1, pe2)
+    for t, (q, a2, a3, a4) in enumerate(qs):
+        assert np.array_equal(down(tout[t]), rm.map_columns(l1, l2, q, a2, a3, a4, nk)), t
+    assert np.array_equal(down(t1, nk + 1), l1) and np.array_equal(down(td), delp)  # nothing rewritten
+    p1, p2 = rm.pe_edges(other, ak, bk, nk)
+    q, a2, a3, a4 = qo[0]
+    assert np.array_equal(down(tout2), rm.map_columns(p1, p2, q, a2, a3, a4, nk))
+    assert np.array_equal(down(tother), p2[..., 1:] - p2[..., :-1])
+
+
+def test_remap_map_rejects_log_group_without_its_target_interfaces():
+    import torch
+
+    from paper_2205_04148_b200 import _lib
+
+    g = _grid_fields(8, 8, 4)
+    t = [g.new3("cuda") for _ in range(6)]
+    ak = torch.zeros(5, dtype=torch.float64, device="cuda")
+    fields = [g.abi(ak, rank=1), g.abi(ak, rank=1), g.abi(t[0])] + [g.abi(x) for x in t[1:6]]
+    with pytest.raises(_lib.Fv3bError):
+        _lib.call("fv3b_remap_map", fields, [-1.0], g.domain(nk=5), torch.cuda.current_stream().cuda_stream)

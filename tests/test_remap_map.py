@@ -66,3 +66,26 @@ def test_constant_is_preserved_and_identity_coordinate():
     a2, a3, a4 = _profile(q, delp, nk)
     q3 = rm.map_columns(pe1, pe1, q, a2, a3, a4, nk)
     assert np.allclose(q3, q, rtol=1e-12)
+
+
+def test_log_pressure_mapping_conserves_and_preserves_constants():
+    """The log-pressure mapping (FV3 pt, kord_tm < 0): map1_ppm on the log
+    interfaces conserves the column integral of q d(log p) and maps a
+    constant profile exactly; log_thickness is the difference of the log
+    interfaces."""
+    from paper_2205_04148_b200.config import RunConfig
+
+    nk = 24
+    delp, q = _columns(64, nk, 5)
+    ak, bk = RunConfig(nk=nk).target_coordinate()
+    pe1, pe2 = rm.pe_edges(delp, ak, bk, nk)
+    l1, l2 = rm.log_edges(pe1, pe2)
+    assert np.array_equal(rm.log_thickness(delp, ak, nk), l1[..., 1:] - l1[..., :-1])
+    assert np.array_equal(l1[..., 0], l2[..., 0]) and np.array_equal(l1[..., -1], l2[..., -1])
+    a2, a3, a4 = _profile(q, delp, nk)
+    q2 = rm.map_columns(l1, l2, q, a2, a3, a4, nk)
+    before = (q * (l1[..., 1:] - l1[..., :-1])).sum(axis=-1)
+    after = (q2 * (l2[..., 1:] - l2[..., :-1])).sum(axis=-1)
+    assert np.allclose(after, before, rtol=1e-12)
+    c = np.full_like(q, 3.25)
+    assert np.allclose(rm.map_columns(l1, l2, c, c, c, np.zeros_like(c), nk), 3.25, rtol=1e-14)

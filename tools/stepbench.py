@@ -7,8 +7,9 @@ from paper_2205_04148_b200.config import RunConfig
 from paper_2205_04148_b200.dycore import Dycore
 from paper_2205_04148_b200.state import initial_state
 
-ni = int(sys.argv[1]) if len(sys.argv) > 1 else 192
-cfg = RunConfig(ni=ni, nj=ni, nk=80)
+args = [a for a in sys.argv[1:] if not a.startswith('--')]
+ni = int(args[0]) if args else 192
+cfg = RunConfig(ni=ni, nj=ni, nk=80, pt_logp='--linear-pt' not in sys.argv)
 t = time.time()
 d = Dycore(cfg, initial_state(cfg))
 print("init", time.time() - t, flush=True)

@@ -55,10 +55,12 @@ def programs(seq):
             key = "tracer_2d"
         elif "remap_kernel" in name:
             key = "remap_tracers"
-        elif "remap_map" in name:
+        elif "remap_map" in name:  # (the scalars' launch, then the winds' and pt's)
             key = "remap_map_winds" if "remap_map" in prog else "remap_map"
         elif "face_thickness" in name:
             key = "remap_faces"
+        elif "log_thickness" in name:
+            key = "remap_logp"
         elif "halo" in name:
             key = "halo"
         else:
