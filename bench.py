@@ -54,20 +54,55 @@ UNIT = "cells/s"
 # CPU path: the oracle restatement of run_reference on host cores
 # ---------------------------------------------------------------------------
 
-def _cpu_tile(args):
-    os.environ["OMP_NUM_THREADS"] = "1"
-    ni, nj, nk, steps = args
+class _HostGrid:
+    """What DecomposedHalo / TorchPacker need from a Grid, for (K, J, I)
+    views of the oracle's (I, J, K) state arrays (uniform halo, no pre-pad)."""
+
+    def __init__(self, ni, nj, h):
+        self.ni, self.nj, self.halo, self.i0 = ni, nj, h, h
+
+
+class _HostRank:
+    """What DecomposedHalo needs from a Dycore: grid, cur, device."""
+
+    def __init__(self, grid):
+        self.grid, self.cur, self.device, self.timer = grid, {}, "cpu", None
+
+
+def _cpu_rank(rank, world, port, px, py, nk, steps, warmup, q):
+    """One host process of the CPU arm: the oracle step on this rank's
+    block of the 192x192 domain, the halos exchanged with the neighbour
+    blocks over gloo at every halo point (DecomposedHalo + DistTransport)."""
+    os.environ.update(OMP_NUM_THREADS="1", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     sys.path.insert(0, str(ROOT))
+    import torch
+    import torch.distributed as dist
+
     from oracle.dycore import OracleDycore
     from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.parallel import DecomposedHalo, DistTransport, TorchPacker
     from paper_2205_04148_b200.state import initial_state
 
-    cfg = RunConfig(ni=ni, nj=nj, nk=nk)
-    d = OracleDycore(cfg, initial_state(cfg))
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        d.step()
-    return time.perf_counter() - t0
+    torch.set_num_threads(1)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = RunConfig(ni=192 // px, nj=192 // py, nk=nk)
+        st = initial_state(cfg)  # the block's own synthetic state (as the GPU ranks of bench.py)
+        od = OracleDycore(cfg, st)
+        host = _HostRank(_HostGrid(cfg.ni, cfg.nj, cfg.halo))
+        halo = DecomposedHalo(host, px, py, rank, transport=DistTransport(rank), packer=TorchPacker(host.grid))
+        t0 = None
+        for it in range(warmup + steps):
+            if it == warmup:  # the timed steps start together
+                dist.barrier()
+                t0 = time.perf_counter()
+            for names in od.phases():
+                host.cur = {n: torch.from_numpy(st[n]).permute(2, 1, 0) for n in names}
+                halo.update(names)
+        dist.barrier()
+        q.put((rank, time.perf_counter() - t0))
+    finally:
+        dist.destroy_process_group()
 
 
 def cpu_tiles(cores: int, ni=192, nj=192, min_tile=32):
@@ -80,26 +115,37 @@ def cpu_tiles(cores: int, ni=192, nj=192, min_tile=32):
     return best
 
 
-def cpu_run(steps: int, nk=80, tile=None, cores=None):
-    """Run ``steps`` oracle timesteps on P processes, one doubly periodic tile
-    each; returns (cells/s, cores, sample)."""
-    import multiprocessing as mp
+def cpu_run(steps: int, nk=80, cores=None, warmup: int = 0):
+    """``steps`` C2 timesteps of the whole 192 x 192 x nk doubly periodic
+    domain on the host: the oracle (oracle/dycore.py, pinned bitwise to the
+    reference's run_reference) on px x py blocks, one process per block,
+    halos exchanged between them over gloo at every halo point of the step;
+    returns (cells/s, processes, sample)."""
+    import socket
+
+    import torch.multiprocessing as mp
 
     cores = cores or os.cpu_count() or 1
     px, py = cpu_tiles(cores)
-    ti, tj = tile or (192 // px, 192 // py)
     nproc = px * py
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
     ctx = mp.get_context("spawn")
+    q = ctx.Queue()
     t0 = time.perf_counter()
-    with ctx.Pool(nproc) as pool:
-        times = pool.map(_cpu_tile, [(ti, tj, nk, steps)] * nproc)
+    procs = [ctx.Process(target=_cpu_rank, args=(r, nproc, port, px, py, nk, steps, warmup, q)) for r in range(nproc)]
+    for p in procs:
+        p.start()
+    times = dict(q.get(timeout=1800) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
     wall = time.perf_counter() - t0
-    # cells/s over the compute itself (the slowest process; pool start-up excluded)
-    t = max(times)
-    cells = nproc * ti * tj * nk * steps
-    sample = (f"{steps} full timestep(s) (n_split=6, nq=8) of {nproc} independent doubly periodic "
-              f"{ti}x{tj}x{nk} tiles, one per process ({nproc * ti}x{tj}x{nk} cells total; tile-local "
-              f"periodic halos, no inter-process exchange); slowest process {t:.1f} s, wall {wall:.1f} s")
+    t = max(times.values())  # between barriers: the job's step time (process start-up excluded)
+    cells = 192 * 192 * nk * steps
+    sample = (f"{steps} full C2 timestep(s) (n_split=6, nq=8; after {warmup} untimed) of the 192x192x{nk} doubly periodic domain, "
+              f"decomposed {px}x{py} into {192 // px}x{192 // py} blocks on {nproc} host processes (one core each), "
+              f"halos exchanged over gloo at every halo point; {t:.1f} s between barriers, wall {wall:.1f} s")
     return cells / t, nproc, sample
 
 
@@ -107,20 +153,19 @@ def run_reference_arm(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     K, W = args.steps, args.warmup
-    # bounded: each step is one full C2 timestep decomposed over the host cores
-    # (tiles >= 32x32); per-step CPU time ~ (192*192*80 / cores) / 25e3 s
-    rates = []
-    for i in range(W + K):
-        v, cores, sample = cpu_run(1)
-        if i >= W:
-            rates.append(v)
-    v = statistics.median(rates)
+    # each step is one full C2 timestep of the 192x192x80 domain decomposed
+    # over the host cores (blocks >= 32x32, gloo halo exchanges); about 7 s
+    # per step on 16 cores, so the sample is bounded at 8 timed steps after
+    # at most one untimed one (the run ends within a few minutes)
+    v, cores, sample = cpu_run(min(K, 8), warmup=min(W, 1))
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": W, "ms_per_step": 192 * 192 * 80 / v * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": W, "ms_per_step": 192 * 192 * 80 / v * 1e3, "higher_is_better": True,
+        "scaling": "weak" if args.config == "c2" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2 doubly periodic 192x192x80 fp64 dycore timestep (n_split=6, nq=8)",
-                   "ni": 192, "nj": 192, "nk": 80, "decomposition": "CPU: tiles over host processes"},
+        "config": workload_of(args, world),
+        "method": {"timing": "host wall clock between barriers, max over the host processes",
+                   "engine": "the oracle (NumPy restatement of run_reference, pinned bitwise to it) on the host cores"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -202,6 +247,31 @@ class LaunchTimer:
         for n, a, b in self.ev:
             out.setdefault(n, []).append(a.elapsed_time(b) * 1e-3)
         return out
+
+
+def workload_of(args, world: int) -> dict:
+    """The line's ``config``: the workload of a bench config at ``world``
+    ranks (shared by both arms, so their configs are the same dict)."""
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.parallel import grid_shape
+
+    l2 = "state > 126 MB L2 per GPU (no flush)"
+    if args.config == "c3":
+        n, nk = args.c3_n, args.nk
+        cfg = RunConfig(ni=n, nj=n, nk=nk)
+        return {"workload": f"C3 cubed sphere C{n} L{nk}, 6 FULL_TILE tiles, edge rotation + corner fill (n_split=6, nq=8)",
+                "name": "c3", "ni": n, "nj": n, "nk": nk, "n_split": cfg.n_split, "nq": cfg.nq,
+                "decomposition": "6 tiles on 1 GPU" if world == 1 else "6 tiles on 6 GPUs", "l2": l2}
+    px, py = grid_shape(world)
+    if args.config == "c4":
+        N = args.c4_n
+        cfg = RunConfig(ni=N // px, nj=N // py, nk=args.nk)
+        workload = f"C4 doubly periodic {N}x{N}x{args.nk} fp64 dycore timestep split {px}x{py} (n_split=6, nq=8)"
+    else:
+        cfg = RunConfig(ni=args.ni, nj=args.ni, nk=args.nk)
+        workload = f"C2 doubly periodic {args.ni}x{args.ni}x{args.nk} fp64 dycore timestep per GPU (n_split=6, nq=8)"
+    return {"workload": workload, "name": args.config, "ni": cfg.ni, "nj": cfg.nj, "nk": cfg.nk,
+            "n_split": cfg.n_split, "nq": cfg.nq, "decomposition": f"{px}x{py}", "l2": l2}
 
 
 class Setup:
@@ -496,10 +566,8 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": su.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded analytic state, state.py)",
-        "config": {"workload": su.workload, "name": args.config,
-                   "ni": cfg.ni, "nj": cfg.nj, "nk": cfg.nk, "n_split": cfg.n_split, "nq": cfg.nq,
-                   "decomposition": su.decomposition, "l2": "state > 126 MB L2 per GPU (no flush)",
-                   "halo": su.halo, "halo_overlap": overlap and len(dycores) == 1,
+        "config": workload_of(args, world),
+        "method": {"halo": su.halo, "halo_overlap": overlap and len(dycores) == 1,
                    "timing": ("CUDA-graph replay of whole timesteps" if graphs else "eager launches, NCCL halo exchange") + ", CUDA events, max over ranks"},
         "e2e": {"value": cells / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
