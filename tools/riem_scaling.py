@@ -10,7 +10,7 @@ import torch
 from paper_2205_04148_b200.executor.scheduled import benchmark
 from paper_2205_04148_b200.inputs import synthetic_inputs
 
-for ni, nj in ((192, 192), (384, 192), (384, 384)):
+for ni, nj in [tuple(map(int, a.split("x"))) for a in sys.argv[1:]] or ((192, 192), (384, 192), (384, 384)):
     dom = (ni, nj, 81)
     r = benchmark("riem_solver_c", synthetic_inputs("riem_solver_c", dom, 1), dom, reps=10)
     print(ni * nj, "columns:", {k: round(v.median * 1e6, 1) if hasattr(v, "median") else v for k, v in r.kernels.items()}, "us")
