@@ -308,7 +308,8 @@ def setup_config(args, rank: int, world: int) -> Setup:
         if world == 1:
             tiles = [Dycore(cfg, initial_state(RunConfig(ni=n, nj=n, nk=nk, seed=2205 + t)), placement=(True,) * 4)
                      for t in range(6)]
-            cl = LoopbackCluster(tiles, halos=[CubeHalo(d, t, transport=None) for t, d in enumerate(tiles)])
+            cl = LoopbackCluster(tiles, halos=[CubeHalo(d, t, transport=None) for t, d in enumerate(tiles)],
+                                 concurrent=True)  # (the six tiles' kernels share the GPU)
             return Setup(cl, tiles, 6 * cfg.cells, "strong", workload, "6 tiles on 1 GPU",
                          "cube rotation + corner fill, device copies (loopback)", True)
         if world != 6:

@@ -512,7 +512,7 @@ class LoopbackCluster:
     validation of the decomposed path)."""
 
     def __init__(self, dycores, px: int = 1, py: int = 1, halos=None, direct: bool = False,
-                 flag_sync: bool = False):
+                 flag_sync: bool = False, concurrent: bool = False):
         """``halos``: per-rank halo objects exposing pack / finish (default:
         a px x py doubly periodic decomposition; cubesphere.CubeHalo for
         the six tiles of a cube; ``cubesphere.CubePeerHalo`` for its
@@ -525,9 +525,14 @@ class LoopbackCluster:
         streams must land on distinct hardware queues (at most
         CUDA_DEVICE_MAX_CONNECTIONS streams), or one rank's spinning barrier
         blocks a neighbour's arrival queued behind it until the barrier's
-        10 s bound expires."""
+        10 s bound expires.  ``concurrent``: every rank's programs between
+        two halo points on its own stream, joined before each exchange and
+        forked after it (stream order only, no device barriers), so the
+        ranks' kernels share the GPU -- the six small cube tiles of C3 on
+        one device fill it together instead of one after another."""
         self.d = dycores
         self.streams = None
+        self.cstreams = [torch.cuda.Stream() for _ in dycores] if concurrent and not flag_sync else None
         if direct and halos is None:
             self.halos = []
             flags = [new_flags(len(dycores), d.device) for d in dycores] if flag_sync else None
@@ -604,13 +609,16 @@ class LoopbackCluster:
     def _on(self, r: int):
         import contextlib
 
-        return torch.cuda.stream(self.streams[r]) if self.streams else contextlib.nullcontext()
+        ranks = self.streams or self.cstreams
+        return torch.cuda.stream(ranks[r]) if ranks else contextlib.nullcontext()
 
     def step(self) -> None:
         gens = [d.phases() for d in self.d]
-        if self.streams:
-            for s in self.streams:
-                s.wait_stream(torch.cuda.current_stream())
+        main = torch.cuda.current_stream()
+        ranks = self.streams or self.cstreams
+        if ranks:
+            for s in ranks:
+                s.wait_stream(main)
         while True:
             reqs = []
             for r, g in enumerate(gens):
@@ -619,7 +627,14 @@ class LoopbackCluster:
             if all(r is None for r in reqs):
                 break
             assert all(r is not None for r in reqs), "ranks out of lockstep"
-            self.exchange_all(reqs)
-        if self.streams:
-            for s in self.streams:
-                torch.cuda.current_stream().wait_stream(s)
+            if self.cstreams:  # join the ranks' programs, exchange on the main stream, fork again
+                for s in self.cstreams:
+                    main.wait_stream(s)
+                self.exchange_all(reqs)
+                for s in self.cstreams:
+                    s.wait_stream(main)
+            else:
+                self.exchange_all(reqs)
+        if ranks:
+            for s in ranks:
+                main.wait_stream(s)

@@ -25,8 +25,9 @@ def _cluster(cfg, states, mode="packed"):
     from paper_2205_04148_b200.parallel import FlagSync, LoopbackCluster, new_flags
 
     tiles = [Dycore(cfg, st, placement=(True, True, True, True)) for st in states]
-    if mode == "packed":
-        return tiles, LoopbackCluster(tiles, halos=[CubeHalo(d, t, transport=None) for t, d in enumerate(tiles)])
+    if mode in ("packed", "concurrent"):  # concurrent: each tile's programs on its own stream (bench C3)
+        return tiles, LoopbackCluster(tiles, halos=[CubeHalo(d, t, transport=None) for t, d in enumerate(tiles)],
+                                      concurrent=mode == "concurrent")
     peers = LoopbackTiles(tiles)
     halos = [CubePeerHalo(d, t, peers) for t, d in enumerate(tiles)]
     if mode == "flags":
@@ -69,7 +70,8 @@ def test_cube_halo_matches_oracle(mode):
             assert np.array_equal(got[n], ref[t][n]), (t, n)
 
 
-@pytest.mark.parametrize("mode,graph", [("packed", False), ("packed", True), ("direct", False), ("direct", True)])
+@pytest.mark.parametrize("mode,graph", [("packed", False), ("packed", True), ("direct", False), ("direct", True),
+                                        ("concurrent", False), ("concurrent", True)])
 def test_cube_dycore_matches_oracle_bitwise(mode, graph):
     import torch
 

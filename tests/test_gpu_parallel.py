@@ -49,7 +49,7 @@ def test_device_packer_single_rank_equals_periodic_kernel():
         assert torch.equal(a.cur[n], b.cur[n]), n
 
 
-@pytest.mark.parametrize("mode", ["packed", "direct", "direct-graph"])
+@pytest.mark.parametrize("mode", ["packed", "direct", "direct-graph", "concurrent", "concurrent-graph"])
 @pytest.mark.parametrize("px,py", [(2, 2), (1, 2)])
 def test_loopback_decomposed_dycore_bitwise(px, py, mode):
     """packed: pack / device copy / unpack; direct: PeerHalo
@@ -76,8 +76,10 @@ def test_loopback_decomposed_dycore_bitwise(px, py, mode):
     for r in range(px * py):
         ri, rj = r % px, r // px
         blocks.append(Dycore(blk_cfg, {n: _block(a, ri, rj, ni, nj, h) for n, a in st.items()}))
-    graph = mode == "direct-graph"
-    cluster = LoopbackCluster(blocks, px, py, direct=mode != "packed", flag_sync=mode == "flags")
+    graph = mode.endswith("-graph")
+    conc = mode.startswith("concurrent")  # each rank's programs on its own stream (packed halos)
+    cluster = LoopbackCluster(blocks, px, py, direct=mode.startswith("direct"), flag_sync=mode == "flags",
+                              concurrent=conc)
     if graph:
         cluster.capture()
     for _ in range(2):

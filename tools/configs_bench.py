@@ -66,16 +66,17 @@ def c1():
             "cells_per_s_graph": 48 * 48 * 16 / (msg * 1e-3)}
 
 
-def c3(n=128):
+def c3(n=128, concurrent=True):
     cfg = RunConfig(ni=n, nj=n, nk=80)
     tiles = [Dycore(cfg, initial_state(RunConfig(ni=n, nj=n, nk=80, seed=2205 + t)), placement=(True,) * 4)
              for t in range(6)]
-    cl = LoopbackCluster(tiles, halos=[CubeHalo(d, t, transport=None) for t, d in enumerate(tiles)])
+    cl = LoopbackCluster(tiles, halos=[CubeHalo(d, t, transport=None) for t, d in enumerate(tiles)],
+                         concurrent=concurrent)
     ms = timeit(cl.step, reps=3, warm=1)
     cl.capture()
     msg = timeit(cl.replay, reps=5, warm=2)
     cells = 6 * n * n * 80
-    return {"config": f"C3 cubed sphere C{n} L80, 6 tiles on 1 GPU (loopback halo)", "ms_per_step_eager": ms,
+    return {"config": f"C3 cubed sphere C{n} L80, 6 tiles on 1 GPU (loopback halo{', tiles on concurrent streams' if concurrent else ''})", "ms_per_step_eager": ms,
             "ms_per_step": msg, "ms_per_tile_step": msg / 6, "cells_per_s": cells / (msg * 1e-3)}
 
 
@@ -105,4 +106,7 @@ def c5(n=384):
 if __name__ == "__main__":
     which = sys.argv[1:] or ["c1", "c3", "c4", "c5"]
     for w in which:
+        if w == "c3-serial":
+            print(json.dumps(c3(concurrent=False)), flush=True)
+            continue
         print(json.dumps(globals()[w]()), flush=True)
