@@ -92,3 +92,50 @@ def test_tuning_table_roundtrip(tmp_path, monkeypatch, lib):
         assert _lib.tune_get("kchunk_csw") == 20
     finally:
         _lib.tune_set("kchunk_csw", 0)
+
+
+def _host_field(arr, halo=0):
+    """A host array as an ABI field (validation only: nothing is launched)."""
+    f = _lib.Field()
+    f.data = arr.ctypes.data
+    nk, nj, ni = arr.shape
+    f.stride[:] = [1, ni, ni * nj]
+    f.shape[:] = [ni, nj, nk]
+    f.halo_lo[:] = [halo, halo, 0]
+    f.rank = 3
+    return f
+
+
+def test_buffer_fields_are_checked(lib):
+    """ABI v5: message buffers, index lists and flag words travel as rank-1
+    buffer fields; a rank other than 1, a null address or too small a
+    capacity is rejected before any launch (so this runs on CPU)."""
+    import numpy as np
+
+    dom = _lib.Domain()
+    dom.ni, dom.nj, dom.nk = 8, 8, 4
+    field = np.zeros((5, 16, 16))
+    small = np.zeros(4)
+    f = _host_field(field, halo=4)
+    stream = None
+
+    def call(name, fields, scalars):
+        farr = (_lib.Field * len(fields))(*fields)
+        sarr = (ctypes.c_double * max(1, len(scalars)))(*scalars)
+        return _lib.entry(name)(farr, len(fields), sarr, len(scalars), ctypes.byref(dom), stream)
+
+    # a strip of 4 x 1 cells over 5 levels needs 20 doubles
+    rc = call("fv3b_halo_pack", [f, _lib.buffer_field(small.ctypes.data, small.size)], [0, 0, 4, 1])
+    assert rc < 0 and "needs" in lib.fv3b_last_error().decode()
+    rc = call("fv3b_halo_pack", [f, _host_field(field)], [0, 0, 4, 1])  # a rank-3 field as the buffer
+    assert rc < 0 and "rank-1" in lib.fv3b_last_error().decode()
+    # one rectangle of 2 x 2 at offset 0, one field of 5 levels: 20 doubles
+    rc = call("fv3b_halo_pack_rects", [f, _lib.buffer_field(small.ctypes.data, small.size)], [1, 0, 0, 2, 2, 0])
+    assert rc < 0 and "needs" in lib.fv3b_last_error().decode()
+    # gather: 3 entries over 5 levels need 15 doubles and 6 int32
+    rc = call("fv3b_halo_gather", [f, _lib.buffer_field(small.ctypes.data, small.size),
+                                   _lib.buffer_field(small.ctypes.data, 8)], [3])
+    assert rc < 0 and "needs" in lib.fv3b_last_error().decode()
+    # the barrier's words: a null address
+    rc = call("fv3b_peer_barrier", [_lib.buffer_field(0, 1), _lib.buffer_field(small.ctypes.data, 1)], [1, 0])
+    assert rc < 0 and "non-null" in lib.fv3b_last_error().decode()
