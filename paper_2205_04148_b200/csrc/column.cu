@@ -101,42 +101,69 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// The ring is addressed by 32-bit shared-window byte offsets (no generic ->
+// shared conversion per copy, immediate field offsets in LDGSTS / LDS).
+__device__ __forceinline__ void cp_async8_s(uint32_t dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ double lds64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+
 template <int NF, class T, class UseF>
 __device__ __forceinline__ void staged(double* ring, int n, Stream<NF> st, UseF use) {
-  constexpr int SS = NF * NC_MAX;  // doubles per slot
-  double* const last = ring + (RD - 1) * SS;
-  double* wr = ring;  // next slot to fill
+  constexpr uint32_t SSB = NF * NC_MAX * sizeof(double);  // bytes per slot
+  constexpr uint32_t FB = NC_MAX * sizeof(double);         // bytes between a slot's fields
+  const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+  const uint32_t last = base + (RD - 1) * SSB;
+  uint32_t wr = base;  // next slot to fill
   auto fill = [&]() {
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
-      cp_async8(wr + f * NC_MAX, st.p[f]);
+      cp_async8_s(wr + f * FB, st.p[f]);
       st.p[f] += st.d[f];
     }
-    wr = wr == last ? ring : wr + SS;
+    wr = wr == last ? base : wr + SSB;
+  };
+  uint32_t rp = base;  // next slot to read
+  auto read = [&]() {
+    T v;
+    if constexpr (NF == 1) v = T{lds64(rp)};
+    else if constexpr (NF == 2) v = T{lds64(rp), lds64(rp + FB)};
+    else v = T{lds64(rp), lds64(rp + FB), lds64(rp + 2 * FB)};
+    rp = rp == last ? base : rp + SSB;
+    return v;
   };
 #pragma unroll
   for (int s = 0; s < RD; ++s) {
     if (s < n) fill();
     cp_async_commit();
   }
-  const double* rp = ring;  // next slot to read
+  // main batches: every step's refill (step s + RD) exists, so no guards
+  int s0 = 0;
 #pragma unroll 1
-  for (int s0 = 0; s0 < n; s0 += RU) {
+  for (; s0 + RU <= n - RD; s0 += RU) {
     cp_async_wait<RD - RU>();  // the batch's RU groups have landed
     T v[RU];
 #pragma unroll
-    for (int u = 0; u < RU; ++u) {
-      if constexpr (NF == 1) v[u] = T{rp[0]};
-      else if constexpr (NF == 2) v[u] = T{rp[0], rp[NC_MAX]};
-      else v[u] = T{rp[0], rp[NC_MAX], rp[2 * NC_MAX]};
-      rp = rp == last ? ring : rp + SS;
-    }
+    for (int u = 0; u < RU; ++u) v[u] = read();
 #pragma unroll
     for (int u = 0; u < RU; ++u) {
-      if (s0 + u < n) use(s0 + u, v[u]);
-      if (s0 + u + RD < n) fill();  // into a slot this batch has read
+      use(s0 + u, v[u]);
+      fill();  // into a slot this batch has read
       cp_async_commit();
     }
+  }
+  // the last < RD + RU steps, one group per step (empty once the refills end)
+#pragma unroll 1
+  for (; s0 < n; ++s0) {
+    cp_async_wait<RD - 1>();
+    const T v = read();
+    use(s0, v);
+    if (s0 + RD < n) fill();
+    cp_async_commit();
   }
   cp_async_wait<0>();
 }
