@@ -73,6 +73,22 @@ def test_cuda_matches_oracle(engine, name, domain, tile, seed):
     assert_outputs_equal(got, ref, rtol=RTOL.get(name, 0.0))
 
 
+@pytest.mark.parametrize("name", ["riem_solver_c", "nh_d"])
+@pytest.mark.parametrize("nk", list(range(5, 16)) + [26, 27])
+def test_cuda_riem_level_counts(engine, name, nk):
+    """The column sweeps stream their operands through an 8-level ring in
+    batches of 2 with a one-step epilogue (column.cu staged()): every split of
+    a pass's n = nk - 3 .. nk - 1 steps between the guard-free batches and the
+    epilogue (none, even and odd batch counts, ring shorter than a pass)."""
+    from paper_2205_04148_b200.inputs import synthetic_inputs
+
+    domain = (33, 5, nk)
+    inputs = synthetic_inputs(name, domain, 400 + nk)
+    got = engine.run_b200(name, inputs, domain, placement=(True,) * 4)
+    ref = interp.run_program(name, inputs, domain, interp.Placement(True, True, True, True))
+    assert_outputs_equal(got, ref)
+
+
 @pytest.mark.parametrize("name", ["riem_solver_c", "remap_profile"])
 def test_cuda_column_full_size_c2(engine, name):
     """192x192 columns x 80 layers (program domain nk = 81) vs the oracle."""
