@@ -172,8 +172,8 @@ __device__ __forceinline__ void staged(double* ring, int n, Stream<NF> st, UseF 
 #define FV3B_PF 4
 #define FV3B_PFS 12
 #endif
-constexpr int PF = FV3B_PF;    // prefetch distance (levels), riem passes with long bodies (A, C)
-constexpr int PFS = FV3B_PFS;  // riem passes with short bodies (B, D, E, F): L2-resident staging reads
+[[maybe_unused]] constexpr int PF = FV3B_PF;    // prefetch distance (levels), riem passes with long bodies (A, C)
+[[maybe_unused]] constexpr int PFS = FV3B_PFS;  // riem passes with short bodies (B, D, E, F): L2-resident staging reads
 
 // Statement-for-statement restatement of templates.riem_stencils for one
 // column.  FAST: branch-free divisions/logs (fastdiv.cuh), returns false if
@@ -194,11 +194,9 @@ constexpr int PFS = FV3B_PFS;  // riem passes with short bodies (B, D, E, F): L2
 template <bool FAST>
 __device__ __forceinline__ bool riem_column(const RiemArgs& a, int i, int j, int c, int NC, double* sm) {
   ColArith<FAST> ar;
-  const int nk = a.nk, L = nk + 1;
+  const int nk = a.nk;
   double* S0 = sm + c;  // pp -> w2 -> pe2 (shifted one level down)
-#ifdef FV3B_RIEM_REGRING
-  (void)L;
-#else
+#ifndef FV3B_RIEM_REGRING
   double* ring = sm - RING + c;  // staged() operand ring (RD levels x 3) below S0
 #endif
 #define AT(S, k) (S)[(k) * NC]
@@ -421,7 +419,9 @@ __device__ __noinline__ void riem_exact(const RiemArgs& a, int i, int j, int c, 
 }
 #endif
 
-__global__ void __launch_bounds__(NC_MAX) riem_kernel(const RiemArgs a) {
+// (minBlocks 1: without it ptxas settles on 128 registers and spills; 177
+// registers cost no residency, which shared memory caps at 8 CTAs per SM)
+__global__ void __launch_bounds__(NC_MAX, 1) riem_kernel(const RiemArgs a) {
   extern __shared__ double sm_[];
 #ifdef FV3B_RIEM_REGRING
   double* sm = sm_;
