@@ -37,7 +37,13 @@ constexpr int SEG = 4;  // cells per sliding-window segment
 // threads per CTA / CTAs per SM by tile height (>= phase-A items): 32x16
 // tiles one CTA of 11 warps, 32x8 tiles two CTAs of 8 warps
 template <int TJ> constexpr int nt_of() { return TJ >= 16 ? 352 : 256; }
-template <int TJ> constexpr int cps_of() { return 2; }
+// two CTAs per SM cap tp_kernel<32,16> at 93 registers, and ptxas spills
+// 24 B (L1-resident); one CTA per SM removes the spill but measured slower
+// (C2 fv_tp_2d 82 vs 74 us, 384x384x80 306 vs 265 us)
+#ifndef FV3B_TP_CPS
+#define FV3B_TP_CPS 2
+#endif
+template <int TJ> constexpr int cps_of() { return FV3B_TP_CPS; }
 
 struct TpArgs {
   CUtensorMap q[NQMAX];
