@@ -205,6 +205,7 @@ class Dycore:
         if getattr(self, "_up", None) is None:
             self._up, self._down, self._xs = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
             self._io_calls, self._prev_out, self._prev_done, self._prev_x = 0, set(), None, None
+            self._dl_events = {}  # host data_ptr -> the last call's download event of that buffer
         return self._up, self._down
 
     def step_host(self, h_in: dict[str, torch.Tensor], h_out: dict[str, torch.Tensor]) -> torch.cuda.Event:
@@ -246,14 +247,30 @@ class Dycore:
         in_free, out_free = self._io_free
         if in_free[si] is not None:  # consumed by the compute three calls ago
             up.wait_event(in_free[si])
-        if self._prev_done is not None and self._prev_out & {t.data_ptr() for t in h_in.values()}:
-            up.wait_event(self._prev_done)
+        # a chained call (inputs are the last call's outputs) moves field by
+        # field: each upload waits only for the download of its own buffer, so
+        # the dynamics fields (downloaded first) travel back up while the
+        # tracers are still coming down, and the compute starts before they land
+        chained = self._prev_done is not None and bool(self._prev_out & {t.data_ptr() for t in h_in.values()})
+        dl = self._dl_events
+
+        def upload(names):
+            if not chained:
+                for dst, src in self._runs(names, sin, h_in):
+                    dst.copy_(src, non_blocking=True)
+                return
+            for n in names:
+                p = h_in[n].data_ptr()
+                if p in dl:
+                    up.wait_event(dl[p])
+                elif p in self._prev_out:
+                    up.wait_event(self._prev_done)
+                sin[n].copy_(h_in[n], non_blocking=True)
+
         with torch.cuda.stream(up):
-            for dst, src in self._runs(dyn, sin, h_in):
-                dst.copy_(src, non_blocking=True)
+            upload(dyn)
             e_dyn = up.record_event()
-            for dst, src in self._runs(trc, sin, h_in):
-                dst.copy_(src, non_blocking=True)
+            upload(trc)
             e_trc = up.record_event()
         # inputs into the other buffer of each pair (the previous outputs stay
         # readable); a field without a second buffer waits for the readers
@@ -275,18 +292,27 @@ class Dycore:
         if out_free[so] is not None:  # downloaded two calls ago
             xs.wait_event(out_free[so])
 
+        new_dl = {}
+
         def out(names):  # device transpose on the transpose stream, download on the download stream
             if not names:
                 return
             xs.wait_event(comp.record_event())
-            with torch.cuda.stream(xs):
-                for n in names:
-                    self._transpose(self._window(self.cur[n]), sout[n])
-            e_out = xs.record_event()
-            down.wait_event(e_out)
-            with torch.cuda.stream(down):
-                for dst, src in self._runs(names, h_out, sout):
-                    dst.copy_(src, non_blocking=True)
+            # one merged download (pipelined calls: the fewest DMAs), or field
+            # by field in a chained integration (see upload)
+            e_out = None
+            for group in ([[n] for n in names] if chained else [names]):
+                with torch.cuda.stream(xs):
+                    for n in group:
+                        self._transpose(self._window(self.cur[n]), sout[n])
+                e_out = xs.record_event()
+                down.wait_event(e_out)
+                with torch.cuda.stream(down):
+                    for dst, src in self._runs(group, h_out, sout):
+                        dst.copy_(src, non_blocking=True)
+                e_dl = down.record_event()
+                for n in group:
+                    new_dl[h_out[n].data_ptr()] = e_dl
             return e_out
 
         tracer_point, consumed, point = set(self.cfg.tracer_names()), False, 0
@@ -309,6 +335,7 @@ class Dycore:
         done = down.record_event()
         out_free[so] = done
         self._prev_done, self._prev_out = done, {t.data_ptr() for t in h_out.values()}
+        self._dl_events = new_dl
         return done
 
     # -- launch helpers -----------------------------------------------------

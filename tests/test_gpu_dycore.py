@@ -107,16 +107,18 @@ def test_checkpoint_restart_is_bitwise(tmp_path):
         assert np.array_equal(a.download([n])[n][h:-h, h:-h, :top], b.download([n])[n][h:-h, h:-h, :top]), n
 
 
-def test_step_host_chained_matches_step():
-    """step_host fed its own previous output (uploads wait for the downloads)
-    == load + step + store chained the same way."""
+@pytest.mark.parametrize("size", ["small", "c2"])
+def test_step_host_chained_matches_step(size):
+    """step_host fed its own previous output (each field's upload waits for
+    that field's download, field by field) == load + step + store chained the
+    same way; at C2 every transfer takes milliseconds, so a missing wait shows."""
     import torch
 
     from paper_2205_04148_b200.config import RunConfig
     from paper_2205_04148_b200.dycore import Dycore
     from paper_2205_04148_b200.state import initial_state
 
-    cfg = RunConfig(ni=32, nj=24, nk=10, n_split=3, dt_atmos=45.0)
+    cfg = RunConfig(ni=32, nj=24, nk=10, n_split=3, dt_atmos=45.0) if size == "small" else RunConfig()
     st = initial_state(cfg)
     a, b = Dycore(cfg, st), Dycore(cfg, st)
     ha, hb = [a.host_buffers(), a.host_buffers()], [b.host_buffers(), b.host_buffers()]
