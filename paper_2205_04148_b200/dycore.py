@@ -461,8 +461,19 @@ class Dycore:
         coord = [self.grid.abi(self.coord[n], rank=1) for n in ("ak", "bk")]
         swapped = []
         # the scalars' group (9 or 10 fields) and the single-field groups in
-        # separate launches (measured: one launch of all of them is slower)
-        for node, launch in self._map_launches():
+        # separate launches (measured: one launch of all of them is slower),
+        # run concurrently: the two read and write disjoint fields (the
+        # scalars rewrite delp; the others map at du, dv and the log-pressure
+        # interfaces), and both column walks are latency-bound at a few warps
+        # per SM, so each fills the other's stalls (step 7.63 -> 7.58 ms).
+        # Under a per-launch timer they run one after the other, so each
+        # launch's events bracket only its own kernel.
+        comp = torch.cuda.current_stream()
+        if getattr(self, "_map_stream", None) is None:
+            self._map_stream = torch.cuda.Stream()
+        fork = comp.record_event()
+        joins = []
+        for idx, (node, launch) in enumerate(self._map_launches()):
             fields, counts = list(coord), []
             for thick, names, sign in launch:
                 counts.append(sign * len(names))
@@ -470,7 +481,16 @@ class Dycore:
                 for q in names:
                     fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4"), self.a(q)]
                     swapped.append(q)
-            self.launch(node, "fv3b_remap_map", fields, counts, self.dom_ifaces)
+            if idx == 0 or self.timer is not None:
+                self.launch(node, "fv3b_remap_map", fields, counts, self.dom_ifaces)
+                continue
+            side = self._map_stream
+            side.wait_event(fork)
+            with torch.cuda.stream(side):
+                self.launch(node, "fv3b_remap_map", fields, counts, self.dom_ifaces)
+                joins.append(side.record_event())
+        for e in joins:
+            comp.wait_event(e)
         self.swap(*swapped)
 
     def phases(self):
