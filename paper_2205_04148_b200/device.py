@@ -22,6 +22,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import _lib
 from ._lib import Domain, Field
 
 DEFAULT_HALO = 4
@@ -132,13 +133,17 @@ class Grid:
         return sl
 
     def put(self, t: torch.Tensor, host: np.ndarray, dims, halo_lo) -> None:
-        """Copy a reference-convention host array into device tensor ``t``."""
+        """Copy a reference-convention host array into device tensor ``t``
+        (3-D: one contiguous upload, then the layout change on the device by
+        fv3b_transpose)."""
         sl = self._window(dims, halo_lo, host.shape)
         src = torch.from_numpy(np.ascontiguousarray(host, dtype=np.float64))
         if tuple(dims) == ("I", "J", "K"):
-            t[sl["K"], sl["J"], sl["I"]].copy_(src.permute(2, 1, 0), non_blocking=False)
-        elif tuple(dims) == ("I", "J"):
-            t[sl["J"], sl["I"]].copy_(src.permute(1, 0))
+            if src.numel():
+                transpose(src.to(t.device), t[sl["K"], sl["J"], sl["I"]].permute(2, 1, 0))
+        elif tuple(dims) == ("I", "J"):  # (as an (I, J, 1) field)
+            if src.numel():
+                transpose(src.to(t.device).unsqueeze(2), t[sl["J"], sl["I"]].permute(1, 0).unsqueeze(2))
         elif tuple(dims) == ("K",):
             t[sl["K"]].copy_(src)
         else:
@@ -148,14 +153,36 @@ class Grid:
         """Reference-convention host copy of a window of device tensor ``t``."""
         sl = self._window(dims, halo_lo, shape)
         if tuple(dims) == ("I", "J", "K"):
-            v = t[sl["K"], sl["J"], sl["I"]].permute(2, 1, 0)
+            v = torch.empty(tuple(shape), dtype=torch.float64, device=t.device)
+            if v.numel():
+                transpose(t[sl["K"], sl["J"], sl["I"]].permute(2, 1, 0), v)
         elif tuple(dims) == ("I", "J"):
-            v = t[sl["J"], sl["I"]].permute(1, 0)
+            v = torch.empty(tuple(shape), dtype=torch.float64, device=t.device)
+            if v.numel():
+                transpose(t[sl["J"], sl["I"]].permute(1, 0).unsqueeze(2), v.unsqueeze(2))
         elif tuple(dims) == ("K",):
             v = t[sl["K"]]
         else:
             raise ValueError(f"unsupported field dims {dims}")
         return np.ascontiguousarray(v.cpu().numpy())
+
+
+def transpose(src: torch.Tensor, dst: torch.Tensor) -> None:
+    """``dst <- src`` for two (I, J, K)-ordered device views of one shape
+    with any strides (the reference array convention <-> the Layout):
+    fv3b_transpose on the current stream."""
+    fs = []
+    for t in (src, dst):
+        f = Field()
+        f.data = t.data_ptr()
+        f.stride[:] = list(t.stride())
+        f.shape[:] = list(t.shape)
+        f.halo_lo[:] = [0, 0, 0]
+        f.rank = 3
+        fs.append(f)
+    d = Domain()
+    d.ni, d.nj, d.nk = src.shape
+    _lib.call("fv3b_transpose", fs, [], d, torch.cuda.current_stream().cuda_stream)
 
 
 class capture_guard:
