@@ -208,6 +208,32 @@ class Dycore:
             self._dl_events = {}  # host data_ptr -> the last call's download event of that buffer
         return self._up, self._down
 
+    def _halo_refreshed(self) -> set[str]:
+        """Fields whose every halo cell a step rewrites before reading one
+        (periodic halo only): the dynamics fields of the first halo point and
+        the tracers of the tracer point."""
+        if not isinstance(self.halo, PeriodicHalo):
+            return set()
+        return {"u", "v", "w", "delp", "pt", "gz"} | set(self.cfg.tracer_names())
+
+    def _interior_rows(self) -> tuple[int, int, int, int]:
+        """(byte offset, row bytes, rows, pitch) of the interior columns of a
+        host array in the reference convention (I, J, K C order, halo h):
+        for each interior i, j in [h, h + nj) over all levels is one
+        contiguous run."""
+        c, h = self.cfg, self.cfg.halo
+        nk1 = c.nk + 1
+        pitch = (c.nj + 2 * h) * nk1 * 8
+        return (h * (c.nj + 2 * h) + h) * nk1 * 8, c.nj * nk1 * 8, c.ni, pitch
+
+    def host_io_bytes(self, h_in: dict[str, torch.Tensor]) -> tuple[int, int]:
+        """(uploaded, downloaded) bytes of one step_host call with these host
+        buffers (the refreshed fields' halos are not uploaded)."""
+        fresh = self._halo_refreshed()
+        _, width, rows, _ = self._interior_rows()
+        up = sum(width * rows if n in fresh else t.numel() * t.element_size() for n, t in h_in.items())
+        return up, sum(t.numel() * t.element_size() for t in h_in.values())
+
     def step_host(self, h_in: dict[str, torch.Tensor], h_out: dict[str, torch.Tensor]) -> torch.cuda.Event:
         """One timestep from pinned host state ``h_in`` to pinned host state
         ``h_out`` (reference array convention, host_buffers()).  Returns an
@@ -253,19 +279,29 @@ class Dycore:
         # tracers are still coming down, and the compute starts before they land
         chained = self._prev_done is not None and bool(self._prev_out & {t.data_ptr() for t in h_in.values()})
         dl = self._dl_events
+        # a periodic domain's first halo points (the substeps' start for the
+        # dynamics fields, the tracer point for the tracers) rewrite every
+        # halo cell of these fields before anything reads one: only their
+        # interior columns travel up (one pitched copy per field, rows of
+        # nj x (nk + 1) values)
+        fresh = self._halo_refreshed()
 
         def upload(names):
-            if not chained:
+            if not chained and not fresh & set(names):
                 for dst, src in self._runs(names, sin, h_in):
                     dst.copy_(src, non_blocking=True)
                 return
             for n in names:
                 p = h_in[n].data_ptr()
-                if p in dl:
+                if chained and p in dl:
                     up.wait_event(dl[p])
-                elif p in self._prev_out:
+                elif chained and p in self._prev_out:
                     up.wait_event(self._prev_done)
-                sin[n].copy_(h_in[n], non_blocking=True)
+                if n in fresh:
+                    off, width, rows, pitch = self._interior_rows()
+                    _lib.memcpy2d(sin[n].data_ptr() + off, pitch, p + off, pitch, width, rows, up.cuda_stream)
+                else:
+                    sin[n].copy_(h_in[n], non_blocking=True)
 
         with torch.cuda.stream(up):
             upload(dyn)
