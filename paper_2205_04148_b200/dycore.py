@@ -217,14 +217,7 @@ class Dycore:
         return {"u", "v", "w", "delp", "pt", "gz"} | set(self.cfg.tracer_names())
 
     def _interior_rows(self) -> tuple[int, int, int, int]:
-        """(byte offset, row bytes, rows, pitch) of the interior columns of a
-        host array in the reference convention (I, J, K C order, halo h):
-        for each interior i, j in [h, h + nj) over all levels is one
-        contiguous run."""
-        c, h = self.cfg, self.cfg.halo
-        nk1 = c.nk + 1
-        pitch = (c.nj + 2 * h) * nk1 * 8
-        return (h * (c.nj + 2 * h) + h) * nk1 * 8, c.nj * nk1 * 8, c.ni, pitch
+        return interior_rows(self.cfg)
 
     def host_io_bytes(self, h_in: dict[str, torch.Tensor]) -> tuple[int, int]:
         """(uploaded, downloaded) bytes of one step_host call with these host
@@ -675,6 +668,17 @@ class Dycore:
 
 # libfv3b kernels launched per entry point (fused entries launch several)
 KERNELS = {"fv3b_c_grid": 3, "fv3b_d_sw": 2}
+
+
+def interior_rows(cfg: RunConfig) -> tuple[int, int, int, int]:
+    """(byte offset, row bytes, rows, pitch) of the interior columns of a
+    step_host array (reference convention: I, J, K C order, halo h, nk + 1
+    levels): for each interior i, j in [h, h + nj) over all levels is one
+    contiguous run."""
+    h = cfg.halo
+    nk1 = cfg.nk + 1
+    pitch = (cfg.nj + 2 * h) * nk1 * 8
+    return (h * (cfg.nj + 2 * h) + h) * nk1 * 8, cfg.nj * nk1 * 8, cfg.ni, pitch
 
 
 def kernels_per_step(cfg: RunConfig) -> int:

@@ -83,3 +83,21 @@ def test_flag_sync_word_addresses():
             remote, local = f[2 + 2 * q].data, f[3 + 2 * q].data
             assert remote == flags[p].data_ptr() + 8 * (phase * world + rank)
             assert local == flags[rank].data_ptr() + 8 * (phase * world + p)
+
+@pytest.mark.parametrize("ni,nj,nk,h", [(192, 192, 80, 4), (32, 24, 10, 4), (7, 5, 3, 2)])
+def test_interior_rows_cover_exactly_the_interior(ni, nj, nk, h):
+    """step_host's pitched interior upload (dycore.interior_rows): the rows
+    of (offset + r * pitch, width) bytes of a reference-convention array are
+    exactly its interior columns over every level, in order."""
+    import numpy as np
+
+    from paper_2205_04148_b200.config import RunConfig
+    from paper_2205_04148_b200.dycore import interior_rows
+
+    cfg = RunConfig(ni=ni, nj=nj, nk=nk, halo=h)
+    a = np.arange((ni + 2 * h) * (nj + 2 * h) * (nk + 1), dtype=np.float64).reshape(ni + 2 * h, nj + 2 * h, nk + 1)
+    flat = a.ravel()
+    off, width, rows, pitch = interior_rows(cfg)
+    assert rows == ni and off % 8 == 0 and width % 8 == 0 and pitch % 8 == 0
+    got = np.stack([flat[(off + r * pitch) // 8:(off + r * pitch + width) // 8] for r in range(rows)])
+    assert np.array_equal(got, a[h:h + ni, h:h + nj, :].reshape(ni, -1))
