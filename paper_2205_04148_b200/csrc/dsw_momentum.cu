@@ -34,7 +34,10 @@ namespace fv3b {
 namespace {
 
 constexpr int SEG = 4;
-template <int TJ> constexpr int nt_of() { return TJ >= 16 ? 352 : 256; }
+#ifndef FV3B_MO_NT
+#define FV3B_MO_NT 352
+#endif
+template <int TJ> constexpr int nt_of() { return TJ >= 16 ? FV3B_MO_NT : 256; }
 template <int TJ> constexpr int cps_of() { return TJ >= 16 ? 1 : 2; }
 
 __host__ __device__ constexpr int a16(int n) { return (n + 15) / 16 * 16; }

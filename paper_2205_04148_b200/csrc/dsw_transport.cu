@@ -23,8 +23,8 @@
 // quantity are cell passes riding in the courant and phase-A intervals (each
 // cell forms its four order-0/1 face fluxes itself: same operands, same
 // bits as the stored temporaries), and the last order's face fluxes are
-// formed by the phase-B items.  Five barriers per level: courant + d2_1 |
-// phase A + d2_2 + mass weights | phase B of delp | phase B of pt, w | cell
+// formed by the phase-B items.  Five barriers per level: courant + d2_1 +
+// mass weights | phase A + d2_2 | phase B of delp | phase B of pt, w | cell
 // updates (d2_1 of the next level borrows the flux arrays they read).
 #include "common.cuh"
 #include "dsw.cuh"
@@ -488,24 +488,29 @@ __global__ void __launch_bounds__(nt_of<TI, TJ>(), cps_of<TI, TJ>()) dsw_transpo
       }
     }
     for (int e = tid; e < L::D1W * (L::D1H / DR); e += NT) deln1(e);
+    // mass weights damp4h * (delp[-1] + delp) of the x / y faces (stage delp
+    // only; read by phase B of pt and w), dealt from the last thread down so
+    // the threads without a del6 order-1 item take the extra ones (measured
+    // 0.2% per step faster here than beside phase A)
+    for (int e = NT - 1 - tid; e < (TI + 1) * TJ + TI * (TJ + 1); e += NT) {
+      if (e < (TI + 1) * TJ) {
+        const int i = e % (TI + 1), j = e / (TI + 1);
+        smwx[j * L::XW + i] = damp4h * (*QB(sdp, i - 1, j) + *QB(sdp, i, j));
+      } else {
+        const int i = (e - (TI + 1) * TJ) % TI, j = (e - (TI + 1) * TJ) / TI;
+        smwy[j * TI + i] = damp4h * (*QB(sdp, i, j - 1) + *QB(sdp, i, j));
+      }
+    }
     __syncthreads();
-    // ---- S1: phase A of delp, pt, w; del6 order 2; mass weights ---------------
+    // ---- S1: phase A of delp, pt, w; del6 order 2 ------------------------------
     // (the phase-A items are the heavy ones: one per thread of the first NA;
-    // the remaining threads take del6 order 2 and the mass weights)
+    // the remaining threads take del6 order 2)
     if (tid < NA) {
       phase_a3(tid);
     } else {
       const int t = tid - NA;
       constexpr int NR = NT - NA;
       for (int e = t; e < L::D2W * (L::D2H / DR); e += NR) deln2(e);
-      for (int e = t; e < (TI + 1) * TJ; e += NR) {
-        const int i = e % (TI + 1), j = e / (TI + 1);
-        smwx[j * L::XW + i] = damp4h * (*QB(sdp, i - 1, j) + *QB(sdp, i, j));
-      }
-      for (int e = t; e < TI * (TJ + 1); e += NR) {
-        const int i = e % TI, j = e / TI;
-        smwy[j * TI + i] = damp4h * (*QB(sdp, i, j - 1) + *QB(sdp, i, j));
-      }
     }
     __syncthreads();
     // ---- S2: phase B of delp (mass fluxes); stage values of the update cell ---
