@@ -9,16 +9,16 @@
 //       kinetic-energy upwind values ub*uu (xppm of u with cub) and vb*vv
 //       (yppm of v with cvb) at cell corners, and the Smagorinsky-scaled
 //       divergence damping ddv at corners;
-//   S2  phase B of fv_tp_2d(wk) -> fxv (smem), fyv (y-thread registers) and
-//       ked = 0.5 * (ub*uu + vb*vv);
-//   S3  (during the next level's S0) the u / v updates of the y-threads'
-//       cells.
+//   S2  phase B of fv_tp_2d(wk) -> fxv, fyv (smem; fyv in place of the
+//       phase-A y fluxes) and ked = 0.5 * (ub*uu + vb*vv);
+//   S3  (during the next level's S0, before its stage wait) the u / v
+//       updates, every thread a share of the tile's cells.
 //
 // The vorticity flux carries its del6 damping (templates.delnflux on wk with
 // dampv, nord = 2): order 1 of the Laplacian chain (d2_v1, each cell forming
 // its four order-0 face fluxes from dampv * wk) runs in S1, order 2 (d2_v2)
-// in S2, and the y-threads add the last order's face fluxes to fxv / fyv in
-// their u / v updates.
+// in S2, and the u / v updates add the last order's face fluxes to fxv /
+// fyv.
 //
 // Every statement keeps the .stn operand order and association (ked is
 // 0.5 * (ub*uu + vb*vv) with both products rounded as in the interpreter),
@@ -175,26 +175,26 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
   const bool yth = tid >= NX2 && tid < NX2 + NY2;
   const int ci2 = yth ? (tid - NX2) % TI : 0;
   const int jb2 = yth ? ((tid - NX2) / TI) * SEG : 0;
-  const int gi2 = gi0 + ci2;
   double fy[SEG + 1];
   int pend_k = -1;
   const int64_t sj = a.sj, sk = a.sk;
 
-  // u / v updates of the previous level (y threads)
+  // u / v updates of the previous level, every thread a share of the tile's
+  // cells (the weighted y fluxes wait in sfy2, which the next phase A rewrites)
+  const double* sfyv = sfy2;
   auto write_pending = [&]() {
-    if (!yth || pend_k < 0) return;
+    if (pend_k < 0) return;
     const double* st = smem + L::o_stage + ((pend_k - k0) & 1) * L::n_stage;
     const double* U = st;
     const double* V = st + L::n_q1;
-#pragma unroll
-    for (int u = 0; u < SEG; ++u) {
-      const int i = ci2, j = jb2 + u, gj = gj0 + j;
-      if (gi2 < a.ni && gj < a.nj) {
-        const int64_t off = gi2 + gj * sj + (int64_t)pend_k * sk;
+    for (int e = tid; e < TI * TJ; e += blockDim.x) {
+      const int i = e % TI, j = e / TI, gi = gi0 + i, gj = gj0 + j;
+      if (gi < a.ni && gj < a.nj) {
+        const int64_t off = gi + gj * sj + (int64_t)pend_k * sk;
         const double rdx = *QB(srdx, i, j), rdy = *QB(srdy, i, j);
         const int64_t m = i + j * sj;
         // fyv / fxv + their del6 increments dfy_v2 / dfx_v2
-        const double fyv = fy[u] + __ldg(gd6u + m) * (*D2(i, j) - *D2(i, j - 1));
+        const double fyv = sfyv[j * TI + i] + __ldg(gd6u + m) * (*D2(i, j) - *D2(i, j - 1));
         const double fxv = sfx[j * L::XW + i] + __ldg(gd6v + m) * (*D2(i, j) - *D2(i - 1, j));
         a.uo[off] = (*QB(U, i, j) * *QB(sdx, i, j) + *CN(sked, i, j) - *CN(sked, i + 1, j) + fyv) * rdx +
                     (*CN(sddv, i + 1, j) - *CN(sddv, i, j)) * rdx;
@@ -378,12 +378,13 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
       }
     } else if (yth) {
       ppm_line<SEG + 1>(sqj + (jb2 + 3) * L::JW + ci2, L::JW, CY(scry, ci2, jb2), L::YW, p1, p2, fy);
+      // the weighted fluxes of this thread's own faces jb2 .. jb2+SEG-1 (face
+      // jb2+SEG belongs to the next segment's thread), in place of fy2
 #pragma unroll
-      for (int u = 0; u < SEG + 1; ++u) {
+      for (int u = 0; u < SEG; ++u) {
         const int j = jb2 + u;
-        fy[u] = 0.5 * (fy[u] + sfy2[j * TI + ci2]) * *CY(syfx, ci2, j);
+        sfy2[j * TI + ci2] = 0.5 * (fy[u] + sfy2[j * TI + ci2]) * *CY(syfx, ci2, j);
       }
-      pend_k = k;
     } else {
       // ked = 0.5 * (ub*uu + vb*vv) over corners [0, TI+1) x [0, TJ+1)
       for (int e = tid - NX2 - NY2; e < (TI + 1) * (TJ + 1); e += blockDim.x - NX2 - NY2) {
@@ -391,6 +392,7 @@ __global__ void __launch_bounds__(nt_of<TJ>(), cps_of<TJ>()) dsw_momentum_kernel
         *CN(sked, i, j) = 0.5 * (*CN(sked, i, j) + *CN(svv, i, j));
       }
     }
+    pend_k = k;
     // d2_v2 = div(dfx_v1, dfy_v1) * rarea, dfx_v1 = del6_v * (d2_v1 - d2_v1[-1,0])
     for (int e = tid; e < L::D2W * L::D2H; e += blockDim.x) {
       const int i = e % L::D2W - 1, j = e / L::D2W - 1;
