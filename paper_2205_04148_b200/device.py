@@ -133,17 +133,22 @@ class Grid:
         return sl
 
     def put(self, t: torch.Tensor, host: np.ndarray, dims, halo_lo) -> None:
-        """Copy a reference-convention host array into device tensor ``t``
-        (3-D: one contiguous upload, then the layout change on the device by
-        fv3b_transpose)."""
+        """Copy a reference-convention host array into tensor ``t`` (on the
+        device: one contiguous upload, then the layout change by
+        fv3b_transpose; a host-side grid of the CPU tests copies directly)."""
         sl = self._window(dims, halo_lo, host.shape)
         src = torch.from_numpy(np.ascontiguousarray(host, dtype=np.float64))
+        dev = t.is_cuda and src.numel() > 0
         if tuple(dims) == ("I", "J", "K"):
-            if src.numel():
+            if dev:
                 transpose(src.to(t.device), t[sl["K"], sl["J"], sl["I"]].permute(2, 1, 0))
+            else:
+                t[sl["K"], sl["J"], sl["I"]].copy_(src.permute(2, 1, 0))
         elif tuple(dims) == ("I", "J"):  # (as an (I, J, 1) field)
-            if src.numel():
+            if dev:
                 transpose(src.to(t.device).unsqueeze(2), t[sl["J"], sl["I"]].permute(1, 0).unsqueeze(2))
+            else:
+                t[sl["J"], sl["I"]].copy_(src.permute(1, 0))
         elif tuple(dims) == ("K",):
             t[sl["K"]].copy_(src)
         else:
@@ -153,13 +158,15 @@ class Grid:
         """Reference-convention host copy of a window of device tensor ``t``."""
         sl = self._window(dims, halo_lo, shape)
         if tuple(dims) == ("I", "J", "K"):
-            v = torch.empty(tuple(shape), dtype=torch.float64, device=t.device)
-            if v.numel():
-                transpose(t[sl["K"], sl["J"], sl["I"]].permute(2, 1, 0), v)
+            v = t[sl["K"], sl["J"], sl["I"]].permute(2, 1, 0)
+            if t.is_cuda and v.numel():
+                v, w = torch.empty(tuple(shape), dtype=torch.float64, device=t.device), v
+                transpose(w, v)
         elif tuple(dims) == ("I", "J"):
-            v = torch.empty(tuple(shape), dtype=torch.float64, device=t.device)
-            if v.numel():
-                transpose(t[sl["J"], sl["I"]].permute(1, 0).unsqueeze(2), v.unsqueeze(2))
+            v = t[sl["J"], sl["I"]].permute(1, 0)
+            if t.is_cuda and v.numel():
+                v, w = torch.empty(tuple(shape), dtype=torch.float64, device=t.device), v
+                transpose(w.unsqueeze(2), v.unsqueeze(2))
         elif tuple(dims) == ("K",):
             v = t[sl["K"]]
         else:
