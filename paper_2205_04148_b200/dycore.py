@@ -434,19 +434,16 @@ class Dycore:
         self.launch("tracer_2d", "fv3b_tracer_2d", fields, [c["ppm_p1"], c["ppm_p2"]], self.dom_layers)
         self.swap(*qs)
 
-    def remap(self) -> None:
+    def remap(self, thickness: bool = True) -> None:
         """remap_profile of every remapped field: the tracers, pt and w at
         delp (the remap_tracers program, and the remap_profile program per
         field), and the D-grid winds at the layer thickness of their points
         (fv3b_face_thickness; delp's halo is refreshed at the tracer halo
-        point).  One launch per kernel, the field groups sharing it."""
-        self.launch("remap_faces", "fv3b_face_thickness", [self.f("delp"), self.s("du"), self.s("dv")], [],
-                    self.dom_layers)
-        if self.cfg.pt_logp:  # pt is profiled at the log-pressure thickness
-            coord = [self.grid.abi(self.coord[n], rank=1) for n in ("ak", "bk")]
-            self.launch("remap_logp", "fv3b_log_thickness",
-                        [self.f("delp")] + coord + [self.s(n) for n in ("dlnp", "lnpe1", "lnpe2")], [],
-                        self.dom_layers)
+        point).  One launch per kernel, the field groups sharing it.
+        ``thickness=False``: the thicknesses were launched already
+        (remap_thickness)."""
+        if thickness:
+            self.remap_thickness()
         fields, counts = [], []
         for thick, names in self._remap_groups():
             counts.append(float(len(names)))
@@ -454,6 +451,38 @@ class Dycore:
             for q in names:
                 fields += [self.f(q), self.f(f"{q}_a2"), self.f(f"{q}_a3"), self.f(f"{q}_a4")]
         self.launch("remap_tracers", "fv3b_remap_profile", fields, counts, self.dom_ifaces)
+
+    def remap_thickness(self) -> None:
+        """The remapping's layer thicknesses: the D-grid winds' at their
+        points (fv3b_face_thickness) and pt's log-pressure interfaces
+        (fv3b_log_thickness), from delp alone."""
+        self.launch("remap_faces", "fv3b_face_thickness", [self.f("delp"), self.s("du"), self.s("dv")], [],
+                    self.dom_layers)
+        if self.cfg.pt_logp:  # pt is profiled at the log-pressure thickness
+            coord = [self.grid.abi(self.coord[n], rank=1) for n in ("ak", "bk")]
+            self.launch("remap_logp", "fv3b_log_thickness",
+                        [self.f("delp")] + coord + [self.s(n) for n in ("dlnp", "lnpe1", "lnpe2")], [],
+                        self.dom_layers)
+
+    def advect_and_thickness(self) -> None:
+        """tracer_2d, with the remapping's thickness kernels on a side stream
+        beside it (they read delp only and write scratch; their few
+        registers and no shared memory fit next to tracer_2d's CTAs).  Under
+        a per-launch timer they stay in line."""
+        if self.timer is not None:
+            self.tracer_2d()
+            self.remap_thickness()
+            return
+        comp = torch.cuda.current_stream()
+        if getattr(self, "_thick_stream", None) is None:
+            self._thick_stream = torch.cuda.Stream()
+        side = self._thick_stream
+        side.wait_event(comp.record_event())
+        with torch.cuda.stream(side):
+            self.remap_thickness()
+            done = side.record_event()
+        self.tracer_2d()
+        comp.wait_event(done)
 
     def _remap_groups(self):
         """(thickness, fields) of the profile launch: the tracers and w (and
@@ -534,8 +563,8 @@ class Dycore:
         for it in range(cfg.n_split):
             yield from self.acoustic_phases(first=it == 0)
         yield cfg.tracer_names() + list(ACCUM) + ["delp"]  # (delp: the winds' remapping thickness)
-        self.tracer_2d()
-        self.remap()
+        self.advect_and_thickness()
+        self.remap(thickness=False)
         self.remap_map()
         self.moist_pk()
 
@@ -629,8 +658,8 @@ class Dycore:
             if not last:
                 dyn.append(self._start(["u", "v"]))
         self._wait(ev_trc, ev_acc)
-        self.tracer_2d()
-        self.remap()
+        self.advect_and_thickness()
+        self.remap(thickness=False)
         self.remap_map()
         self.moist_pk()
         # the exchange stream joins the compute stream (graph capture, next step)
